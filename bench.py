@@ -1,0 +1,419 @@
+"""Benchmark: Shampoo optimizer step on the ResNet-50 parameter set (BASELINE.json config 2/3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--precision double|single]
+
+One process per GPU (torchrun for N>1, NCCL).  A "step" is one full optimizer
+step over the 161 ResNet-50 parameter tensors (25.56 M variables) with
+synthetic fp32 gradients already resident in HBM: stats update, root inverse
+when t % 50 == 0, preconditioning + grafting + momentum, all-gather of the
+directions (N>1), parameter update.  Defaults W=5, K=50 put exactly one
+refresh (t=50) in the timed window, so ms_per_step is the amortised cost.
+Timing: CUDA events on the launching stream, barrier + synchronize around the
+K steps, max over ranks.  The optimizer state (factors + inverses ~2 GB) is far
+larger than L2, so no explicit flush is needed (stated in config).
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy oracle port, oracle/shampoo_oracle.py) on the host cores with every
+thread the BLAS can use, on a bounded sample (see cpu_baseline.sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Shampoo step ms (ResNet-50 params) at 1/2/4/8 B200; root-inverse ms/block"
+CFG = dict(max_preconditioner_dim=2048, precondition_frequency=50, betas=(0.0, 0.999), epsilon=1e-12,
+           momentum=0.9, use_nesterov=True, weight_decay=1e-4, use_decoupled_weight_decay=True)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+    if os.path.exists(path):
+        d = json.load(open(path))
+        p.update(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"], source="measured (MEASURED_PEAKS.json)")
+    fp64 = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(fp64):
+        p["fp64_tflops"] = json.load(open(fp64))["fp64_tflops"]
+        p["fp64_source"] = "measured (profiles/fp64_peak.json, torch DGEMM 8192^3)"
+    return p
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def resnet_shapes():
+    from paper_2309_06497_b200.model_shapes import MODEL_SHAPES
+    return [tuple(s) for s in MODEL_SHAPES["resnet50"]]
+
+
+# ---------------------------------------------------------------- reference (CPU) arm
+
+
+def cpu_reference(sample_plain_steps: int = 1, rootinv_budget_s: float = 8.0):
+    """Oracle (numpy float64, reference algorithm) on the full ResNet-50 set.
+
+    Sample: `sample_plain_steps` non-refresh steps over all 161 blocks (with
+    preset inverses so the full preconditioning path runs) plus eigh root
+    inverses for a stratified subset of factor sizes, scaled by sum n^3 to the
+    full refresh; amortised = plain + refresh / 50.
+    """
+    from oracle import shampoo_oracle as O
+
+    shapes = resnet_shapes()
+    rng = np.random.default_rng(0)
+    params = [(rng.standard_normal(s) * 0.05).astype(np.float32).astype(np.float64) for s in shapes]
+    grng = np.random.default_rng(1)
+    cfg = O.OracleConfig(grafting=O.GraftKind.ADAGRAD, **CFG)
+    opt = O.OracleShampoo(params, cfg)
+    opt.t = 1  # a non-refresh step; preset inverses = I so precondition runs
+    sizes = {}
+    for row in opt.states:
+        for st in row:
+            if st is not None and st.kind == "shampoo":
+                st.inverses = [np.eye(d) for d in st.shape]
+                for d in st.shape:
+                    sizes[d] = sizes.get(d, 0) + 1
+    plain = []
+    for _ in range(sample_plain_steps):
+        grads = [(grng.standard_normal(s) * 1e-2).astype(np.float32).astype(np.float64) for s in shapes]
+        t0 = time.perf_counter()
+        opt.step(grads)
+        plain.append(time.perf_counter() - t0)
+        opt.t = 1
+    # refresh: time eigh root inverses per distinct size (small counts), scale by multiplicity
+    refresh_s, measured_n3, total_n3 = 0.0, 0.0, sum(c * d ** 3 for d, c in sizes.items())
+    spent = 0.0
+    per_size = {}
+    for d in sorted(sizes, reverse=True):
+        g = rng.standard_normal((d, 64))
+        a = g @ g.T / 64 + 1e-3 * np.eye(d)
+        t0 = time.perf_counter()
+        O.root_inverse_eigh(a, 4, eps=1e-12)
+        dt = time.perf_counter() - t0
+        per_size[d] = dt
+        spent += dt
+        if spent > rootinv_budget_s:
+            break
+    for d, c in sizes.items():
+        if d in per_size:
+            refresh_s += c * per_size[d]
+            measured_n3 += c * d ** 3
+    refresh_s *= total_n3 / max(measured_n3, 1.0)
+    plain_ms = 1e3 * float(np.median(plain))
+    amort_ms = plain_ms + 1e3 * refresh_s / 50.0
+    return {"plain_ms": plain_ms, "refresh_extra_ms": 1e3 * refresh_s, "amortized_ms": amort_ms,
+            "cores": os.cpu_count(),
+            "sample": (f"{sample_plain_steps} plain step(s) over all 161 ResNet-50 blocks + eigh root inverses "
+                       f"of {len(per_size)}/{len(sizes)} distinct factor sizes scaled by sum n^3 to the full "
+                       f"refresh; amortised over f=50")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    r = cpu_reference(sample_plain_steps=max(1, min(args.steps, 2)))
+    line = {"metric": METRIC, "value": round(r["amortized_ms"], 3), "unit": "ms", "impl": "reference",
+            "n_gpus": args.gpus, "steps": max(1, min(args.steps, 2)), "warmup": 0,
+            "ms_per_step": round(r["amortized_ms"], 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "resnet50_shampoo_step", "params": 25557032, "blocks": 161,
+                       "max_preconditioner_dim": 2048, "precondition_frequency": 50, "grafting": "adagrad",
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": round(r["amortized_ms"], 3), "unit": "ms", "cores": r["cores"],
+                             "kind": "port", "sample": r["sample"], "plain_ms": round(r["plain_ms"], 1),
+                             "refresh_ms": round(r["refresh_extra_ms"], 1)},
+            "e2e": {"value": round(r["amortized_ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def measure_fp64_peak(torch):
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e9
+    for _ in range(5):
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_06497_b200 as P
+    from paper_2309_06497_b200 import _native as N
+    from paper_2309_06497_b200.distributed import GroupExchange
+    import ctypes as C
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    shapes = resnet_shapes()
+    n_params = sum(math.prod(s) for s in shapes)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    params = [torch.randn(s, generator=gen, device=dev) * 0.05 for s in shapes]
+    pool = []
+    gen.manual_seed(1 + rank * 0)  # identical gradients on every rank (no DDP all-reduce modelled)
+    for _ in range(4):
+        pool.append([torch.randn(s, generator=gen, device=dev) * 1e-2 for s in shapes])
+    cfg = P.ShampooConfig(grafting=P.GraftKind.ADAGRAD, precision=args.precision, **CFG)
+    exchange = GroupExchange(world) if world > 1 else None
+    opt = P.Shampoo(params, cfg, world_size=world, group_size=world, rank=rank, exchange=exchange)
+    lib = N.lib()
+    stream = torch.cuda.current_stream(dev)
+
+    sf, pf, n3 = C.c_double(), C.c_double(), C.c_double()
+    lib.shampoo_work(opt._ctx, C.byref(sf), C.byref(pf), C.byref(n3))
+
+    # warm-up (includes the t=0 refresh)
+    for w in range(args.warmup):
+        opt.step(pool[w % 4])
+    torch.cuda.synchronize()
+    lib.shampoo_timing_enable(opt._ctx, 1)
+    lib.shampoo_timing_get(opt._ctx, None, None)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gather_events = []
+    refresh_steps = 0
+    if exchange is not None:
+        def timed_exchange(buf, gr, mp):
+            ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ga.record(stream)
+            exchange(buf, gr, mp)
+            gb.record(stream)
+            gather_events.append((ga, gb))
+
+        opt.exchange = timed_exchange
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for k in range(args.steps):
+            t = opt.step_count
+            if t >= cfg.start_preconditioning_step and t % cfg.precondition_frequency == 0:
+                refresh_steps += 1
+            opt.step(pool[k % 4])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    opt.exchange = exchange
+    gather_ms = sum(a.elapsed_time(b) for a, b in gather_events)
+    total_ms = ev0.elapsed_time(ev1)
+    launches = P.launch_count() - launches0
+    ms = (C.c_double * 5)()
+    cnt = (C.c_int64 * 5)()
+    lib.shampoo_timing_get(opt._ctx, ms, cnt)
+    lib.shampoo_timing_enable(opt._ctx, 0)
+    phase_ms = {k: ms[i] / args.steps for i, k in enumerate(
+        ["stats", "root_inverse", "precondition", "graft_momentum", "apply"])}
+    phase_ms["allgather"] = gather_ms / args.steps
+    # max over ranks
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+
+    # kernel-level roofline: the plain-step GEMM phases (tensor/FP64 pipe) and the elementwise phases (HBM)
+    pk = peaks()
+    if "fp64_tflops" not in pk and args.precision == "double":
+        pk["fp64_tflops"] = measure_fp64_peak(torch)
+        pk["fp64_source"] = "measured in this run (torch DGEMM 8192^3, best of 5)"
+    plain_steps = args.steps - refresh_steps
+    stats_ms = ms[0] / max(cnt[0], 1)
+    prec_ms = ms[2] / max(cnt[2], 1)
+    rinv_ms = ms[1] / max(cnt[1], 1) if cnt[1] else None
+    candidates = {"stats": stats_ms, "precondition": prec_ms,
+                  "root_inverse_amortized": (ms[1] / args.steps)}
+    dominant = max(candidates, key=candidates.get)
+    if args.precision == "double":
+        peak, unit, bound = pk["fp64_tflops"], "TFLOP/s", "fp64"
+    else:
+        peak, unit, bound = pk["bf16_tflops"], "TFLOP/s", "tensor"
+    if dominant == "stats":
+        achieved = sf.value / (stats_ms * 1e-3) / 1e12
+    elif dominant == "precondition":
+        achieved = pf.value / (prec_ms * 1e-3) / 1e12
+    else:
+        # Jacobi eigensolver: useful work is ~9 n^3 flops per factor (tridiagonal-equivalent eigh count)
+        achieved = 9.0 * n3.value / ((rinv_ms or 1e9) * 1e-3) / 1e12
+    roofline = {"bound": bound, "kernel": dominant, "achieved": round(achieved, 3), "peak": round(peak, 2),
+                "unit": unit, "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": pk.get("fp64_source") if args.precision == "double" else pk["source"],
+                "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+                "stats_ms_per_launch": round(stats_ms, 4), "precondition_ms_per_launch": round(prec_ms, 4),
+                "root_inverse_ms_per_refresh": round(rinv_ms, 2) if rinv_ms else None,
+                "stats_gflop": round(sf.value / 1e9, 2), "precondition_gflop": round(pf.value / 1e9, 2),
+                "sum_n3_G": round(n3.value / 1e9, 2)}
+
+    # e2e through the public API with host buffers: pinned H2D of grads, step, D2H of params
+    e2e = None
+    if not args.skip_e2e:
+        host_grads = [[g.cpu().pin_memory() for g in pool[i]] for i in range(2)]
+        host_params = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
+        dev_grads = [torch.empty_like(p) for p in params]
+        e2e_steps = min(args.steps, 10)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(e2e_steps):
+            for d, h in zip(dev_grads, host_grads[k % 2]):
+                d.copy_(h, non_blocking=True)
+            opt.step(dev_grads)
+            for h, p in zip(host_params, opt.params()):
+                h.copy_(p, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": 4 * n_params,
+               "d2h_bytes_per_step": 4 * n_params, "steps": e2e_steps,
+               "note": "plain steps (no refresh in window) + pinned H2D grads + D2H params"}
+
+    # Adam baseline on the same shapes
+    adam_ms = None
+    if not args.skip_adam:
+        ap = [p.clone().requires_grad_(True) for p in params]
+        for p, g in zip(ap, pool[0]):
+            p.grad = g.clone()
+        adam = torch.optim.Adam(ap, lr=1e-3, fused=True)
+        for _ in range(3):
+            adam.step()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(20):
+            adam.step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        adam_ms = a0.elapsed_time(a1) / 20
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+        r = cpu_reference(1)
+        cpu = {"value": round(r["amortized_ms"], 2), "unit": "ms", "cores": r["cores"], "kind": "port",
+               "sample": r["sample"], "plain_ms": round(r["plain_ms"], 1),
+               "refresh_ms": round(r["refresh_extra_ms"], 1)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(ms_per_step, 4), "unit": "ms", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64" if args.precision == "double" else "f32", "data": "synthetic",
+                "config": {"workload": "resnet50_shampoo_step", "params": n_params, "blocks": 161,
+                           "max_preconditioner_dim": 2048, "precondition_frequency": 50,
+                           "grafting": "adagrad", "momentum": "nesterov 0.9", "precision": args.precision,
+                           "epsilon": 1e-12, "refresh_steps_in_window": refresh_steps,
+                           "parallelism": f"dp{world} (block-sharded, all-gather)",
+                           "l2": "state (factors+inverses ~2 GB) >> 126 MB L2; no flush needed"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary(), "adam_fused_ms": round(adam_ms, 4) if adam_ms else None,
+                "device_state_gb": round(opt.device_bytes / 1e9, 3)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["double", "single"], default="double")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-adam", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

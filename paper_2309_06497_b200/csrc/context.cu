@@ -1,0 +1,736 @@
+// Optimizer context and the C ABI entry points (include/shampoo_b200.h).
+//
+// A context owns the device state of the blocks assigned to one rank
+// (optim.py:205-210 "owned" restriction), laid out in one HBM arena:
+//   per-element arrays in owned-block order (G, g_eff, filter, graft acc,
+//   momentum, P_sh, two mode-chain temporaries), Kronecker factors and their
+//   inverses (sum_k d_k^2 per block), the group gather buffer
+//   (group_size x max_payload scalars, dist.py:179-183) and solver workspaces.
+// Each step phase is a handful of grouped launches over device-side block and
+// chunk tables, independent of the number of blocks.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "elementwise.cuh"
+#include "gemm.cuh"
+#include "rootinv.cuh"
+
+namespace shampoo {
+
+int64_t g_launches = 0;
+
+namespace {
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct EngineBase {
+  virtual ~EngineBase() = default;
+};
+
+template <typename T>
+struct Engine : EngineBase {
+  GemmBatch<T> stats;                  // factor EMA updates, all owned blocks x modes
+  GemmBatch<T> prec[kMaxOrder];        // mode-k products, k = 0..order-1 (order >= 2)
+  GemvBatch<T> prec1;                  // order-1 blocks: P = X g
+};
+
+// Event pairs per phase; elapsed times are collected lazily in shampoo_timing_get.
+struct PhaseTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[SHAMPOO_NUM_PHASES];
+  std::vector<cudaEvent_t> pool;
+  double ms[SHAMPOO_NUM_PHASES] = {0, 0, 0, 0, 0};
+  int64_t count[SHAMPOO_NUM_PHASES] = {0, 0, 0, 0, 0};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  ~PhaseTimer() {
+    for (auto& v : pending)
+      for (auto& p : v) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+      }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+struct PhaseScope {
+  PhaseTimer* t;
+  int phase;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  PhaseScope(PhaseTimer* t_, int p, cudaStream_t s_) : t(t_), phase(p), s(s_) {
+    if (t->on) {
+      a = t->get();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~PhaseScope() {
+    if (t->on) {
+      cudaEvent_t b = t->get();
+      cudaEventRecord(b, s);
+      t->pending[phase].push_back({a, b});
+    }
+  }
+};
+
+}  // namespace
+}  // namespace shampoo
+
+using namespace shampoo;
+
+struct shampoo_ctx {
+  shampoo_plan plan;
+  shampoo_config cfg{};
+  int32_t rank = 0, grank = 0, device = 0;
+  bool f32 = false;
+  size_t esz = 8;
+  int32_t nparams = 0;
+  // owned blocks
+  std::vector<int32_t> owned;       // global ids, ascending
+  std::vector<int32_t> local_of;    // global id -> local or -1
+  std::vector<int64_t> vofs;        // per owned: element offset in per-element arenas
+  std::vector<int64_t> fac_off;     // per owned: element offset of factor 0 in FACT/INV
+  std::vector<int64_t> step;        // per owned: ShampooBlockState.step
+  std::vector<int64_t> last_inv;    // per owned: last_inverse_step
+  std::vector<int32_t> ready_h;     // per owned: inverse present
+  int64_t graft_step = 0;           // GraftState.step (identical for all owned blocks)
+  int64_t n_elem = 0, n_fac = 0;
+  bool any_order3 = false;
+  // arena
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  void *G = nullptr, *GE = nullptr, *FILT = nullptr, *GA = nullptr, *MOM = nullptr, *PS = nullptr;
+  void *T1 = nullptr, *T2 = nullptr, *FACT = nullptr, *INV = nullptr, *BUF = nullptr;
+  double *part = nullptr, *gnorm2 = nullptr, *pg2 = nullptr, *ps2 = nullptr;
+  int32_t* d_ready = nullptr;
+  int32_t *d_cb = nullptr, *d_cc = nullptr;
+  // tables
+  DevBlock* d_blocks = nullptr;
+  DevBlock* d_params = nullptr;
+  Chunk *d_owned_chunks = nullptr, *d_all_chunks = nullptr, *d_param_chunks = nullptr;
+  int n_owned_chunks = 0, n_all_chunks = 0, n_param_chunks = 0;
+  void** d_ptrs = nullptr;  // [grads | params]
+  int32_t* d_flag = nullptr;
+  int32_t* h_flag = nullptr;
+  std::unique_ptr<EngineBase> engine;
+  RootInverseBatch rinv;
+  std::vector<int32_t> job_block;   // root-inverse job -> owned local block
+  int64_t guard[4] = {0, 0, 0, 0};
+  PhaseTimer timer;
+
+  ~shampoo_ctx() {
+    engine.reset();
+    cudaFree(arena);
+    cudaFree(d_blocks);
+    cudaFree(d_params);
+    cudaFree(d_owned_chunks);
+    cudaFree(d_all_chunks);
+    cudaFree(d_param_chunks);
+    cudaFree(d_ptrs);
+    cudaFreeHost(h_flag);
+  }
+  template <typename T>
+  Engine<T>& eng() { return *static_cast<Engine<T>*>(engine.get()); }
+};
+
+namespace {
+
+int upload_ptrs(shampoo_ctx* c, const void* const* grads, const void* const* params, cudaStream_t s) {
+  std::vector<const void*> h(2 * c->nparams, nullptr);
+  for (int i = 0; i < c->nparams; ++i) {
+    if (grads) h[i] = grads[i];
+    if (params) h[c->nparams + i] = params[i];
+  }
+  // pageable source: staged by the driver before return, so the host vector may die
+  SH_CUDA_CHECK(cudaMemcpyAsync(c->d_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+  return SHAMPOO_OK;
+}
+
+StepScalars make_scalars(const shampoo_ctx* c, int64_t t, int32_t dtype, int64_t graft_step) {
+  const shampoo_config& k = c->cfg;
+  StepScalars sc{};
+  sc.weight_decay = k.weight_decay;
+  sc.l2 = k.weight_decay > 0.0 && !k.use_decoupled_weight_decay;
+  sc.decoupled = k.weight_decay > 0.0 && k.use_decoupled_weight_decay;
+  sc.beta1 = k.beta1;
+  sc.one_minus_beta1 = 1.0 - k.beta1;
+  sc.use_filter = k.beta1 > 0.0;
+  sc.inv_bc1 = (sc.use_filter && k.use_bias_correction) ? 1.0 / (1.0 - std::pow(k.beta1, (double)(t + 1))) : 1.0;
+  sc.graft = k.grafting;
+  sc.beta2g = k.grafting_beta2;
+  sc.one_minus_beta2g = 1.0 - k.grafting_beta2;
+  const bool debias = (k.grafting == SHAMPOO_GRAFT_ADAM || k.grafting == SHAMPOO_GRAFT_NORMALIZED_ADAM);
+  sc.inv_bc2g = (debias && k.use_bias_correction && graft_step > 0)
+                    ? 1.0 / (1.0 - std::pow(k.grafting_beta2, (double)graft_step))
+                    : 1.0;
+  sc.graft_eps = k.grafting_epsilon;
+  sc.momentum = k.momentum;
+  sc.nesterov = k.use_nesterov;
+  sc.precond = (double)t >= k.start_preconditioning_step;
+  sc.pdtype = dtype;
+  sc.lr = k.lr;
+  return sc;
+}
+
+ElemArenas arenas(shampoo_ctx* c) {
+  ElemArenas a{};
+  a.G = c->G;
+  a.GE = c->cfg.beta1 > 0.0 ? c->GE : c->G;
+  a.FILT = c->FILT;
+  a.GA = c->GA;
+  a.MOM = c->MOM;
+  a.PS = c->PS;
+  a.BUF = c->BUF;
+  a.part = c->part;
+  a.gnorm2 = c->gnorm2;
+  a.pg2 = c->pg2;
+  a.ps2 = c->ps2;
+  a.ready = c->d_ready;
+  return a;
+}
+
+template <typename T>
+int build_engine(shampoo_ctx* c) {
+  auto* e = new Engine<T>();
+  c->engine.reset(e);
+  const shampoo_config& k = c->cfg;
+  const double alpha = k.beta2 == 1.0 ? 1.0 : 1.0 - k.beta2;  // precond.py:237-241
+  const double beta = k.beta2 == 1.0 ? 1.0 : k.beta2;
+  T* G = static_cast<T*>(c->G);
+  T* GE = static_cast<T*>(k.beta1 > 0.0 ? c->GE : c->G);
+  T* FACT = static_cast<T*>(c->FACT);
+  T* INV = static_cast<T*>(c->INV);
+  T* PS = static_cast<T*>(c->PS);
+  T* tmp[2] = {static_cast<T*>(c->T1), static_cast<T*>(c->T2)};
+  for (size_t l = 0; l < c->owned.size(); ++l) {
+    const BlockPlan& b = c->plan.blocks[c->owned[l]];
+    if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
+    const std::vector<int64_t> d = b.dims();
+    const int order = b.order;
+    int64_t off = c->fac_off[l];
+    for (int m = 0; m < order; ++m) {
+      int64_t outer = 1, inner = 1;
+      for (int q = 0; q < m; ++q) outer *= d[q];
+      for (int q = m + 1; q < order; ++q) inner *= d[q];
+      e->stats.add(make_mode_gram(G + c->vofs[l], outer, d[m], inner, FACT + off, alpha, beta));
+      if (order == 1) {
+        GemvProblem gp{};
+        gp.n = (int32_t)d[0];
+        gp.mask_index = (int32_t)l;
+        gp.X = INV + off;
+        gp.x = GE + c->vofs[l];
+        gp.y = PS + c->vofs[l];
+        gp.alpha = 1.0;
+        e->prec1.add(gp);
+      } else {
+        const T* in = (m == 0) ? GE + c->vofs[l] : tmp[(m - 1) & 1] + c->vofs[l];
+        T* out = (m == order - 1) ? PS + c->vofs[l] : tmp[m & 1] + c->vofs[l];
+        GemmProblem p = make_mode_product(INV + off, in, out, outer, d[m], inner, 1.0);
+        p.flags |= kGemmMasked;
+        p.mask_index = (int32_t)l;
+        e->prec[m].add(p);
+      }
+      off += d[m] * d[m];
+    }
+  }
+  int rc = e->stats.upload();
+  if (rc) return rc;
+  for (int m = 0; m < kMaxOrder; ++m)
+    if ((rc = e->prec[m].upload())) return rc;
+  return e->prec1.upload();
+}
+
+template <typename T>
+int precondition_impl(shampoo_ctx* c, cudaStream_t s) {
+  Engine<T>& e = c->eng<T>();
+  int rc;
+  if ((rc = e.prec1.launch(s, c->d_ready))) return rc;
+  for (int m = 0; m < kMaxOrder; ++m)
+    if ((rc = e.prec[m].launch(s, c->d_ready))) return rc;
+  if ((rc = launch_sumsq<T>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, c->PS, c->part, s))) return rc;
+  return launch_block_reduce(c->d_cb, c->d_cc, (int)c->owned.size(), c->part, c->ps2, s);
+}
+
+int check_cfg(const shampoo_config* k) {
+  // optim.py:86-126 validation (host mirror also validates; this guards the C ABI)
+  auto bad = [](const char* m) {
+    set_error(m);
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  };
+  if (!(k->beta1 >= 0.0 && k->beta1 < 1.0)) return bad("betas[0] must lie in [0, 1)");
+  if (!(k->beta2 > 0.0 && k->beta2 <= 1.0)) return bad("betas[1] must lie in (0, 1]");
+  if (!(k->grafting_beta2 > 0.0 && k->grafting_beta2 <= 1.0)) return bad("grafting_beta2 must lie in (0, 1]");
+  if (!(k->lr > 0.0)) return bad("lr must be positive");
+  if (k->epsilon < 0.0) return bad("epsilon must be non-negative");
+  if (k->momentum < 0.0 || k->momentum >= 1.0) return bad("momentum must lie in [0, 1)");
+  if (k->weight_decay < 0.0) return bad("weight_decay must be non-negative");
+  if (k->max_preconditioner_dim < 1) return bad("max_preconditioner_dim must be at least 1");
+  if (k->precondition_frequency < 1) return bad("precondition_frequency must be at least 1");
+  if (k->start_preconditioning_step < 0) return bad("start_preconditioning_step must be non-negative");
+  if (k->exponent_override < 0) return bad("exponent_override must be a non-negative integer");
+  if (!(k->exponent_multiplier > 0.0)) return bad("exponent_multiplier must be positive");
+  if (!(k->grafting_epsilon > 0.0)) return bad("grafting_epsilon must be positive");
+  if (k->grafting < 0 || k->grafting > 6) return bad("unknown grafting kind");
+  if (k->solver == SHAMPOO_SOLVER_NEWTON && k->exponent_multiplier != 1.0)
+    return bad("the coupled Newton solver supports exponent_multiplier=1 only");
+  return SHAMPOO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* shampoo_version(void) { return "paper_2309_06497_b200 0.1 (sm_100a)"; }
+int64_t shampoo_launch_count(void) { return g_launches; }
+
+int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int32_t rank, int32_t device,
+                       shampoo_ctx** out) {
+  *out = nullptr;
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (rank < 0 || rank >= plan->world) {
+    set_error("rank out of range");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  SH_CUDA_CHECK(cudaSetDevice(device));
+  std::unique_ptr<shampoo_ctx> c(new shampoo_ctx());
+  c->plan = *plan;
+  c->cfg = *cfg;
+  c->rank = rank;
+  c->grank = rank % plan->group;
+  c->device = device;
+  c->f32 = cfg->precision == SHAMPOO_PRECISION_SINGLE;
+  c->esz = c->f32 ? 4 : 8;
+  c->nparams = (int32_t)plan->params.size();
+  const int nb = (int)plan->blocks.size();
+  c->local_of.assign(nb, -1);
+  for (int i = 0; i < nb; ++i) {
+    const BlockPlan& b = plan->blocks[i];
+    if (b.owner != c->grank) continue;
+    if (b.kind == SHAMPOO_BLOCK_ADAGRAD || b.kind == SHAMPOO_BLOCK_DIAGONAL) {
+      set_error("large_dim_method ADAGRAD/DIAGONAL fallback blocks are not built in this release");
+      return SHAMPOO_ERR_UNSUPPORTED;
+    }
+    c->local_of[i] = (int32_t)c->owned.size();
+    c->owned.push_back(i);
+    c->vofs.push_back(c->n_elem);
+    c->n_elem += b.var_count;
+    c->fac_off.push_back(c->n_fac);
+    if (b.kind == SHAMPOO_BLOCK_SHAMPOO) {
+      for (int64_t d : b.dims()) c->n_fac += d * d;
+      if (b.order >= 3) c->any_order3 = true;
+    }
+  }
+  const size_t no = c->owned.size();
+  c->step.assign(no, 0);
+  c->last_inv.assign(no, -1);
+  c->ready_h.assign(no, 0);
+  // chunk tables
+  std::vector<Chunk> oc, ac, pc;
+  std::vector<int32_t> cb(no), cc(no);
+  for (size_t l = 0; l < no; ++l) {
+    const BlockPlan& b = plan->blocks[c->owned[l]];
+    cb[l] = (int32_t)oc.size();
+    for (int64_t s = 0; s < b.var_count; s += kChunk) oc.push_back(Chunk{b.block_id, 0, s, std::min<int64_t>(kChunk, b.var_count - s)});
+    cc[l] = (int32_t)oc.size() - cb[l];
+  }
+  for (int i = 0; i < nb; ++i) {
+    const BlockPlan& b = plan->blocks[i];
+    for (int64_t s = 0; s < b.var_count; s += kChunk) ac.push_back(Chunk{i, 0, s, std::min<int64_t>(kChunk, b.var_count - s)});
+  }
+  std::vector<DevBlock> db(nb), dp(c->nparams);
+  for (int i = 0; i < nb; ++i) {
+    const BlockPlan& b = plan->blocks[i];
+    const ParamPlan& pp = plan->params[b.param];
+    DevBlock& d = db[i];
+    std::memset(&d, 0, sizeof(d));
+    d.param = b.param;
+    d.order = b.order;
+    d.kind = b.kind;
+    d.local = c->local_of[i];
+    d.numel = b.var_count;
+    d.gofs = b.gather_offset;
+    d.vofs = d.local >= 0 ? c->vofs[d.local] : 0;
+    for (int k = 0; k < b.order; ++k) {
+      d.dims[k] = b.hi[k] - b.lo[k];
+      d.lo[k] = b.lo[k];
+      d.mstride[k] = pp.mstride[k];
+    }
+  }
+  for (int p = 0; p < c->nparams; ++p) {
+    std::memset(&dp[p], 0, sizeof(DevBlock));
+    dp[p].param = p;
+    const int64_t n = plan->params[p].numel;
+    for (int64_t s = 0; s < n; s += kChunk) pc.push_back(Chunk{p, 0, s, std::min<int64_t>(kChunk, n - s)});
+  }
+  c->n_owned_chunks = (int)oc.size();
+  c->n_all_chunks = (int)ac.size();
+  c->n_param_chunks = (int)pc.size();
+  // arena layout
+  const size_t E = (size_t)c->n_elem, es = c->esz;
+  const bool filt = cfg->beta1 > 0.0, graft = cfg->grafting != SHAMPOO_GRAFT_SGD, mom = cfg->momentum > 0.0;
+  const size_t buf_elems = (size_t)plan->group * plan->max_payload;
+  struct Sl {
+    void** p;
+    size_t bytes;
+  };
+  std::vector<Sl> slots = {
+      {&c->G, E * es},
+      {&c->GE, filt ? E * es : 0},
+      {&c->FILT, filt ? E * es : 0},
+      {&c->GA, graft ? E * es : 0},
+      {&c->MOM, mom ? E * es : 0},
+      {&c->PS, E * es},
+      {&c->T1, E * es},
+      {&c->T2, c->any_order3 ? E * es : 0},
+      {&c->FACT, (size_t)c->n_fac * es},
+      {&c->INV, (size_t)c->n_fac * es},
+      {&c->BUF, std::max<size_t>(buf_elems, 1) * es},
+      {(void**)&c->part, std::max<size_t>(oc.size(), 1) * 8},
+      {(void**)&c->gnorm2, std::max<size_t>(no, 1) * 8},
+      {(void**)&c->pg2, std::max<size_t>(no, 1) * 8},
+      {(void**)&c->ps2, std::max<size_t>(no, 1) * 8},
+      {(void**)&c->d_ready, std::max<size_t>(no, 1) * 4},
+      {(void**)&c->d_cb, std::max<size_t>(no, 1) * 4},
+      {(void**)&c->d_cc, std::max<size_t>(no, 1) * 4},
+      {(void**)&c->d_flag, 16},
+  };
+  size_t total = 0;
+  for (auto& s : slots) total += align_up(s.bytes);
+  cudaError_t err = cudaMalloc(&c->arena, total);
+  if (err != cudaSuccess) {
+    set_error(std::string("arena allocation of ") + std::to_string(total) + " bytes: " + cudaGetErrorString(err));
+    return SHAMPOO_ERR_OUT_OF_MEMORY;
+  }
+  c->arena_bytes = total;
+  SH_CUDA_CHECK(cudaMemset(c->arena, 0, total));
+  size_t at = 0;
+  for (auto& s : slots) {
+    *s.p = s.bytes ? (void*)(c->arena + at) : nullptr;
+    at += align_up(s.bytes);
+  }
+  SH_CUDA_CHECK(cudaMalloc(&c->d_blocks, std::max(nb, 1) * sizeof(DevBlock)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_params, std::max(c->nparams, 1) * sizeof(DevBlock)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_owned_chunks, std::max<size_t>(oc.size(), 1) * sizeof(Chunk)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_all_chunks, std::max<size_t>(ac.size(), 1) * sizeof(Chunk)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_param_chunks, std::max<size_t>(pc.size(), 1) * sizeof(Chunk)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_ptrs, std::max(2 * c->nparams, 1) * sizeof(void*)));
+  SH_CUDA_CHECK(cudaMallocHost(&c->h_flag, 16));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_blocks, db.data(), nb * sizeof(DevBlock), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_params, dp.data(), c->nparams * sizeof(DevBlock), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_owned_chunks, oc.data(), oc.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_all_chunks, ac.data(), ac.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_param_chunks, pc.data(), pc.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_cb, cb.data(), no * sizeof(int32_t), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(c->d_cc, cc.data(), no * sizeof(int32_t), cudaMemcpyHostToDevice));
+  rc = c->f32 ? build_engine<float>(c.get()) : build_engine<double>(c.get());
+  if (rc) return rc;
+  // root-inverse jobs: every (owned shampoo block, mode)
+  std::vector<int32_t> jn, jp;
+  for (size_t l = 0; l < no; ++l) {
+    const BlockPlan& b = plan->blocks[c->owned[l]];
+    if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
+    const int p = cfg->exponent_override ? cfg->exponent_override : 2 * b.order;  // precond.py:217
+    for (int64_t d : b.dims()) {
+      jn.push_back((int32_t)d);
+      jp.push_back(p);
+      c->job_block.push_back((int32_t)l);
+    }
+  }
+  if ((rc = c->rinv.setup(jn, jp))) return rc;
+  size_t j = 0;
+  for (size_t l = 0; l < no; ++l) {
+    const BlockPlan& b = plan->blocks[c->owned[l]];
+    if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
+    int64_t off = c->fac_off[l];
+    for (int64_t d : b.dims()) {
+      char* f = static_cast<char*>(c->FACT) + off * c->esz;
+      char* x = static_cast<char*>(c->INV) + off * c->esz;
+      c->rinv.set_io((int)j++, f, c->f32, x, c->f32);
+      off += d * d;
+    }
+  }
+  SH_CUDA_CHECK(cudaDeviceSynchronize());
+  *out = c.release();
+  return SHAMPOO_OK;
+}
+
+void shampoo_ctx_destroy(shampoo_ctx* ctx) { delete ctx; }
+
+int64_t shampoo_ctx_device_bytes(const shampoo_ctx* ctx) { return (int64_t)ctx->arena_bytes; }
+
+int shampoo_check_finite(shampoo_ctx* c, const void* const* grads, int32_t dtype, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = upload_ptrs(c, grads, nullptr, s);
+  if (rc) return rc;
+  SH_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), s));
+  if ((rc = launch_finite<double>(c->d_param_chunks, c->n_param_chunks, c->d_params,
+                                  (const void* const*)c->d_ptrs, dtype, c->d_flag, s)))
+    return rc;
+  SH_CUDA_CHECK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SH_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (c->h_flag[0]) {
+    set_error("gradient contains non-finite entries; step aborted");
+    return SHAMPOO_ERR_NONFINITE_GRAD;
+  }
+  return SHAMPOO_OK;
+}
+
+int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* const* params, int32_t dtype,
+                         int64_t t, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = upload_ptrs(c, grads, params, s);
+  if (rc) return rc;
+  const int64_t gstep = c->graft_step + 1;  // GraftState.update increments first (grafting.py:71)
+  const StepScalars sc = make_scalars(c, t, dtype, gstep);
+  ElemArenas ar = arenas(c);
+  const void* const* gp = (const void* const*)c->d_ptrs;
+  const void* const* pp = (const void* const*)(c->d_ptrs + c->nparams);
+  const int no = (int)c->owned.size();
+  const bool normalized = c->cfg.grafting >= SHAMPOO_GRAFT_NORMALIZED_ADAGRAD;
+  PhaseScope scope(&c->timer, 0, s);
+  if (normalized) {
+    rc = c->f32 ? launch_prepare<float>(0, c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gp, pp, sc, ar, s)
+                : launch_prepare<double>(0, c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gp, pp, sc, ar, s);
+    if (rc) return rc;
+    if ((rc = launch_block_reduce(c->d_cb, c->d_cc, no, c->part, c->gnorm2, s))) return rc;
+  }
+  rc = c->f32 ? launch_prepare<float>(1, c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gp, pp, sc, ar, s)
+              : launch_prepare<double>(1, c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gp, pp, sc, ar, s);
+  if (rc) return rc;
+  if ((rc = launch_block_reduce(c->d_cb, c->d_cc, no, c->part, c->pg2, s))) return rc;
+  rc = c->f32 ? c->eng<float>().stats.launch(s) : c->eng<double>().stats.launch(s);
+  if (rc) return rc;
+  c->graft_step = gstep;
+  for (size_t l = 0; l < c->owned.size(); ++l)
+    if (c->plan.blocks[c->owned[l]].kind == SHAMPOO_BLOCK_SHAMPOO) ++c->step[l];
+  return SHAMPOO_OK;
+}
+
+int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (refreshed) *refreshed = 0;
+  const shampoo_config& k = c->cfg;
+  if ((double)t < k.start_preconditioning_step || t % k.precondition_frequency != 0) return SHAMPOO_OK;
+  if (c->rinv.jobs() == 0) return SHAMPOO_OK;
+  const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
+  PhaseScope scope(&c->timer, 1, s);
+  std::vector<int32_t> has_prev(c->rinv.jobs());
+  for (size_t j = 0; j < has_prev.size(); ++j) has_prev[j] = c->ready_h[c->job_block[j]];
+  int rc = c->rinv.run(1.0 / corr, has_prev, k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance, s,
+                       c->guard, nullptr, nullptr);
+  if (rc) return rc;
+  for (size_t l = 0; l < c->owned.size(); ++l) {
+    if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_SHAMPOO) continue;
+    c->ready_h[l] = 1;
+    c->last_inv[l] = t;
+  }
+  SH_CUDA_CHECK(cudaMemcpyAsync(c->d_ready, c->ready_h.data(), c->ready_h.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+  if (refreshed) *refreshed = 1;
+  return SHAMPOO_OK;
+}
+
+int shampoo_precondition_graft(shampoo_ctx* c, const void* const* params, int32_t dtype, int64_t t,
+                               void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = upload_ptrs(c, nullptr, params, s);
+  if (rc) return rc;
+  const StepScalars sc = make_scalars(c, t, dtype, c->graft_step);
+  if (sc.precond) {
+    PhaseScope scope(&c->timer, 2, s);
+    rc = c->f32 ? precondition_impl<float>(c, s) : precondition_impl<double>(c, s);
+    if (rc) return rc;
+  }
+  const void* const* pp = (const void* const*)(c->d_ptrs + c->nparams);
+  PhaseScope scope(&c->timer, 3, s);
+  return c->f32 ? launch_final<float>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, pp, sc, arenas(c), s)
+                : launch_final<double>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, pp, sc, arenas(c), s);
+}
+
+int shampoo_apply(shampoo_ctx* c, void* const* params, int32_t dtype, double lr, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = upload_ptrs(c, nullptr, (const void* const*)params, s);
+  if (rc) return rc;
+  StepScalars sc{};
+  sc.lr = lr;
+  sc.pdtype = dtype;
+  void* const* pp = (void* const*)(c->d_ptrs + c->nparams);
+  PhaseScope scope(&c->timer, 4, s);
+  return c->f32 ? launch_apply<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s)
+                : launch_apply<double>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s);
+}
+
+int shampoo_timing_enable(shampoo_ctx* c, int32_t enable) {
+  c->timer.on = enable != 0;
+  return SHAMPOO_OK;
+}
+
+int shampoo_timing_get(shampoo_ctx* c, double* ms, int64_t* counts) {
+  for (int p = 0; p < SHAMPOO_NUM_PHASES; ++p) {
+    for (auto& ev : c->timer.pending[p]) {
+      SH_CUDA_CHECK(cudaEventSynchronize(ev.second));
+      float e = 0.f;
+      SH_CUDA_CHECK(cudaEventElapsedTime(&e, ev.first, ev.second));
+      c->timer.ms[p] += e;
+      c->timer.count[p] += 1;
+      c->timer.pool.push_back(ev.first);
+      c->timer.pool.push_back(ev.second);
+    }
+    c->timer.pending[p].clear();
+    if (ms) ms[p] = c->timer.ms[p];
+    if (counts) counts[p] = c->timer.count[p];
+    c->timer.ms[p] = 0;
+    c->timer.count[p] = 0;
+  }
+  return SHAMPOO_OK;
+}
+
+int shampoo_work(shampoo_ctx* c, double* stats_flops, double* precond_flops, double* sum_n3) {
+  if (c->f32) {
+    *stats_flops = c->eng<float>().stats.flops();
+    double f = 0;
+    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<float>().prec[m].flops();
+    *precond_flops = f;
+  } else {
+    *stats_flops = c->eng<double>().stats.flops();
+    double f = 0;
+    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<double>().prec[m].flops();
+    *precond_flops = f;
+  }
+  // order-1 matvecs: 2 n^2 each
+  for (size_t l = 0; l < c->owned.size(); ++l) {
+    const BlockPlan& b = c->plan.blocks[c->owned[l]];
+    if (b.kind == SHAMPOO_BLOCK_SHAMPOO && b.order == 1) *precond_flops += 2.0 * b.var_count * b.var_count;
+  }
+  *sum_n3 = c->rinv.work_n3();
+  return SHAMPOO_OK;
+}
+
+void* shampoo_gather_buffer(shampoo_ctx* c, int64_t* scalars, int32_t* dtype) {
+  if (scalars) *scalars = (int64_t)c->plan.group * c->plan.max_payload;
+  if (dtype) *dtype = c->f32 ? SHAMPOO_DTYPE_F32 : SHAMPOO_DTYPE_F64;
+  return c->BUF;
+}
+
+int shampoo_guard_stats_get(shampoo_ctx* c, shampoo_guard_stats* out) {
+  out->primary = c->guard[0];
+  out->double_retry = c->guard[1];
+  out->fallback_previous = c->guard[2];
+  out->fallback_identity = c->guard[3];
+  return SHAMPOO_OK;
+}
+
+int shampoo_guard_stats_set(shampoo_ctx* c, const shampoo_guard_stats* in) {
+  c->guard[0] = in->primary;
+  c->guard[1] = in->double_retry;
+  c->guard[2] = in->fallback_previous;
+  c->guard[3] = in->fallback_identity;
+  return SHAMPOO_OK;
+}
+
+void* shampoo_state_view(shampoo_ctx* c, int32_t block_id, const char* name, int32_t mode, int64_t* numel,
+                         int32_t* dtype) {
+  if (block_id < 0 || block_id >= (int32_t)c->local_of.size()) return nullptr;
+  const int l = c->local_of[block_id];
+  if (l < 0) return nullptr;
+  const BlockPlan& b = c->plan.blocks[block_id];
+  if (dtype) *dtype = c->f32 ? SHAMPOO_DTYPE_F32 : SHAMPOO_DTYPE_F64;
+  const std::string n(name);
+  char* base = nullptr;
+  if (n == "factor" || n == "inv_factor") {
+    if (b.kind != SHAMPOO_BLOCK_SHAMPOO || mode < 0 || mode >= b.order) return nullptr;
+    int64_t off = c->fac_off[l];
+    const auto d = b.dims();
+    for (int m = 0; m < mode; ++m) off += d[m] * d[m];
+    if (numel) *numel = d[mode] * d[mode];
+    base = static_cast<char*>(n == "factor" ? c->FACT : c->INV);
+    return base + off * c->esz;
+  }
+  void* arr = nullptr;
+  if (n == "graft_accumulator") arr = c->GA;
+  else if (n == "filtered_grad") arr = c->FILT;
+  else if (n == "momentum") arr = c->MOM;
+  if (!arr) return nullptr;
+  if (numel) *numel = b.var_count;
+  return static_cast<char*>(arr) + c->vofs[l] * c->esz;
+}
+
+int shampoo_state_scalars_get(shampoo_ctx* c, int32_t block_id, int64_t* step, int64_t* last_inverse_step,
+                              int32_t* ready) {
+  if (block_id < 0 || block_id >= (int32_t)c->local_of.size() || c->local_of[block_id] < 0) {
+    set_error("block not owned by this context");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  const int l = c->local_of[block_id];
+  *step = c->step[l];
+  *last_inverse_step = c->last_inv[l];
+  *ready = c->ready_h[l];
+  return SHAMPOO_OK;
+}
+
+int shampoo_state_scalars_set(shampoo_ctx* c, int32_t block_id, int64_t step, int64_t last_inverse_step,
+                              int32_t ready) {
+  if (block_id < 0 || block_id >= (int32_t)c->local_of.size() || c->local_of[block_id] < 0) {
+    set_error("block not owned by this context");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  const int l = c->local_of[block_id];
+  c->step[l] = step;
+  c->last_inv[l] = last_inverse_step;
+  c->ready_h[l] = ready;
+  SH_CUDA_CHECK(cudaMemcpy(c->d_ready, c->ready_h.data(), c->ready_h.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+  return SHAMPOO_OK;
+}
+
+int shampoo_graft_step_get(shampoo_ctx* c, int64_t* step) {
+  *step = c->graft_step;
+  return SHAMPOO_OK;
+}
+
+int shampoo_graft_step_set(shampoo_ctx* c, int64_t step) {
+  c->graft_step = step;
+  return SHAMPOO_OK;
+}
+
+int shampoo_batched_root_inverse(const double* const* mats, double* const* outs, const int32_t* n, int32_t count,
+                                 int32_t root_p, double exponent_multiplier, double epsilon, int32_t solver,
+                                 double newton_tolerance, int32_t* status, int32_t* iters, void* stream) {
+  if (root_p < 1 || !(exponent_multiplier > 0.0) || epsilon < 0.0) {
+    set_error("invalid root-inverse request");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  if (solver == SHAMPOO_SOLVER_NEWTON && exponent_multiplier != 1.0) {
+    set_error("the coupled Newton solver computes plain p-th root inverses; exponent_multiplier must be 1");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RootInverseBatch rb;
+  std::vector<int32_t> nv(n, n + count), pv(count, root_p);
+  int rc = rb.setup(nv, pv);
+  if (rc) return rc;
+  for (int j = 0; j < count; ++j) rb.set_io(j, mats[j], false, outs[j], false);
+  int64_t stats[4] = {0, 0, 0, 0};
+  std::vector<int32_t> st, it;
+  rc = rb.run(1.0, {}, exponent_multiplier, epsilon, solver, newton_tolerance, s, stats, &st, &it);
+  if (rc) return rc;
+  for (int j = 0; j < count; ++j) {
+    if (status) status[j] = st[j];
+    if (iters) iters[j] = it[j];
+  }
+  return SHAMPOO_OK;
+}
+
+}  // extern "C"

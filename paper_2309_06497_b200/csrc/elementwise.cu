@@ -1,0 +1,261 @@
+// HBM-bound elementwise kernels of the step.  One CTA per Chunk (<= kChunk
+// elements of one block), block-contiguous state arrays, per-chunk partial
+// sums reduced per block in a fixed order (deterministic norms).
+//
+// Reference semantics (optim.py:278-354, grafting.py:68-110):
+//   prepare: g (+wd*w if L2) -> graft accumulator -> beta1 filter -> ||P_graft||^2
+//   final:   p = ready ? (||P_graft||/||P_sh||) P_sh : P_graft ; + wd*w ; momentum/Nesterov
+//   apply:   W -= lr * p  for every block, read back from the gather buffer
+#include "elementwise.cuh"
+
+namespace shampoo {
+
+namespace {
+
+constexpr int NT = 256;
+
+template <typename T>
+__device__ __forceinline__ T graft_dir(int32_t graft, T ge, T acc, double inv_bc2, double eps) {
+  if (graft == SHAMPOO_GRAFT_SGD) return ge;
+  return ge / (T(sqrt((double)acc * inv_bc2)) + T(eps));
+}
+
+__device__ __forceinline__ bool graft_summed(int32_t g) {
+  return g == SHAMPOO_GRAFT_ADAGRAD || g == SHAMPOO_GRAFT_NORMALIZED_ADAGRAD;
+}
+__device__ __forceinline__ bool graft_normalized(int32_t g) {
+  return g >= SHAMPOO_GRAFT_NORMALIZED_ADAGRAD;
+}
+
+__global__ void __launch_bounds__(NT) k_finite(const Chunk* __restrict__ chunks,
+                                               const DevBlock* __restrict__ params,
+                                               const void* const* __restrict__ grads, int32_t dtype,
+                                               int32_t* flag) {
+  const Chunk c = chunks[blockIdx.x];
+  const void* g = grads[params[c.block].param];
+  int bad = 0;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const double v = load_as<double>(g, c.start + e, dtype);
+    if (!isfinite(v)) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restrict__ chunks,
+                                                const DevBlock* __restrict__ blocks,
+                                                const void* const* __restrict__ grads,
+                                                const void* const* __restrict__ params, StepScalars sc,
+                                                ElemArenas ar) {
+  __shared__ double red[32];
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  T* G = static_cast<T*>(ar.G) + B.vofs;
+  T* GE = static_cast<T*>(ar.GE) + B.vofs;
+  T* F = static_cast<T*>(ar.FILT) + B.vofs;
+  T* GA = static_cast<T*>(ar.GA) + B.vofs;
+  const void* gp = grads[B.param];
+  const void* wp = params[B.param];
+  const bool normalized = graft_normalized(sc.graft);
+  double inv_norm = 1.0;
+  if (pass == 1 && normalized) {
+    const double n2 = ar.gnorm2[B.local];
+    inv_norm = n2 > 0.0 ? 1.0 / sqrt(n2) : 1.0;
+  }
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    T g;
+    if (pass == 0 || !normalized) {
+      const int64_t po = block_to_param_offset(B, j);
+      g = load_as<T>(gp, po, sc.pdtype);
+      if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
+      G[j] = g;
+    } else {
+      g = G[j];
+    }
+    if (pass == 0) {
+      acc += (double)g * (double)g;
+      continue;
+    }
+    T a = T(0);
+    if (sc.graft != SHAMPOO_GRAFT_SGD) {
+      const T gg = normalized ? T((double)g * inv_norm) : g;
+      const T sq = gg * gg;
+      a = GA[j];
+      a = graft_summed(sc.graft) ? a + sq : T(sc.beta2g) * a + T(sc.one_minus_beta2g) * sq;
+      GA[j] = a;
+    }
+    T ge = g;
+    if (sc.use_filter) {
+      const T f = T(sc.beta1) * F[j] + T(sc.one_minus_beta1) * g;
+      F[j] = f;
+      ge = f * T(sc.inv_bc1);
+      GE[j] = ge;
+    }
+    const T pg = graft_dir<T>(sc.graft, ge, a, sc.inv_bc2g, sc.graft_eps);
+    acc += (double)pg * (double)pg;
+  }
+  acc = block_sum<double, NT>(acc, red);
+  if (threadIdx.x == 0) ar.part[blockIdx.x] = acc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_sumsq(const Chunk* __restrict__ chunks,
+                                              const DevBlock* __restrict__ blocks,
+                                              const T* __restrict__ X, double* part) {
+  __shared__ double red[32];
+  const Chunk c = chunks[blockIdx.x];
+  const T* x = X + blocks[c.block].vofs + c.start;
+  double acc = 0;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) acc += (double)x[e] * (double)x[e];
+  acc = block_sum<double, NT>(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// one warp per block; fixed summation order over its chunks
+__global__ void k_block_reduce(const int32_t* __restrict__ cb, const int32_t* __restrict__ cc, int nblocks,
+                               const double* __restrict__ part, double* out) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= nblocks) return;
+  const int lane = threadIdx.x & 31;
+  double s = 0;
+  for (int i = lane; i < cc[b]; i += 32) s += part[cb[b] + i];
+  s = warp_sum(s);
+  if (lane == 0) out[b] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
+                                              const DevBlock* __restrict__ blocks,
+                                              const void* const* __restrict__ params, StepScalars sc,
+                                              ElemArenas ar) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  const T* G = static_cast<const T*>(sc.use_filter ? ar.GE : ar.G) + B.vofs;
+  const T* GA = static_cast<const T*>(ar.GA) + B.vofs;
+  const T* PS = static_cast<const T*>(ar.PS) + B.vofs;
+  T* M = static_cast<T*>(ar.MOM) + B.vofs;
+  T* out = static_cast<T*>(ar.BUF) + B.gofs;
+  const void* wp = params[B.param];
+  const bool use_ps = sc.precond && B.kind == SHAMPOO_BLOCK_SHAMPOO && ar.ready[B.local];
+  double ratio = 0.0;
+  bool ps_zero = false;
+  if (use_ps) {
+    const double n2 = ar.ps2[B.local];
+    ps_zero = (n2 == 0.0);
+    if (!ps_zero) ratio = sqrt(ar.pg2[B.local]) / sqrt(n2);  // grafting.py:95-110
+  }
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    T p;
+    if (use_ps && !ps_zero) {
+      p = T(ratio * (double)PS[j]);
+    } else {
+      const T a = sc.graft != SHAMPOO_GRAFT_SGD ? GA[j] : T(0);
+      p = graft_dir<T>(sc.graft, G[j], a, sc.inv_bc2g, sc.graft_eps);
+    }
+    if (sc.decoupled) p += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
+    if (sc.momentum > 0.0) {
+      const T m = T(sc.momentum) * M[j] + p;
+      M[j] = m;
+      p = sc.nesterov ? T(sc.momentum) * m + p : m;
+    }
+    out[j] = p;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_apply(const Chunk* __restrict__ chunks,
+                                              const DevBlock* __restrict__ blocks,
+                                              void* const* __restrict__ params,
+                                              const T* __restrict__ buf, double lr, int32_t pdtype) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  const T* p = buf + B.gofs;
+  void* wp = params[B.param];
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    const int64_t po = block_to_param_offset(B, j);
+    const double step = __dmul_rn(lr, (double)p[j]);  // W -= lr * P (optim.py:354), no FMA contraction
+    if (pdtype == SHAMPOO_DTYPE_F32) {
+      float* w = static_cast<float*>(wp);
+      w[po] = (float)__dsub_rn((double)w[po], step);
+    } else {
+      double* w = static_cast<double*>(wp);
+      w[po] = __dsub_rn(w[po], step);
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T>
+int launch_finite(const Chunk* chunks, int nchunks, const DevBlock* params, const void* const* grads,
+                  int32_t dtype, int32_t* flag, cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_finite<<<nchunks, NT, 0, s>>>(chunks, params, grads, dtype, flag);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_prepare(int pass, const Chunk* chunks, int nchunks, const DevBlock* blocks,
+                   const void* const* grads, const void* const* params, const StepScalars& sc,
+                   const ElemArenas& ar, cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_prepare<T><<<nchunks, NT, 0, s>>>(pass, chunks, blocks, grads, params, sc, ar);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_sumsq(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* X, double* part,
+                 cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_sumsq<T><<<nchunks, NT, 0, s>>>(chunks, blocks, static_cast<const T*>(X), part);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+int launch_block_reduce(const int32_t* cb, const int32_t* cc, int nblocks, const double* part, double* out,
+                        cudaStream_t s) {
+  if (!nblocks) return SHAMPOO_OK;
+  k_block_reduce<<<(nblocks + 7) / 8, 256, 0, s>>>(cb, cc, nblocks, part, out);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_final(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* params,
+                 const StepScalars& sc, const ElemArenas& ar, cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_final<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, sc, ar);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
+                 const void* buf, const StepScalars& sc, cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_apply<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const T*>(buf), sc.lr, sc.pdtype);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+#define SH_INST(T)                                                                                   \
+  template int launch_finite<T>(const Chunk*, int, const DevBlock*, const void* const*, int32_t,    \
+                                int32_t*, cudaStream_t);                                             \
+  template int launch_prepare<T>(int, const Chunk*, int, const DevBlock*, const void* const*,       \
+                                 const void* const*, const StepScalars&, const ElemArenas&,         \
+                                 cudaStream_t);                                                      \
+  template int launch_sumsq<T>(const Chunk*, int, const DevBlock*, const void*, double*, cudaStream_t); \
+  template int launch_final<T>(const Chunk*, int, const DevBlock*, const void* const*,              \
+                               const StepScalars&, const ElemArenas&, cudaStream_t);                 \
+  template int launch_apply<T>(const Chunk*, int, const DevBlock*, void* const*, const void*,        \
+                               const StepScalars&, cudaStream_t);
+SH_INST(double)
+SH_INST(float)
+
+}  // namespace shampoo

@@ -1,0 +1,61 @@
+// Elementwise / reduction kernels of the step (HBM-bound work).
+#pragma once
+
+#include "common.cuh"
+
+namespace shampoo {
+
+constexpr int kChunk = 2048;  // elements per CTA work item (256 threads x 8)
+
+// Host-computed scalars for one step (all reference semantics resolved on host).
+struct StepScalars {
+  double weight_decay;
+  double beta1, one_minus_beta1, inv_bc1;  // filter + bias correction (optim.py:308-316)
+  double beta2g, one_minus_beta2g, inv_bc2g, graft_eps;  // grafting.py:68-92
+  double momentum;
+  double lr;
+  int32_t l2;          // weight decay folded into g (optim.py:292-293)
+  int32_t decoupled;   // p += wd * w (optim.py:334-335)
+  int32_t nesterov;
+  int32_t graft;       // SHAMPOO_GRAFT_*
+  int32_t use_filter;  // beta1 > 0
+  int32_t precond;     // t >= start_preconditioning_step
+  int32_t pdtype;      // caller tensor dtype
+  int32_t pad;
+};
+
+struct ElemArenas {
+  void* G;        // raw gradient block copies (post L2)
+  void* GE;       // g_eff (== G when no filter)
+  void* FILT;     // filtered gradient state (beta1 > 0)
+  void* GA;       // graft accumulator
+  void* MOM;      // momentum
+  void* PS;       // preconditioned direction
+  void* BUF;      // gather buffer
+  double* part;   // per-chunk partial sums
+  double* gnorm2; // per owned block ||g||^2 (normalized grafting)
+  double* pg2;    // per owned block ||P_graft||^2
+  double* ps2;    // per owned block ||P_shampoo||^2
+  const int32_t* ready;  // per owned block: inverse present
+};
+
+template <typename T>
+int launch_finite(const Chunk* chunks, int nchunks, const DevBlock* params, const void* const* grads,
+                  int32_t dtype, int32_t* flag, cudaStream_t s);
+template <typename T>
+int launch_prepare(int pass, const Chunk* chunks, int nchunks, const DevBlock* blocks,
+                   const void* const* grads, const void* const* params, const StepScalars& sc,
+                   const ElemArenas& ar, cudaStream_t s);
+template <typename T>
+int launch_sumsq(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* X, double* part,
+                 cudaStream_t s);
+int launch_block_reduce(const int32_t* chunk_begin, const int32_t* chunk_count, int nblocks,
+                        const double* part, double* out, cudaStream_t s);
+template <typename T>
+int launch_final(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* params,
+                 const StepScalars& sc, const ElemArenas& ar, cudaStream_t s);
+template <typename T>
+int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
+                 const void* buf, const StepScalars& sc, cudaStream_t s);
+
+}  // namespace shampoo

@@ -1,0 +1,975 @@
+// Batched guarded root inverse (see rootinv.cuh).
+//
+// Eigen path: parallel two-sided block Jacobi in FP64.
+//   * n <= 64: one CTA solves the whole (even-padded) matrix in shared memory
+//     with cyclic Jacobi in round-robin (circle-method) pair order.
+//   * n > 64: the matrix is cut into m = np/32 row blocks; each outer round
+//     pairs blocks (circle method), one CTA per pair diagonalises its 64x64
+//     sub-problem in shared memory (same in-CTA solver), then a tiled kernel
+//     applies A <- W^T A W and V <- V W with 64x64x64 FP64 tile products.
+//     Every job runs its own round/sweep counter, so small matrices converge
+//     and drop out while large ones continue.
+// Rotation thresholds: rotate (a,b) iff |a_ab| > max(4u sqrt|a_aa||a_bb|, tol_abs),
+// tol_abs = max(0.1 u ||A||_F, 1e-9 eps); ignoring smaller couplings changes
+// X = f(A) by < 1e-9 relative (the f'(lambda) bound near the eps floor).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "rootinv.cuh"
+
+namespace shampoo {
+
+namespace {
+
+constexpr int NS = 64;            // sub-problem size (2 x 32-row blocks)
+constexpr int HB = 32;            // row-block size
+constexpr int LDS_ = NS + 1;      // padded smem leading dim
+constexpr int SLOT = NS * NS + NS + 2;  // U (64x64) + D (64) + flag
+constexpr int ECH = 4096;         // elements per chunk for elementwise job kernels
+constexpr int MAX_SWEEPS = 40;
+constexpr double U64 = 1.1102230246251565e-16;
+
+__device__ __forceinline__ int circle_pos(int r, int i, int m) {
+  return i == 0 ? 0 : 1 + (i - 1 + r) % (m - 1);
+}
+
+__device__ __forceinline__ int find_job(const int32_t* __restrict__ begin, int njobs, int x) {
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_any(const void* p, int64_t i, int f32) {
+  return f32 ? T(static_cast<const float*>(p)[i]) : T(static_cast<const double*>(p)[i]);
+}
+
+// ---------------------------------------------------------------- state / init
+
+__global__ void k_reset(RootState* st, int njobs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  RootState s{};
+  s.active = 1;
+  st[j] = s;
+}
+
+// A = scale * in (zero padded), V = I; accumulate ||A||^2 and non-finite flags.
+__global__ void __launch_bounds__(256) k_init(const RootJob* __restrict__ jobs, RootState* st,
+                                              const int32_t* __restrict__ ebegin, int njobs,
+                                              double* __restrict__ ws, double* __restrict__ vs,
+                                              double in_scale) {
+  __shared__ double red[32];
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  double s2 = 0, tr = 0;
+  int bad = 0;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    double a = 0;
+    if (i < J.n && k < J.n) {
+      a = ld_any<double>(J.in, (int64_t)i * J.n + k, J.in_f32) * in_scale;
+      if (!isfinite(a)) bad = 1;
+      s2 += a * a;
+      if (i == k) tr += a;
+    }
+    ws[J.ws_off + e] = a;
+    vs[J.v_off + e] = (i == k) ? 1.0 : 0.0;
+  }
+  s2 = block_sum<double, 256>(s2, red);
+  tr = block_sum<double, 256>(tr, red);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (s2 != 0) atomicAdd(&st[j].norm2, s2);
+    if (tr != 0) atomicAdd(&st[j].trace, tr);
+    if (bad) atomicOr(&st[j].nonfinite, 1);
+  }
+}
+
+__global__ void k_init_finish(const RootJob* __restrict__ jobs, RootState* st, int32_t* mask,
+                              int njobs, double eps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  RootState& s = st[j];
+  if (s.nonfinite || !isfinite(s.norm2)) {
+    s.status = kEigNonFiniteInput;
+    s.active = 0;
+  }
+  s.tol_abs = fmax(0.1 * U64 * sqrt(s.norm2), 1e-9 * eps);
+  if (jobs[j].n == 0) s.active = 0;
+  mask[j] = s.active;
+}
+
+// ---------------------------------------------------------------- in-CTA Jacobi
+
+// Diagonalise S (ns x ns, ld LDS_) in place, accumulating rotations into U
+// (initialised to I here).  Returns (in all threads) whether any rotation ran.
+__device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, int* sweeps_out) {
+  __shared__ double pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
+  __shared__ int pa[NS / 2], pb[NS / 2];
+  __shared__ int rot_round, rot_sweep;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < ns * ns; e += blockDim.x) {
+    const int i = e / ns, k = e % ns;
+    U[i * LDS_ + k] = (i == k) ? 1.0 : 0.0;
+  }
+  const int half = ns / 2;
+  int any = 0, sw = 0;
+  __syncthreads();
+  for (sw = 0; sw < MAX_SWEEPS; ++sw) {
+    if (tid == 0) rot_sweep = 0;
+    for (int r = 0; r < ns - 1; ++r) {
+      if (tid == 0) rot_round = 0;
+      __syncthreads();
+      if (tid < half) {
+        const int a = circle_pos(r, tid, ns), b = circle_pos(r, ns - 1 - tid, ns);
+        const double apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
+        const double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (fabs(apq) > thr) {
+          const double tau = (aqq - app) / (2.0 * apq);
+          t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          rot_round = 1;
+        }
+        pa[tid] = a;
+        pb[tid] = b;
+        pc[tid] = c;
+        ps[tid] = s;
+        pt[tid] = t;
+        papq[tid] = apq;
+        papp[tid] = app;
+        paqq[tid] = aqq;
+      }
+      __syncthreads();
+      if (rot_round) {
+        // rows: S <- J^T S
+        for (int w = tid; w < half * ns; w += blockDim.x) {
+          const int q = w / ns, col = w % ns;
+          const double s = ps[q];
+          if (s == 0.0) continue;
+          const double c = pc[q];
+          const int a = pa[q], b = pb[q];
+          const double xa = S[a * LDS_ + col], xb = S[b * LDS_ + col];
+          S[a * LDS_ + col] = c * xa - s * xb;
+          S[b * LDS_ + col] = s * xa + c * xb;
+        }
+        __syncthreads();
+        // columns: S <- S J, U <- U J
+        for (int w = tid; w < half * ns; w += blockDim.x) {
+          const int q = w % half, row = w / half;
+          const double s = ps[q];
+          if (s == 0.0) continue;
+          const double c = pc[q];
+          const int a = pa[q], b = pb[q];
+          double xa = S[row * LDS_ + a], xb = S[row * LDS_ + b];
+          S[row * LDS_ + a] = c * xa - s * xb;
+          S[row * LDS_ + b] = s * xa + c * xb;
+          xa = U[row * LDS_ + a];
+          xb = U[row * LDS_ + b];
+          U[row * LDS_ + a] = c * xa - s * xb;
+          U[row * LDS_ + b] = s * xa + c * xb;
+        }
+        __syncthreads();
+        if (tid < half && ps[tid] != 0.0) {
+          // exact 2x2 update (Golub & Van Loan, sym.schur2): b_aa = a_aa - t a_ab, b_bb = a_bb + t a_ab
+          const int a = pa[tid], b = pb[tid];
+          const double t = pt[tid], apq = papq[tid];
+          S[a * LDS_ + a] = papp[tid] - t * apq;
+          S[b * LDS_ + b] = paqq[tid] + t * apq;
+          S[a * LDS_ + b] = 0.0;
+          S[b * LDS_ + a] = 0.0;
+        }
+        if (tid == 0) rot_sweep = 1;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    const int rs = rot_sweep;
+    __syncthreads();
+    if (!rs) break;
+    any = 1;
+  }
+  if (sweeps_out) *sweeps_out = sw;
+  __syncthreads();
+  return any;
+}
+
+// One CTA per (job, pair).  Small jobs are solved completely here.
+__global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jobs, RootState* st,
+                                                  const int32_t* __restrict__ pbegin, int njobs,
+                                                  double* __restrict__ ws, double* __restrict__ vs,
+                                                  double* __restrict__ us) {
+  extern __shared__ double smem[];
+  double* S = smem;
+  double* U = smem + NS * LDS_;
+  const int j = find_job(pbegin, njobs, blockIdx.x);
+  if (!st[j].active) return;
+  const RootJob& J = jobs[j];
+  const int pair = blockIdx.x - pbegin[j];
+  const int np = J.np;
+  double* A = ws + J.ws_off;
+  const bool small = (J.m == 0);
+  int ns, ra = 0, rb = 0;
+  if (small) {
+    ns = np;
+  } else {
+    ns = NS;
+    const int r = st[j].round;
+    ra = circle_pos(r, pair, J.m);
+    rb = circle_pos(r, J.m - 1 - pair, J.m);
+  }
+  auto gidx = [&](int x) { return small ? x : (x < HB ? ra * HB + x : rb * HB + (x - HB)); };
+  for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
+    const int i = e / ns, k = e % ns;
+    S[i * LDS_ + k] = A[(int64_t)gidx(i) * np + gidx(k)];
+  }
+  __syncthreads();
+  int sweeps = 0;
+  const int any = cta_jacobi(S, U, ns, st[j].tol_abs, &sweeps);
+  if (small) {
+    double* V = vs + J.v_off;
+    for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
+      const int i = e / ns, k = e % ns;
+      A[(int64_t)i * np + k] = (i == k) ? S[i * LDS_ + i] : 0.0;
+      V[(int64_t)i * np + k] = U[i * LDS_ + k];
+    }
+    if (threadIdx.x == 0) {
+      st[j].active = 0;
+      st[j].sweep = sweeps;
+      if (sweeps >= MAX_SWEEPS) st[j].status = kEigNoConvergence;
+    }
+    return;
+  }
+  double* slot = us + J.u_off + (int64_t)pair * SLOT;
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) slot[e] = U[(e / NS) * LDS_ + (e % NS)];
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) slot[NS * NS + e] = S[e * LDS_ + e];
+  if (threadIdx.x == 0) {
+    slot[NS * NS + NS] = any ? 1.0 : 0.0;
+    if (any) st[j].rotated = 1;
+  }
+}
+
+// C(64x64) += X' Y' in registers; X'(i,k) = TX ? X[k][i] : X[i][k]; Y'(k,j) = TY ? Y[j][k] : Y[k][j]
+template <bool TX, bool TY>
+__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&acc)[4][4], int ty, int tx) {
+#pragma unroll 4
+  for (int k = 0; k < NS; ++k) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = TX ? X[k * LDS_ + ty * 4 + i] : X[(ty * 4 + i) * LDS_ + k];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b[q] = TY ? Y[(tx * 4 + q) * LDS_ + k] : Y[k * LDS_ + tx * 4 + q];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] = fma(a[i], b[q], acc[i][q]);
+  }
+}
+
+__device__ __forceinline__ void tri_decode(int l, int& hi, int& lo) {
+  int r = (int)((sqrt(8.0 * l + 1.0) - 1.0) * 0.5);
+  while ((r + 1) * (r + 2) / 2 <= l) ++r;
+  while (r * (r + 1) / 2 > l) --r;
+  hi = r;
+  lo = l - r * (r + 1) / 2;
+}
+
+// A <- W^T A W (pair tiles P<=Q) and V <- V W (row chunk x pair), one CTA per item.
+__global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
+                                               const RootState* __restrict__ st,
+                                               const int32_t* __restrict__ ibegin, int njobs,
+                                               double* __restrict__ ws, double* __restrict__ vs,
+                                               const double* __restrict__ us) {
+  extern __shared__ double smem[];
+  double* X = smem;                 // loaded tile
+  double* UP = smem + NS * LDS_;
+  double* UQ = smem + 2 * NS * LDS_;
+  double* T = smem + 3 * NS * LDS_;
+  const int j = find_job(ibegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  if (J.m == 0 || !st[j].active) return;
+  const int item = blockIdx.x - ibegin[j];
+  const int h = J.m / 2, np = J.np, r = st[j].round;
+  const int nA = h * (h + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
+  const double* slots = us + J.u_off;
+  auto pblk = [&](int P, int x) {  // global row of local index x in pair P
+    const int b = x < HB ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m);
+    return b * HB + (x & (HB - 1));
+  };
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+  double* A = ws + J.ws_off;
+  if (item < nA) {
+    int Q, P;
+    tri_decode(item, Q, P);  // Q >= P
+    const double* sP = slots + (int64_t)P * SLOT;
+    const double* sQ = slots + (int64_t)Q * SLOT;
+    if (P == Q) {
+      for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+        const int a = e / NS, b = e % NS;
+        A[(int64_t)pblk(P, a) * np + pblk(P, b)] = (a == b) ? sP[NS * NS + a] : 0.0;
+      }
+      return;
+    }
+    const bool rp = sP[NS * NS + NS] != 0.0, rq = sQ[NS * NS + NS] != 0.0;
+    if (!rp && !rq) return;
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+      const int a = e / NS, b = e % NS;
+      X[a * LDS_ + b] = A[(int64_t)pblk(P, a) * np + pblk(Q, b)];
+      UP[a * LDS_ + b] = sP[e];
+      UQ[a * LDS_ + b] = sQ[e];
+    }
+    __syncthreads();
+    mm64<false, false>(X, UQ, acc, ty, tx);  // T = X UQ
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        T[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
+        acc[i][q] = 0.0;
+      }
+    __syncthreads();
+    mm64<true, false>(UP, T, acc, ty, tx);  // R = UP^T T
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) X[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
+    __syncthreads();
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+      const int a = e / NS, b = e % NS;
+      A[(int64_t)pblk(P, a) * np + pblk(Q, b)] = X[a * LDS_ + b];
+      // mirror (coalesced along a)
+      A[(int64_t)pblk(Q, b) * np + pblk(P, a)] = X[a * LDS_ + b];
+    }
+    return;
+  }
+  // V tile
+  const int v = item - nA;
+  const int P = v % h, R = v / h;
+  const double* sP = slots + (int64_t)P * SLOT;
+  if (sP[NS * NS + NS] == 0.0) return;
+  double* V = vs + J.v_off;
+  const int r0 = R * NS;
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int a = e / NS, b = e % NS;
+    const int gr = r0 + a;
+    X[a * LDS_ + b] = gr < np ? V[(int64_t)gr * np + pblk(P, b)] : 0.0;
+    UP[a * LDS_ + b] = sP[e];
+  }
+  __syncthreads();
+  mm64<false, false>(X, UP, acc, ty, tx);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) X[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
+  __syncthreads();
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int a = e / NS, b = e % NS;
+    const int gr = r0 + a;
+    if (gr < np) V[(int64_t)gr * np + pblk(P, b)] = X[a * LDS_ + b];
+  }
+}
+
+// Advance per-job round/sweep counters; count active jobs (single CTA).
+__global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, RootState* st,
+                                              int32_t* mask, int njobs, int32_t* count) {
+  __shared__ int red[32];
+  int act = 0;
+  for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
+    RootState& s = st[j];
+    if (s.active && jobs[j].m > 0) {
+      if (++s.round == jobs[j].m - 1) {
+        s.round = 0;
+        ++s.sweep;
+        if (!s.rotated) {
+          s.active = 0;
+        } else if (s.sweep >= MAX_SWEEPS) {
+          s.active = 0;
+          s.status = kEigNoConvergence;
+        }
+        s.rotated = 0;
+      }
+    }
+    mask[j] = s.active;
+    act += s.active;
+  }
+  act = block_sum<int, 256>(act, red);
+  if (threadIdx.x == 0) *count = act;
+}
+
+// ---------------------------------------------------------------- reconstruction
+
+// sf_k = (w_k - min(w_min, 0) + eps)^(-eta/(2p)); mask = status ok.
+__global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ jobs, RootState* st,
+                                                   int32_t* mask, const double* __restrict__ ws,
+                                                   double* __restrict__ wv, double eta, double eps) {
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  const RootJob& J = jobs[j];
+  if (st[j].status != kEigOk) {
+    if (threadIdx.x == 0) mask[j] = 0;
+    return;
+  }
+  const double* A = ws + J.ws_off;
+  double wmin = INFINITY;
+  for (int i = threadIdx.x; i < J.n; i += blockDim.x) wmin = fmin(wmin, A[(int64_t)i * J.np + i]);
+  // block min
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmin = fmin(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = wmin;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double shift = fmin(red[0], 0.0);
+  const double ex = -eta / (2.0 * J.root_p);
+  int bad = 0;
+  for (int i = threadIdx.x; i < J.n; i += blockDim.x) {
+    const double w = A[(int64_t)i * J.np + i] - shift + eps;
+    if (eps == 0.0 && w <= 0.0) bad = 1;
+    wv[J.w_off + i] = pow(w, ex);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (bad) st[j].status = kEigEpsZeroSingular;
+    mask[j] = bad ? 0 : 1;
+  }
+}
+
+// Y = V diag(sf) written over the A workspace (ld np).
+__global__ void __launch_bounds__(256) k_eig_y(const RootJob* __restrict__ jobs,
+                                               const int32_t* __restrict__ mask,
+                                               const int32_t* __restrict__ ebegin, int njobs,
+                                               double* __restrict__ ws, const double* __restrict__ vs,
+                                               const double* __restrict__ wv) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    ws[J.ws_off + e] = (i < J.n && k < J.n) ? vs[J.v_off + e] * wv[J.w_off + k] : 0.0;
+  }
+}
+
+// Non-finite check of the reconstructed X (n x n, contiguous at v_off).
+__global__ void __launch_bounds__(256) k_check_x(const RootJob* __restrict__ jobs, RootState* st,
+                                                 const int32_t* __restrict__ mask,
+                                                 const int32_t* __restrict__ ebegin, int njobs,
+                                                 const double* __restrict__ vs) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.n * J.n;
+  int bad = 0;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x)
+    if (!isfinite(vs[J.v_off + e])) bad = 1;
+  bad = __syncthreads_or(bad);
+  if (bad && threadIdx.x == 0) st[j].status = kEigNonFiniteResult;
+}
+
+// Guard select: ok -> X; else previous (untouched) or eps^(-eta/p) I.
+__global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                const int32_t* __restrict__ ebegin, int njobs,
+                                                const double* __restrict__ vs) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  const bool ok = st[j].status == kEigOk;
+  if (!ok && J.has_prev) return;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.n * J.n;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    double v;
+    if (ok) v = vs[J.v_off + e];
+    else v = (e / J.n == e % J.n) ? J.idscale : 0.0;
+    if (J.out_f32) static_cast<float*>(J.out)[e] = (float)v;
+    else static_cast<double*>(J.out)[e] = v;
+  }
+}
+
+__global__ void k_mask_ok(const RootState* __restrict__ st, int32_t* mask, int njobs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < njobs) mask[j] = st[j].status == kEigOk;
+}
+
+__global__ void k_count(const RootJob* __restrict__ jobs, RootState* st, int njobs, int64_t* stats) {
+  if (threadIdx.x != 0) return;
+  for (int j = 0; j < njobs; ++j) {
+    if (st[j].status == kEigOk) {
+      st[j].result = 0;
+      ++stats[0];
+    } else if (jobs[j].has_prev) {
+      st[j].result = 2;
+      ++stats[2];
+    } else {
+      st[j].result = 3;
+      ++stats[3];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- coupled Newton
+
+// Per job scratch at nx + n2_off: X0, X1, M0, M1, T, Pa, Pb, Xbest (8 n^2).
+struct NewtonJob {
+  int32_t n, p;
+  int64_t off;
+  double best;
+  int32_t iters, converged;
+};
+
+__global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__ jobs, RootState* st,
+                                                     NewtonJob* nj, int32_t* mask,
+                                                     const int32_t* __restrict__ ebegin, int njobs,
+                                                     const double* __restrict__ ws, double* __restrict__ nx,
+                                                     double eps, int phase) {
+  // phase 0: after k_init (norm2 of A known) compute c; phase 1: fill X0, M0, Xbest
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  NewtonJob& N = nj[j];
+  if (st[j].status != kEigOk) {
+    if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) mask[j] = 0;
+    return;
+  }
+  const int n = J.n;
+  const double nrm = sqrt(st[j].norm2);
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)n * n;
+  double* X0 = nx + N.off;
+  double* M0 = X0 + 2 * tot;
+  double* XB = X0 + 7 * tot;
+  if (nrm == 0.0) {
+    // zero matrix: eps^(-1/p) I (matfun.py:182-188)
+    const double v = eps > 0.0 ? pow(eps, -1.0 / J.root_p) : 0.0;
+    for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x)
+      XB[e] = (e / n == e % n) ? v : 0.0;
+    if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) {
+      mask[j] = 0;
+      N.converged = eps > 0.0;
+      N.iters = 0;
+      N.best = 0.0;
+    }
+    return;
+  }
+  // ||A + eps I||_F^2 = ||A||^2 + 2 eps tr(A) + n eps^2; tr(A) folded via st.tol_abs slot? compute directly
+  const double* A = ws + J.ws_off;
+  const double tr = st[j].trace;
+  const double fro2 = st[j].norm2 + (eps > 0.0 ? 2.0 * eps * tr + n * eps * eps : 0.0);
+  const int p = J.root_p;
+  const double c = pow(2.0 * sqrt(fro2) / (p + 1), 1.0 / p);
+  const double cp = pow(c, (double)p);
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int64_t i = e / n, k = e % n;
+    const double a = A[i * J.np + k] + ((i == k && eps > 0.0) ? eps : 0.0);
+    X0[e] = (i == k) ? 1.0 / c : 0.0;
+    M0[e] = a / cp;
+    XB[e] = X0[e];
+  }
+  if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) {
+    mask[j] = 1;
+    N.best = INFINITY;
+    N.iters = 0;
+    N.converged = 0;
+  }
+}
+
+// T = ((p+1) I - M_cur) / p
+__global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ nj, const int32_t* __restrict__ mask,
+                                                  const int32_t* __restrict__ ebegin, int njobs,
+                                                  double* __restrict__ nx, int cur) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const NewtonJob& N = nj[j];
+  const int64_t tot = (int64_t)N.n * N.n;
+  const double* M = nx + N.off + (2 + cur) * tot;
+  double* T = nx + N.off + 4 * tot;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const bool d = (e / N.n == e % N.n);
+    T[e] = ((d ? (double)(N.p + 1) : 0.0) - M[e]) / N.p;
+  }
+}
+
+// residual = max row sum |M_next - I|; best tracking; convergence (one CTA per job)
+__global__ void __launch_bounds__(256) k_newton_res(NewtonJob* nj, int32_t* mask, int njobs,
+                                                    double* __restrict__ nx, int nxt, double tol,
+                                                    int32_t* count) {
+  __shared__ double red[32];
+  __shared__ int improved;
+  const int j = blockIdx.x;
+  if (!mask[j]) return;
+  NewtonJob& N = nj[j];
+  const int n = N.n;
+  const int64_t tot = (int64_t)n * n;
+  const double* M = nx + N.off + (2 + nxt) * tot;
+  double rmax = 0.0;
+  int bad = 0;
+  for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
+    double s = 0;
+    for (int k = threadIdx.x & 31; k < n; k += 32) s += fabs(M[(int64_t)i * n + k] - (i == k ? 1.0 : 0.0));
+    s = warp_sum(s);
+    if (!isfinite(s)) bad = 1;
+    rmax = fmax(rmax, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rmax;
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    double r = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+    N.iters += 1;
+    improved = 0;
+    if (bad || !isfinite(r)) {
+      mask[j] = 0;  // diverged: keep best iterate, not converged
+    } else {
+      if (r < N.best) {
+        N.best = r;
+        improved = 1;
+      }
+      if (r < tol) {
+        N.converged = 1;
+        mask[j] = 0;
+      } else if (N.iters >= 1000) {
+        mask[j] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (improved) {
+    const double* X = nx + N.off + nxt * tot;
+    double* XB = nx + N.off + 7 * tot;
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) XB[e] = X[e];
+  }
+  if (threadIdx.x == 0 && mask[j]) atomicAdd(count, 1);
+}
+
+// X = sym(Xbest) into the V workspace (contiguous n x n); status from convergence.
+__global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict__ jobs, RootState* st,
+                                                       const NewtonJob* __restrict__ nj,
+                                                       const int32_t* __restrict__ ebegin, int njobs,
+                                                       const double* __restrict__ nx, double* __restrict__ vs) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  const NewtonJob& N = nj[j];
+  if (st[j].status != kEigOk) return;
+  const int n = J.n;
+  const int64_t tot = (int64_t)n * n;
+  const double* XB = nx + N.off + 7 * tot;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int64_t i = e / n, k = e % n;
+    vs[J.v_off + e] = 0.5 * (XB[i * n + k] + XB[k * n + i]);
+  }
+}
+
+__global__ void k_newton_status(RootState* st, const NewtonJob* __restrict__ nj, int njobs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  if (st[j].status == kEigOk && !nj[j].converged) st[j].status = kEigNoConvergence;
+  st[j].sweep = nj[j].iters;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+
+RootInverseBatch::~RootInverseBatch() {
+  cudaFree(d_jobs_);
+  cudaFree(d_state_);
+  cudaFree(ws_);
+  cudaFree(vs_);
+  cudaFree(us_);
+  cudaFree(wv_);
+  cudaFree(nx_);
+  cudaFree(d_pair_begin_);
+  cudaFree(d_item_begin_);
+  cudaFree(d_elem_begin_);
+  cudaFree(d_count_);
+  cudaFreeHost(h_count_);
+}
+
+double RootInverseBatch::work_n3() const {
+  double w = 0;
+  for (const auto& j : host_) w += (double)j.n * j.n * j.n;
+  return w;
+}
+
+int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int32_t>& root_p) {
+  host_.clear();
+  ws_elems_ = u_elems_ = w_elems_ = n2_elems_ = 0;
+  has_big_ = false;
+  std::vector<int32_t> pbeg, ibeg, ebeg;
+  int32_t pairs = 0, items = 0, echunks = 0;
+  n2_off_.clear();
+  for (size_t j = 0; j < n.size(); ++j) {
+    RootJob J{};
+    J.n = n[j];
+    J.root_p = root_p[j];
+    if (J.n <= NS) {
+      J.np = J.n + (J.n & 1);
+      J.m = 0;
+    } else {
+      J.np = (J.n + NS - 1) / NS * NS;
+      J.m = J.np / HB;
+      has_big_ = true;
+    }
+    J.ws_off = ws_elems_;
+    J.v_off = ws_elems_;
+    ws_elems_ += (int64_t)J.np * J.np;
+    J.u_off = u_elems_;
+    J.w_off = w_elems_;
+    w_elems_ += J.np;
+    pbeg.push_back(pairs);
+    ibeg.push_back(items);
+    ebeg.push_back(echunks);
+    if (J.m == 0) {
+      pairs += 1;
+    } else {
+      const int h = J.m / 2;
+      pairs += h;
+      u_elems_ += (int64_t)h * SLOT;
+      items += h * (h + 1) / 2 + (J.np / NS) * h;
+    }
+    echunks += (int32_t)(((int64_t)J.np * J.np + ECH - 1) / ECH);
+    n2_off_.push_back(n2_elems_);
+    n2_elems_ += 8 * (int64_t)J.n * J.n;
+    J.in_scale = 1.0;
+    host_.push_back(J);
+  }
+  total_pairs_ = pairs;
+  total_items_ = items;
+  total_elem_chunks_ = echunks;
+  const size_t nj = host_.size();
+  if (nj == 0) return SHAMPOO_OK;
+  SH_CUDA_CHECK(cudaMalloc(&d_jobs_, nj * sizeof(RootJob)));
+  SH_CUDA_CHECK(cudaMalloc(&d_state_, nj * sizeof(RootState)));
+  SH_CUDA_CHECK(cudaMalloc(&ws_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&vs_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&us_, std::max<int64_t>(u_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&wv_, std::max<int64_t>(w_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&d_pair_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_item_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_elem_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_count_, 4 * sizeof(int32_t) + nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMallocHost(&h_count_, 4 * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMemcpy(d_pair_begin_, pbeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_item_begin_, ibeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_elem_begin_, ebeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // reconstruction X = Y Y^T : Y in ws (ld np), X into vs (ld n, contiguous)
+  recon_.host.clear();
+  for (const auto& J : host_) {
+    GemmProblem p = make_gemm(false, true, J.n, J.n, J.n, ws_ + J.ws_off, J.np, ws_ + J.ws_off, J.np,
+                              vs_ + J.v_off, J.n, 1.0, 0.0);
+    p.flags |= kGemmSym | kGemmMasked;
+    p.mask_index = (int32_t)(&J - host_.data());
+    recon_.add(p);
+  }
+  int rc = recon_.upload();
+  if (rc) return rc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       2 * NS * LDS_ * (int)sizeof(double)));
+    SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       4 * NS * LDS_ * (int)sizeof(double)));
+    attr_done = true;
+  }
+  return SHAMPOO_OK;
+}
+
+void RootInverseBatch::set_io(int j, const void* in, bool in_f32, void* out, bool out_f32) {
+  host_[j].in = in;
+  host_[j].in_f32 = in_f32;
+  host_[j].out = out;
+  host_[j].out_f32 = out_f32;
+}
+
+int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters) {
+  const int nj = (int)host_.size();
+  int32_t* mask = d_count_ + 4;
+  // Jacobi rounds until every job is inactive
+  for (int R = 0;; ++R) {
+    k_subsolve<<<total_pairs_, 256, 2 * NS * LDS_ * sizeof(double), s>>>(d_jobs_, d_state_, d_pair_begin_, nj,
+                                                                          ws_, vs_, us_);
+    SH_LAUNCH_CHECK();
+    if (!has_big_) break;
+    if (total_items_ > 0) {
+      k_apply<<<total_items_, 256, 4 * NS * LDS_ * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
+                                                                          ws_, vs_, us_);
+      SH_LAUNCH_CHECK();
+    }
+    k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_);
+    SH_LAUNCH_CHECK();
+    if ((R & 7) == 7) {
+      SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_count_[0] == 0) break;
+    }
+    if (R > 64 * MAX_SWEEPS * 4) break;  // safety net; k_book flags non-convergence
+  }
+  (void)iters;
+  k_eig_scale<<<nj, 256, 0, s>>>(d_jobs_, d_state_, mask, ws_, wv_, eta, eps);
+  SH_LAUNCH_CHECK();
+  k_eig_y<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, mask, d_elem_begin_, nj, ws_, vs_, wv_);
+  SH_LAUNCH_CHECK();
+  int rc = recon_.launch(s, mask);
+  if (rc) return rc;
+  return SHAMPOO_OK;
+}
+
+int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters) {
+  const int nj = (int)host_.size();
+  int32_t* mask = d_count_ + 4;
+  if (!nx_) SH_CUDA_CHECK(cudaMalloc(&nx_, std::max<int64_t>(n2_elems_, 1) * sizeof(double)));
+  std::vector<NewtonJob> hn(nj);
+  for (int j = 0; j < nj; ++j) {
+    hn[j].n = host_[j].n;
+    hn[j].p = host_[j].root_p;
+    hn[j].off = n2_off_[j];
+  }
+  NewtonJob* dn = nullptr;
+  SH_CUDA_CHECK(cudaMalloc(&dn, nj * sizeof(NewtonJob)));
+  SH_CUDA_CHECK(cudaMemcpyAsync(dn, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice, s));
+  k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, 0);
+  SH_LAUNCH_CHECK();
+  // GEMM sets for cur = 0/1: X_nxt = X_cur T ; powers ; M_nxt = T^p M_cur
+  int maxp = 1;
+  for (const auto& J : host_) maxp = std::max(maxp, J.root_p);
+  GemmBatch<double> xstep[2], mstep[2];
+  std::vector<GemmBatch<double>*> pw;  // power chain, step q: P_q = P_{q-1} T
+  std::vector<std::unique_ptr<GemmBatch<double>>> powers(std::max(0, maxp - 1));
+  for (auto& p : powers) p.reset(new GemmBatch<double>());
+  for (int j = 0; j < nj; ++j) {
+    const int n = host_[j].n, p = host_[j].root_p;
+    const int64_t tot = (int64_t)n * n;
+    double* base = nx_ + n2_off_[j];
+    double *X[2] = {base, base + tot}, *M[2] = {base + 2 * tot, base + 3 * tot};
+    double *T = base + 4 * tot, *Pab[2] = {base + 5 * tot, base + 6 * tot};
+    // power chain result location: p==1 -> T ; else Pab[(p-2)&1]
+    double* Pfinal = (p == 1) ? T : Pab[(p - 2) & 1];
+    for (int c = 0; c < 2; ++c) {
+      GemmProblem g = make_gemm(false, false, n, n, n, X[c], n, T, n, X[c ^ 1], n, 1.0, 0.0);
+      g.flags |= kGemmMasked;
+      g.mask_index = j;
+      xstep[c].add(g);
+      g = make_gemm(false, false, n, n, n, Pfinal, n, M[c], n, M[c ^ 1], n, 1.0, 0.0);
+      g.flags |= kGemmMasked;
+      g.mask_index = j;
+      mstep[c].add(g);
+    }
+    for (int q = 2; q <= p; ++q) {
+      const double* prev = (q == 2) ? T : Pab[(q - 3) & 1];
+      GemmProblem g = make_gemm(false, false, n, n, n, prev, n, T, n, Pab[(q - 2) & 1], n, 1.0, 0.0);
+      g.flags |= kGemmMasked;
+      g.mask_index = j;
+      powers[q - 2]->add(g);
+    }
+  }
+  int rc;
+  for (int c = 0; c < 2; ++c) {
+    if ((rc = xstep[c].upload())) return rc;
+    if ((rc = mstep[c].upload())) return rc;
+  }
+  for (auto& p : powers)
+    if ((rc = p->upload())) return rc;
+  int cur = 0;
+  for (int it = 1; it <= 1000; ++it) {
+    k_newton_t<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, nx_, cur);
+    SH_LAUNCH_CHECK();
+    if ((rc = xstep[cur].launch(s, mask))) return rc;
+    for (auto& p : powers)
+      if ((rc = p->launch(s, mask))) return rc;
+    if ((rc = mstep[cur].launch(s, mask))) return rc;
+    SH_CUDA_CHECK(cudaMemsetAsync(d_count_, 0, sizeof(int32_t), s));
+    k_newton_res<<<nj, 256, 0, s>>>(dn, mask, nj, nx_, cur ^ 1, tol, d_count_);
+    SH_LAUNCH_CHECK();
+    cur ^= 1;
+    if ((it & 3) == 0 || it < 4) {
+      SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_count_[0] == 0) break;
+    }
+  }
+  k_newton_finish<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, vs_);
+  SH_LAUNCH_CHECK();
+  k_newton_status<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, dn, nj);
+  SH_LAUNCH_CHECK();
+  SH_CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(dn);
+  (void)iters;
+  return SHAMPOO_OK;
+}
+
+int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
+                          int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
+                          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters) {
+  const int nj = (int)host_.size();
+  if (nj == 0) return SHAMPOO_OK;
+  for (int j = 0; j < nj; ++j) {
+    host_[j].in_scale = in_scale;
+    host_[j].has_prev = has_prev.empty() ? 0 : has_prev[j];
+    host_[j].idscale = eps > 0.0 ? std::pow(eps, -eta / host_[j].root_p) : 1.0;  // matfun.py:287-293
+  }
+  SH_CUDA_CHECK(cudaMemcpyAsync(d_jobs_, host_.data(), nj * sizeof(RootJob), cudaMemcpyHostToDevice, s));
+  k_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, nj);
+  SH_LAUNCH_CHECK();
+  k_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, ws_, vs_, in_scale);
+  SH_LAUNCH_CHECK();
+  int32_t* mask = d_count_ + 4;
+  k_init_finish<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, mask, nj, eps);
+  SH_LAUNCH_CHECK();
+  int rc = (solver == SHAMPOO_SOLVER_NEWTON) ? run_newton(eps, newton_tol, s, host_iters)
+                                             : run_eigh(eta, eps, s, host_iters);
+  if (rc) return rc;
+  k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
+  SH_LAUNCH_CHECK();
+  k_check_x<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, mask, d_elem_begin_, nj, vs_);
+  SH_LAUNCH_CHECK();
+  k_select<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, vs_);
+  SH_LAUNCH_CHECK();
+  int64_t* d_stats = nullptr;
+  SH_CUDA_CHECK(cudaMallocAsync(&d_stats, 4 * sizeof(int64_t), s));
+  SH_CUDA_CHECK(cudaMemcpyAsync(d_stats, stats, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  k_count<<<1, 32, 0, s>>>(d_jobs_, d_state_, nj, d_stats);
+  SH_LAUNCH_CHECK();
+  SH_CUDA_CHECK(cudaMemcpyAsync(stats, d_stats, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  std::vector<RootState> hs(nj);
+  SH_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_state_, nj * sizeof(RootState), cudaMemcpyDeviceToHost, s));
+  SH_CUDA_CHECK(cudaStreamSynchronize(s));
+  SH_CUDA_CHECK(cudaFreeAsync(d_stats, s));
+  if (host_status) {
+    host_status->resize(nj);
+    for (int j = 0; j < nj; ++j) (*host_status)[j] = hs[j].status;
+  }
+  if (host_iters) {
+    host_iters->resize(nj);
+    for (int j = 0; j < nj; ++j) (*host_iters)[j] = hs[j].sweep;
+  }
+  return SHAMPOO_OK;
+}
+
+}  // namespace shampoo

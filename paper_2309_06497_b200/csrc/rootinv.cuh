@@ -1,0 +1,95 @@
+// Batched guarded root inverse X = A^(-eta/p) of symmetric PSD matrices.
+//
+// Follows matfun.py:139-157 (eigh path: shift-clamp w - min(w_min,0) + eps,
+// X = Q diag(w^(-eta/p)) Q^T) and matfun.py:164-222 (coupled Newton), wrapped
+// in the retry guard of matfun.py:240-293.  All arithmetic is FP64 (the
+// reference default precision): the eigen path is a parallel two-sided block
+// Jacobi solver; the Newton path uses the grouped DGEMM.
+#pragma once
+
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace shampoo {
+
+enum EigStatus : int32_t {
+  kEigOk = 0,
+  kEigNonFiniteInput = 1,
+  kEigNoConvergence = 2,
+  kEigEpsZeroSingular = 3,
+  kEigNonFiniteResult = 4,
+};
+
+// One matrix of a batch.
+struct RootJob {
+  int32_t n;         // true size
+  int32_t np;        // padded size (n<=64: n rounded to even; else multiple of 64)
+  int32_t m;         // 32-row blocks (np/32) for big jobs, 0 for small
+  int32_t root_p;
+  int64_t ws_off;    // A workspace offset (np*np)
+  int64_t v_off;     // V workspace offset (np*np)
+  int64_t u_off;     // pair-slot offset (big jobs)
+  int64_t w_off;     // vector workspace offset (np)
+  const void* in;    // n x n input (row-major)
+  void* out;         // n x n output (row-major)
+  int32_t in_f32, out_f32;
+  int32_t has_prev;  // output already holds a previous inverse
+  int32_t pad;
+  double in_scale;   // multiply input by this (1/bias-correction)
+  double idscale;    // identity-fallback scale eps^(-eta/p) (or 1)
+};
+
+// Mutable per-job solver state (device).
+struct RootState {
+  int32_t active, round, sweep, rotated;
+  int32_t status, result;  // result: 0 primary, 2 previous, 3 identity
+  double norm2;            // ||A||_F^2
+  double tol_abs;
+  double trace;            // tr(A)
+  int32_t nonfinite, pad;
+};
+
+class RootInverseBatch {
+ public:
+  RootInverseBatch() = default;
+  RootInverseBatch(const RootInverseBatch&) = delete;
+  RootInverseBatch& operator=(const RootInverseBatch&) = delete;
+  ~RootInverseBatch();
+  // sizes/root_p per job; allocates workspaces; jobs' in/out filled by set_io.
+  int setup(const std::vector<int32_t>& n, const std::vector<int32_t>& root_p);
+  void set_io(int j, const void* in, bool in_f32, void* out, bool out_f32);
+  // Run on all jobs. scale: input multiplier; has_prev per job (host).
+  // stats[4] accumulates GuardStats branches; host_status receives per-job status.
+  int run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
+          int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
+          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters);
+  size_t jobs() const { return host_.size(); }
+  double work_n3() const;  // sum n^3
+
+ private:
+  int run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters);
+  int run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters);
+  std::vector<RootJob> host_;
+  RootJob* d_jobs_ = nullptr;
+  RootState* d_state_ = nullptr;
+  double* ws_ = nullptr;   // A workspaces
+  double* vs_ = nullptr;   // V workspaces
+  double* us_ = nullptr;   // pair slots
+  double* wv_ = nullptr;   // vectors
+  double* nx_ = nullptr;   // Newton scratch (3 x n^2 per job)
+  int32_t* d_pair_begin_ = nullptr;
+  int32_t* d_item_begin_ = nullptr;
+  int32_t* d_elem_begin_ = nullptr;
+  int32_t* d_count_ = nullptr;
+  int32_t* h_count_ = nullptr;  // pinned
+  int32_t total_pairs_ = 0, total_items_ = 0, total_elem_chunks_ = 0;
+  int64_t ws_elems_ = 0, u_elems_ = 0, w_elems_ = 0, n2_elems_ = 0;
+  std::vector<int64_t> n2_off_;
+  bool has_big_ = false;
+  // reconstruction X = Y Y^T for all jobs
+  GemmBatch<double> recon_;
+  bool recon_ready_ = false;
+};
+
+}  // namespace shampoo

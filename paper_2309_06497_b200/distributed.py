@@ -1,0 +1,139 @@
+"""``DistributedShampoo``: the torch.optim facade over the device-native step.
+
+Paper API (arXiv 2309.06497 §5): ``DistributedShampoo(params,
+lr, betas, epsilon, momentum, use_nesterov, weight_decay,
+use_decoupled_weight_decay, use_bias_correction, max_preconditioner_dim,
+precondition_frequency, start_preconditioning_step, exponent_override,
+exponent_multiplier, grafting, grafting_epsilon, grafting_beta2, solver,
+newton_tolerance, num_trainers_per_group)``; kwargs map 1:1 onto
+``ShampooConfig`` (optim.py:53-84) and reuse its validation.
+
+Distribution (dist.py:133-369): one process per GPU.  The
+greedy plan is computed identically on every rank by the C++ planner; each
+rank keeps state only for the blocks its group rank owns, writes their
+directions into its region of the padded gather buffer, and an in-place NCCL
+all-gather inside each group of ``num_trainers_per_group`` ranks replicates
+all directions before every rank applies every block.  Groups are exact
+replicas (the assignment is replicated across groups).
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from .config import GraftKind, LargeDimMethod, ShampooConfig, Solver
+from .optimizer import GuardStats, Shampoo
+
+__all__ = ["DistributedShampoo", "GroupExchange"]
+
+
+class GroupExchange:
+    """Replica groups of ``group_size`` consecutive ranks and the region all-gather.
+
+    Mirrors dist.py:350-359: every group gathers independently; group g holds
+    ranks [g*J_G, (g+1)*J_G).  ``__call__(buf, group_rank, max_payload)`` fills
+    ``buf`` (group_size * max_payload scalars) from every rank's region.
+    """
+
+    def __init__(self, group_size: int, process_group=None):
+        self.world = dist.get_world_size(process_group)
+        self.rank = dist.get_rank(process_group)
+        if group_size <= 0:
+            group_size = self.world
+        if self.world % group_size:
+            from .config import InvalidGroupSizeError
+            raise InvalidGroupSizeError(f"group size {group_size} must divide world size {self.world}")
+        self.group_size = group_size
+        self.group = None
+        if group_size == self.world:
+            self.group = process_group
+        else:
+            for g in range(self.world // group_size):  # every rank creates every group
+                ranks = list(range(g * group_size, (g + 1) * group_size))
+                pg = dist.new_group(ranks)
+                if self.rank in ranks:
+                    self.group = pg
+        self.bytes_per_step = 0
+
+    def __call__(self, buf: torch.Tensor, group_rank: int, max_payload: int) -> None:
+        if max_payload == 0 or self.group_size == 1:
+            return
+        region = buf[group_rank * max_payload:(group_rank + 1) * max_payload]
+        out = buf[: self.group_size * max_payload]
+        try:
+            dist.all_gather_into_tensor(out, region, group=self.group)  # in place (NCCL)
+        except (RuntimeError, NotImplementedError, AttributeError):
+            # backends without the flat collective (e.g. gloo on CPU): list form, same bytes
+            parts = list(out.split(max_payload))
+            dist.all_gather(parts, region.clone(), group=self.group)
+        self.bytes_per_step = (self.group_size - 1) * max_payload * buf.element_size()
+
+
+class DistributedShampoo(torch.optim.Optimizer):
+    """Drop-in ``torch.optim.Optimizer`` running the B200 Shampoo step."""
+
+    def __init__(self, params, lr: float = 0.1, betas=(0.0, 0.999), epsilon: float = 1e-12,
+                 momentum: float = 0.9, use_nesterov: bool = True, weight_decay: float = 1e-4,
+                 use_decoupled_weight_decay: bool = True, use_bias_correction: bool = True,
+                 max_preconditioner_dim: int = 2048, precondition_frequency: int = 50,
+                 start_preconditioning_step: float = 0, exponent_override: int = 0,
+                 exponent_multiplier: float = 1.0, grafting=GraftKind.SGD,
+                 grafting_epsilon: float = 1e-8, grafting_beta2: float = 0.999, solver=Solver.EIGH,
+                 newton_tolerance: float = 1e-6, num_trainers_per_group: int = -1,
+                 large_dim_method=LargeDimMethod.BLOCKING, precision: str = "double",
+                 lr_schedule: str = "constant", warmup_steps: int = 0, total_steps: int = 0,
+                 process_group=None):
+        grafting = GraftKind(grafting) if not isinstance(grafting, GraftKind) else grafting
+        solver = Solver(solver) if not isinstance(solver, Solver) else solver
+        large_dim_method = (LargeDimMethod(large_dim_method)
+                            if not isinstance(large_dim_method, LargeDimMethod) else large_dim_method)
+        self.config = ShampooConfig(
+            lr=lr, lr_schedule=lr_schedule, warmup_steps=warmup_steps, total_steps=total_steps,
+            betas=tuple(betas), epsilon=epsilon, momentum=momentum, use_nesterov=use_nesterov,
+            weight_decay=weight_decay, use_decoupled_weight_decay=use_decoupled_weight_decay,
+            use_bias_correction=use_bias_correction, max_preconditioner_dim=max_preconditioner_dim,
+            precondition_frequency=precondition_frequency,
+            start_preconditioning_step=start_preconditioning_step, exponent_override=exponent_override,
+            exponent_multiplier=exponent_multiplier, grafting=grafting, grafting_epsilon=grafting_epsilon,
+            grafting_beta2=grafting_beta2, large_dim_method=large_dim_method, solver=solver,
+            newton_tolerance=newton_tolerance, precision=precision)
+        defaults = dict(lr=lr, betas=tuple(betas), epsilon=epsilon, momentum=momentum,
+                        weight_decay=weight_decay)
+        super().__init__(params, defaults)
+        if len(self.param_groups) != 1:
+            raise ValueError("DistributedShampoo supports a single parameter group")
+        self._plist = list(self.param_groups[0]["params"])
+        if dist.is_available() and dist.is_initialized():
+            self.exchange = GroupExchange(num_trainers_per_group, process_group)
+            world, rank, group = self.exchange.world, self.exchange.rank, self.exchange.group_size
+        else:
+            if num_trainers_per_group not in (-1, 0, 1):
+                raise ValueError("num_trainers_per_group > 1 needs torch.distributed to be initialised")
+            self.exchange, world, rank, group = None, 1, 0, 1
+        self.engine = Shampoo([p.data for p in self._plist], self.config, world_size=world,
+                              group_size=group, rank=rank, exchange=self.exchange)
+
+    @property
+    def guard_stats(self) -> GuardStats:
+        return self.engine.guard_stats
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        grads = [p.grad if p.grad is not None else torch.zeros_like(p) for p in self._plist]
+        self.engine.step(grads)
+        return loss
+
+    def state_dict(self) -> dict:
+        """``state_tree`` nesting (optim.py:387-423) plus the torch param-group metadata."""
+        return {"state": self.engine.state_tree(), "param_groups": [
+            {k: v for k, v in g.items() if k != "params"} for g in self.param_groups]}
+
+    def load_state_dict(self, state_dict: dict) -> None:
+        self.engine.load_state_tree(state_dict["state"])
