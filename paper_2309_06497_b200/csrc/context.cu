@@ -244,6 +244,9 @@ int build_engine(shampoo_ctx* c) {
       off += d[m] * d[m];
     }
   }
+  // single precision keeps float factors but accumulates the contraction in FP64, like the
+  // reference's float64 tensordot followed by one cast (precond.py:236)
+  e->stats.fp64_accumulate = true;
   int rc = e->stats.upload();
   if (rc) return rc;
   for (int m = 0; m < kMaxOrder; ++m)
@@ -529,7 +532,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   std::vector<int32_t> has_prev(c->rinv.jobs());
   for (size_t j = 0; j < has_prev.size(); ++j) has_prev[j] = c->ready_h[c->job_block[j]];
   int rc = c->rinv.run(1.0 / corr, has_prev, k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance, s,
-                       c->guard, nullptr, nullptr);
+                       c->guard, nullptr, nullptr, /*allow_warm=*/true);
   if (rc) return rc;
   for (size_t l = 0; l < c->owned.size(); ++l) {
     if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_SHAMPOO) continue;

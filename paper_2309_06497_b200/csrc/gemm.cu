@@ -1,10 +1,15 @@
 // Grouped strided GEMM / GEMV kernels (see gemm.cuh).
 //
-// Tile 64x64x16, 256 threads, 4x4 register micro-tile per thread.  Each warp
-// covers a 16x32 sub-tile (4 row groups x 8 column groups) so that the
-// per-k shared-memory reads are broadcast-friendly: 4 wavefronts per 16 DFMA
-// issue slots, i.e. the FP64 pipe, not shared memory, is the limiter.
-// Global->register prefetch of the next k-slab overlaps the current one.
+// FP64: 64x64x16 CTA tile, 4 warps, 32x32 warp tile of FP64 tensor-core MMAs
+// (mma.sync.aligned.m16n8k4.row.col.f64 -> DMMA), k-major shared tiles with
+// leading dim 68 (== 4 mod 16 doubles: conflict-free fragment loads).
+// FP32: 64x64x16 tile, 256 threads, 4x4 FFMA micro-tiles (single-precision
+// mode; the tcgen05 path replaces it for the statistics GEMM).
+// Split-K: problems with K > kSplitChunk are cut into K chunks; each chunk
+// writes a raw 64x64 partial into a workspace and k_split_reduce sums the
+// chunks in a fixed order (deterministic) and applies the epilogue.
+// Symmetric (SYRK) problems compute only tiles tm >= tn and write C[i][j] and
+// C[j][i] from the same value, so factors stay exactly symmetric.
 #include <algorithm>
 #include <cmath>
 
@@ -14,36 +19,225 @@ namespace shampoo {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256, PAD = 4;
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int64_t kSplitChunk = 2048;
 
 __device__ __forceinline__ int64_t ev(const Idx2& x, int32_t v) {
   if (x.div == 0x7fffffff) return (int64_t)v * x.lo;
   return (int64_t)(v / x.div) * x.hi + (int64_t)(v % x.div) * x.lo;
 }
 
-// Load 4 elements of a 64x16 operand slab into registers.
+__device__ __forceinline__ void tri_index(int64_t l, int& tm, int& tn) {
+  int r = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(r + 1) * (r + 2) / 2 <= l) ++r;
+  while ((int64_t)r * (r + 1) / 2 > l) --r;
+  tm = r;
+  tn = (int)(l - (int64_t)r * (r + 1) / 2);
+}
+
+struct TileWork {
+  int prob, tm, tn, split;
+  int64_t tile;  // tile index within the problem
+};
+
+__device__ __forceinline__ TileWork locate(const GemmProblem* __restrict__ probs, const int64_t* __restrict__ begin,
+                                           int nprob, int64_t item) {
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  TileWork w;
+  w.prob = lo;
+  const GemmProblem& P = probs[lo];
+  const int64_t l = item - begin[lo];
+  w.split = (int)(l % P.ksplit);
+  w.tile = l / P.ksplit;
+  if (P.flags & kGemmSym) tri_index(w.tile, w.tm, w.tn);
+  else {
+    w.tm = (int)(w.tile / P.tiles_n);
+    w.tn = (int)(w.tile % P.tiles_n);
+  }
+  return w;
+}
+
+// Epilogue for one output element; for SYM diagonal tiles only i >= j is written (mirrored).
 template <typename T>
-__device__ __forceinline__ void load_slab(const T* __restrict__ X, const Idx2& xr, const Idx2& xk,
-                                          int rows, int K, int r0, int k0, bool kfast, T (&v)[4]) {
+__device__ __forceinline__ void store_out(const GemmProblem& P, int tm, int tn, int gi, int gj, double acc) {
+  if (gi >= P.M || gj >= P.N) return;
+  const bool sym = (P.flags & kGemmSym) != 0;
+  if (sym && tm == tn && gi < gj) return;
+  T* __restrict__ C = static_cast<T*>(P.C);
+  const int64_t at = ev(P.c_r, gi) + ev(P.c_c, gj);
+  double v = P.alpha * acc;
+  if (P.flags & kGemmReadC) v = fma(P.beta, (double)C[at], v);
+  const T o = T(v);
+  C[at] = o;
+  if (sym && gi != gj) C[ev(P.c_r, gj) + ev(P.c_c, gi)] = o;
+}
+
+// ---------------------------------------------------------------- FP64 DMMA kernel
+
+constexpr int LDA = BM + 4;  // 68 doubles
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// 64 x 16 slab: 1024 elements, 8 per thread (128 threads)
+template <typename T>
+__device__ __forceinline__ void load_slab64(const T* __restrict__ X, const Idx2& xr, const Idx2& xk, int rows,
+                                            int kend, int r0, int k0, bool kfast, double (&v)[8]) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    int r, k;
+    if (kfast) {
+      const int f = tid * 8 + e;
+      r = f >> 4;
+      k = f & 15;
+    } else {
+      r = tid & 63;
+      k = (tid >> 6) + 2 * e;
+    }
+    const int gr = r0 + r, gk = k0 + k;
+    v[e] = (gr < rows && gk < kend) ? (double)X[ev(xr, gr) + ev(xk, gk)] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void store_slab64(double (*S)[LDA], bool kfast, const double (&v)[8]) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    int r, k;
+    if (kfast) {
+      const int f = tid * 8 + e;
+      r = f >> 4;
+      k = f & 15;
+    } else {
+      r = tid & 63;
+      k = (tid >> 6) + 2 * e;
+    }
+    S[k][r] = v[e];
+  }
+}
+
+// T: storage type of A/B/C (float inputs are widened; accumulation is always FP64).
+template <typename T>
+__global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restrict__ probs,
+                                                     const int64_t* __restrict__ begin, int nprob,
+                                                     const int32_t* __restrict__ mask, double* __restrict__ ws) {
+  __shared__ __align__(16) double As[2][BK][LDA];
+  __shared__ __align__(16) double Bs[2][BK][LDA];
+  const TileWork w = locate(probs, begin, nprob, blockIdx.x);
+  const GemmProblem& P = probs[w.prob];
+  if ((P.flags & kGemmMasked) && mask && mask[P.mask_index] == 0) return;
+  const int m0 = w.tm * BM, n0 = w.tn * BN;
+  const int kbeg = w.split * P.kchunk;
+  const int kend = min(P.K, kbeg + P.kchunk);
+  const T* __restrict__ A = static_cast<const T*>(P.A);
+  const T* __restrict__ B = static_cast<const T*>(P.B);
+  const bool akf = (P.a_k.lo == 1), bkf = (P.b_k.lo == 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, tq = lane & 3;
+
+  double c[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[i][j][q] = 0.0;
+
+  double ra[8], rb[8];
+  const int nk = (kend - kbeg + BK - 1) / BK;
+  load_slab64(A, P.a_r, P.a_k, P.M, kend, m0, kbeg, akf, ra);
+  load_slab64(B, P.b_r, P.b_k, P.N, kend, n0, kbeg, bkf, rb);
+  store_slab64(As[0], akf, ra);
+  store_slab64(Bs[0], bkf, rb);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int cur = kt & 1;
+    if (kt + 1 < nk) {
+      load_slab64(A, P.a_r, P.a_k, P.M, kend, m0, kbeg + (kt + 1) * BK, akf, ra);
+      load_slab64(B, P.b_r, P.b_k, P.N, kend, n0, kbeg + (kt + 1) * BK, bkf, rb);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[2][2], b[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        a[i][0] = As[cur][kk + tq][wm + i * 16 + g];
+        a[i][1] = As[cur][kk + tq][wm + i * 16 + g + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[cur][kk + tq][wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_16x8x4(c[i][j], a[i][0], a[i][1], b[j]);
+    }
+    if (kt + 1 < nk) {
+      store_slab64(As[cur ^ 1], akf, ra);
+      store_slab64(Bs[cur ^ 1], bkf, rb);
+    }
+    __syncthreads();
+  }
+  if (P.ksplit > 1) {
+    double* part = ws + P.ws_off + (w.tile * P.ksplit + w.split) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = wm + i * 16 + g + (q >> 1) * 8, cc = wn + j * 8 + 2 * tq + (q & 1);
+          part[r * BN + cc] = c[i][j][q];
+        }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = wm + i * 16 + g + (q >> 1) * 8, cc = wn + j * 8 + 2 * tq + (q & 1);
+        store_out<T>(P, w.tm, w.tn, m0 + r, n0 + cc, c[i][j][q]);
+      }
+}
+
+// ---------------------------------------------------------------- FP32 FFMA kernel
+
+constexpr int PADF = 4;
+
+template <typename T>
+__device__ __forceinline__ void load_slab_f(const T* __restrict__ X, const Idx2& xr, const Idx2& xk, int rows,
+                                            int kend, int r0, int k0, bool kfast, T (&v)[4]) {
   const int tid = threadIdx.x;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     int r, k;
     if (kfast) {
-      const int f = tid * 4 + e;  // 4 consecutive k per thread
+      const int f = tid * 4 + e;
       r = f / BK;
       k = f % BK;
     } else {
-      r = tid % BM;  // consecutive threads -> consecutive rows
+      r = tid % BM;
       k = tid / BM + 4 * e;
     }
     const int gr = r0 + r, gk = k0 + k;
-    v[e] = (gr < rows && gk < K) ? X[ev(xr, gr) + ev(xk, gk)] : T(0);
+    v[e] = (gr < rows && gk < kend) ? X[ev(xr, gr) + ev(xk, gk)] : T(0);
   }
 }
 
 template <typename T>
-__device__ __forceinline__ void store_slab(T (*S)[BM + PAD], bool kfast, const T (&v)[4]) {
+__device__ __forceinline__ void store_slab_f(T (*S)[BM + PADF], bool kfast, const T (&v)[4]) {
   const int tid = threadIdx.x;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -60,71 +254,44 @@ __device__ __forceinline__ void store_slab(T (*S)[BM + PAD], bool kfast, const T
   }
 }
 
-__device__ __forceinline__ void tri_index(int64_t l, int& tm, int& tn) {
-  // l -> (tm, tn) with tm >= tn, row-major over the lower triangle
-  int r = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(r + 1) * (r + 2) / 2 <= l) ++r;
-  while ((int64_t)r * (r + 1) / 2 > l) --r;
-  tm = r;
-  tn = (int)(l - (int64_t)r * (r + 1) / 2);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(NT) grouped_gemm_kernel(const GemmProblem* __restrict__ probs,
-                                                          const int64_t* __restrict__ begin,
-                                                          int nprob, const int32_t* __restrict__ mask) {
-  __shared__ __align__(16) T As[2][BK][BM + PAD];
-  __shared__ __align__(16) T Bs[2][BK][BN + PAD];
-
-  // locate problem: last p with begin[p] <= blockIdx.x
-  const int64_t tile = blockIdx.x;
-  int lo = 0, hi = nprob - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (begin[mid] <= tile) lo = mid;
-    else hi = mid - 1;
-  }
-  const GemmProblem& P = probs[lo];
+__global__ void __launch_bounds__(256) gemm_f32_ffma(const GemmProblem* __restrict__ probs,
+                                                     const int64_t* __restrict__ begin, int nprob,
+                                                     const int32_t* __restrict__ mask, double* __restrict__ ws) {
+  __shared__ __align__(16) float As[2][BK][BM + PADF];
+  __shared__ __align__(16) float Bs[2][BK][BN + PADF];
+  const TileWork w = locate(probs, begin, nprob, blockIdx.x);
+  const GemmProblem& P = probs[w.prob];
   if ((P.flags & kGemmMasked) && mask && mask[P.mask_index] == 0) return;
-  const int64_t lt = tile - begin[lo];
-  int tm, tn;
-  if (P.flags & kGemmSym) {
-    tri_index(lt, tm, tn);
-  } else {
-    tm = (int)(lt / P.tiles_n);
-    tn = (int)(lt % P.tiles_n);
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const T* __restrict__ A = static_cast<const T*>(P.A);
-  const T* __restrict__ B = static_cast<const T*>(P.B);
+  const int m0 = w.tm * BM, n0 = w.tn * BN;
+  const int kbeg = w.split * P.kchunk;
+  const int kend = min(P.K, kbeg + P.kchunk);
+  const float* __restrict__ A = static_cast<const float*>(P.A);
+  const float* __restrict__ B = static_cast<const float*>(P.B);
   const bool akf = (P.a_k.lo == 1), bkf = (P.b_k.lo == 1);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
-  const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
-
-  T acc[4][4];
+  const int ty = (warp >> 1) * 4 + (lane >> 3);
+  const int tx = (warp & 1) * 8 + (lane & 7);
+  float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
-
-  T ra[4], rb[4];
-  const int nk = (P.K + BK - 1) / BK;
-  load_slab<T>(A, P.a_r, P.a_k, P.M, P.K, m0, 0, akf, ra);
-  load_slab<T>(B, P.b_r, P.b_k, P.N, P.K, n0, 0, bkf, rb);
-  store_slab<T>(As[0], akf, ra);
-  store_slab<T>(Bs[0], bkf, rb);
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  float ra[4], rb[4];
+  const int nk = (kend - kbeg + BK - 1) / BK;
+  load_slab_f<float>(A, P.a_r, P.a_k, P.M, kend, m0, kbeg, akf, ra);
+  load_slab_f<float>(B, P.b_r, P.b_k, P.N, kend, n0, kbeg, bkf, rb);
+  store_slab_f<float>(As[0], akf, ra);
+  store_slab_f<float>(Bs[0], bkf, rb);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int cur = kt & 1;
     if (kt + 1 < nk) {
-      load_slab<T>(A, P.a_r, P.a_k, P.M, P.K, m0, (kt + 1) * BK, akf, ra);
-      load_slab<T>(B, P.b_r, P.b_k, P.N, P.K, n0, (kt + 1) * BK, bkf, rb);
+      load_slab_f<float>(A, P.a_r, P.a_k, P.M, kend, m0, kbeg + (kt + 1) * BK, akf, ra);
+      load_slab_f<float>(B, P.b_r, P.b_k, P.N, kend, n0, kbeg + (kt + 1) * BK, bkf, rb);
     }
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      T a[4], b[4];
+      float a[4], b[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = As[cur][kk][ty * 4 + i];
 #pragma unroll
@@ -132,59 +299,81 @@ __global__ void __launch_bounds__(NT) grouped_gemm_kernel(const GemmProblem* __r
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     if (kt + 1 < nk) {
-      store_slab<T>(As[cur ^ 1], akf, ra);
-      store_slab<T>(Bs[cur ^ 1], bkf, rb);
+      store_slab_f<float>(As[cur ^ 1], akf, ra);
+      store_slab_f<float>(Bs[cur ^ 1], bkf, rb);
     }
     __syncthreads();
   }
+  if (P.ksplit > 1) {
+    double* part = ws + P.ws_off + (w.tile * P.ksplit + w.split) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part[(ty * 4 + i) * BN + tx * 4 + j] = acc[i][j];
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) store_out<float>(P, w.tm, w.tn, m0 + ty * 4 + i, n0 + tx * 4 + j, acc[i][j]);
+}
 
-  T* __restrict__ C = static_cast<T*>(P.C);
-  const T alpha = T(P.alpha), beta = T(P.beta);
-  const bool readc = (P.flags & kGemmReadC) != 0;
-  const bool mirror = (P.flags & kGemmSym) && tm != tn;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gi = m0 + ty * 4 + i;
-    if (gi >= P.M) continue;
-    const int64_t ri = ev(P.c_r, gi);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gj = n0 + tx * 4 + j;
-      if (gj >= P.N) continue;
-      const int64_t at = ri + ev(P.c_c, gj);
-      T v = alpha * acc[i][j];
-      if (readc) v = fma(beta, C[at], v);
-      C[at] = v;
-      if (mirror) C[ev(P.c_r, gj) + ev(P.c_c, gi)] = v;
-    }
+// Sum split-K partials in split order (fp64) and apply the epilogue; one CTA per split tile.
+template <typename T>
+__global__ void __launch_bounds__(256) k_split_reduce(const GemmProblem* __restrict__ probs,
+                                                      const int64_t* __restrict__ rbegin,
+                                                      const int32_t* __restrict__ rprob, int nred,
+                                                      const int32_t* __restrict__ mask,
+                                                      const double* __restrict__ ws) {
+  int lo = 0, hi = nred - 1;
+  const int64_t item = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rbegin[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmProblem& P = probs[rprob[lo]];
+  if ((P.flags & kGemmMasked) && mask && mask[P.mask_index] == 0) return;
+  const int64_t tile = item - rbegin[lo];
+  int tm, tn;
+  if (P.flags & kGemmSym) tri_index(tile, tm, tn);
+  else {
+    tm = (int)(tile / P.tiles_n);
+    tn = (int)(tile % P.tiles_n);
+  }
+  const double* part = ws + P.ws_off + tile * P.ksplit * (BM * BN);
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < P.ksplit; ++q) s += part[(int64_t)q * (BM * BN) + e];
+    store_out<T>(P, tm, tn, tm * BM + e / BN, tn * BN + e % BN, s);
   }
 }
 
 // One warp per output row; CTA = 8 rows.
 template <typename T>
 __global__ void __launch_bounds__(256) grouped_gemv_kernel(const GemvProblem* __restrict__ probs,
-                                                           const int64_t* __restrict__ begin,
-                                                           int nprob, const int32_t* __restrict__ mask) {
-  const int64_t g = blockIdx.x;
+                                                           const int64_t* __restrict__ begin, int nprob,
+                                                           const int32_t* __restrict__ mask) {
+  const int64_t gi = blockIdx.x;
   int lo = 0, hi = nprob - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (begin[mid] <= g) lo = mid;
+    if (begin[mid] <= gi) lo = mid;
     else hi = mid - 1;
   }
   const GemvProblem& P = probs[lo];
   if (mask && mask[P.mask_index] == 0) return;
-  const int row = (int)(g - begin[lo]) * 8 + (threadIdx.x >> 5);
+  const int row = (int)(gi - begin[lo]) * 8 + (threadIdx.x >> 5);
   if (row >= P.n) return;
   const T* __restrict__ X = static_cast<const T*>(P.X) + (int64_t)row * P.n;
   const T* __restrict__ x = static_cast<const T*>(P.x);
-  T s = 0;
-  for (int j = threadIdx.x & 31; j < P.n; j += 32) s = fma(X[j], x[j], s);
+  double s = 0;
+  for (int j = threadIdx.x & 31; j < P.n; j += 32) s = fma((double)X[j], (double)x[j], s);
   s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) static_cast<T*>(P.y)[row] = T(P.alpha) * s;
+  if ((threadIdx.x & 31) == 0) static_cast<T*>(P.y)[row] = T(P.alpha * s);
 }
 
 }  // namespace
@@ -193,39 +382,74 @@ template <typename T>
 GemmBatch<T>::~GemmBatch() {
   cudaFree(d_prob_);
   cudaFree(d_begin_);
+  cudaFree(d_rbegin_);
+  cudaFree(d_rprob_);
+  cudaFree(ws_);
 }
 
 template <typename T>
 int GemmBatch<T>::upload() {
   cudaFree(d_prob_);
   cudaFree(d_begin_);
+  cudaFree(d_rbegin_);
+  cudaFree(d_rprob_);
+  cudaFree(ws_);
   d_prob_ = nullptr;
-  d_begin_ = nullptr;
-  total_tiles_ = 0;
+  d_begin_ = d_rbegin_ = nullptr;
+  d_rprob_ = nullptr;
+  ws_ = nullptr;
+  total_items_ = total_red_ = 0;
   if (host.empty()) return SHAMPOO_OK;
-  std::vector<int64_t> begin(host.size());
+  std::vector<int64_t> begin(host.size()), rbegin;
+  std::vector<int32_t> rprob;
+  int64_t ws_elems = 0;
   for (size_t i = 0; i < host.size(); ++i) {
     GemmProblem& p = host[i];
     p.tiles_m = (p.M + BM - 1) / BM;
     p.tiles_n = (p.N + BN - 1) / BN;
-    p.tiles = (p.flags & kGemmSym) ? (int64_t)p.tiles_m * (p.tiles_m + 1) / 2
-                                   : (int64_t)p.tiles_m * p.tiles_n;
+    p.tiles = (p.flags & kGemmSym) ? (int64_t)p.tiles_m * (p.tiles_m + 1) / 2 : (int64_t)p.tiles_m * p.tiles_n;
     if (p.M == 0 || p.N == 0) p.tiles = 0;
-    begin[i] = total_tiles_;
-    total_tiles_ += p.tiles;
+    p.ksplit = (int32_t)std::max<int64_t>(1, (p.K + kSplitChunk - 1) / kSplitChunk);
+    p.kchunk = (int32_t)(p.ksplit == 1 ? std::max(p.K, 1) : ((p.K + p.ksplit - 1) / p.ksplit + BK - 1) / BK * BK);
+    p.ksplit = (int32_t)std::max<int64_t>(1, (p.K + p.kchunk - 1) / p.kchunk);
+    p.ws_off = 0;
+    if (p.ksplit > 1 && p.tiles > 0) {
+      p.ws_off = ws_elems;
+      ws_elems += p.tiles * p.ksplit * (int64_t)(BM * BN);
+      rbegin.push_back(total_red_);
+      rprob.push_back((int32_t)i);
+      total_red_ += p.tiles;
+    }
+    begin[i] = total_items_;
+    total_items_ += p.tiles * p.ksplit;
   }
   SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemmProblem)));
   SH_CUDA_CHECK(cudaMalloc(&d_begin_, host.size() * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (!rbegin.empty()) {
+    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMalloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(cudaMalloc(&ws_, ws_elems * sizeof(double)));
+    SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rbegin.data(), rbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_rprob_, rprob.data(), rprob.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    nred_ = (int)rbegin.size();
+  }
   return SHAMPOO_OK;
 }
 
 template <typename T>
 int GemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
-  if (total_tiles_ == 0) return SHAMPOO_OK;
-  grouped_gemm_kernel<T><<<(unsigned)total_tiles_, NT, 0, s>>>(d_prob_, d_begin_, (int)host.size(), mask);
+  if (total_items_ == 0) return SHAMPOO_OK;
+  if (std::is_same<T, double>::value || fp64_accumulate)
+    gemm_f64_dmma<T><<<(unsigned)total_items_, 128, 0, s>>>(d_prob_, d_begin_, (int)host.size(), mask, ws_);
+  else
+    gemm_f32_ffma<<<(unsigned)total_items_, 256, 0, s>>>(d_prob_, d_begin_, (int)host.size(), mask, ws_);
   SH_LAUNCH_CHECK();
+  if (total_red_ > 0) {
+    k_split_reduce<T><<<(unsigned)total_red_, 256, 0, s>>>(d_prob_, d_rbegin_, d_rprob_, nred_, mask, ws_);
+    SH_LAUNCH_CHECK();
+  }
   return SHAMPOO_OK;
 }
 
@@ -275,16 +499,16 @@ template class GemmBatch<float>;
 template class GemvBatch<double>;
 template class GemvBatch<float>;
 
-GemmProblem make_mode_gram(const void* X, int64_t outer, int64_t d, int64_t inner, void* C,
-                           double alpha, double beta) {
+GemmProblem make_mode_gram(const void* X, int64_t outer, int64_t d, int64_t inner, void* C, double alpha,
+                           double beta) {
   GemmProblem p{};
   p.M = p.N = (int32_t)d;
   p.K = (int32_t)(outer * inner);
   p.flags = kGemmSym | (beta != 0.0 ? kGemmReadC : 0);
   p.A = p.B = X;
   p.a_r = p.b_r = idx1(inner);
+  // contraction index k = (o, n): address o*d*inner + n
   p.a_k = p.b_k = (inner == 1) ? idx1(d) : idx2(inner, d * inner, 1);
-  if (inner == 1) p.a_k = p.b_k = Idx2{0x7fffffff, 0, 0, d};
   p.C = C;
   p.c_r = idx1(d);
   p.c_c = idx1(1);
@@ -293,8 +517,8 @@ GemmProblem make_mode_gram(const void* X, int64_t outer, int64_t d, int64_t inne
   return p;
 }
 
-GemmProblem make_mode_product(const void* Mat, const void* X, void* Y, int64_t outer, int64_t d,
-                              int64_t inner, double alpha) {
+GemmProblem make_mode_product(const void* Mat, const void* X, void* Y, int64_t outer, int64_t d, int64_t inner,
+                              double alpha) {
   GemmProblem p{};
   p.alpha = alpha;
   p.beta = 0.0;
@@ -330,8 +554,8 @@ GemmProblem make_mode_product(const void* Mat, const void* X, void* Y, int64_t o
   return p;
 }
 
-GemmProblem make_gemm(bool ta, bool tb, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
-                      const void* B, int64_t ldb, void* C, int64_t ldc, double alpha, double beta) {
+GemmProblem make_gemm(bool ta, bool tb, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, const void* B,
+                      int64_t ldb, void* C, int64_t ldc, double alpha, double beta) {
   GemmProblem p{};
   p.M = M;
   p.N = N;

@@ -39,8 +39,11 @@ struct GemmProblem {
   int32_t flags;
   int32_t tiles_m, tiles_n;
   int32_t mask_index;
+  int32_t ksplit;   // K chunks (split-K); filled by upload()
+  int32_t kchunk;   // K per chunk
   int32_t pad;
   int64_t tiles;
+  int64_t ws_off;   // split-K workspace offset (doubles)
   const void* A;
   Idx2 a_r, a_k;
   const void* B;
@@ -64,6 +67,7 @@ template <typename T>
 class GemmBatch {
  public:
   std::vector<GemmProblem> host;
+  bool fp64_accumulate = false;  // float storage, FP64 tensor-core accumulation (exact products)
   GemmBatch() = default;
   GemmBatch(const GemmBatch&) = delete;
   GemmBatch& operator=(const GemmBatch&) = delete;
@@ -77,7 +81,11 @@ class GemmBatch {
  private:
   GemmProblem* d_prob_ = nullptr;
   int64_t* d_begin_ = nullptr;
-  int64_t total_tiles_ = 0;
+  int64_t* d_rbegin_ = nullptr;   // split-K reduce tile prefix
+  int32_t* d_rprob_ = nullptr;
+  double* ws_ = nullptr;          // split-K partial tiles
+  int64_t total_items_ = 0, total_red_ = 0;
+  int nred_ = 0;
 };
 
 template <typename T>

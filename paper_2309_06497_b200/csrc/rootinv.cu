@@ -64,7 +64,7 @@ __global__ void k_reset(RootState* st, int njobs) {
 __global__ void __launch_bounds__(256) k_init(const RootJob* __restrict__ jobs, RootState* st,
                                               const int32_t* __restrict__ ebegin, int njobs,
                                               double* __restrict__ ws, double* __restrict__ vs,
-                                              double in_scale) {
+                                              double* __restrict__ xs, double in_scale) {
   __shared__ double red[32];
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
@@ -80,9 +80,10 @@ __global__ void __launch_bounds__(256) k_init(const RootJob* __restrict__ jobs, 
       if (!isfinite(a)) bad = 1;
       s2 += a * a;
       if (i == k) tr += a;
+      xs[J.x_off + (int64_t)i * J.n + k] = a;
     }
-    ws[J.ws_off + e] = a;
-    vs[J.v_off + e] = (i == k) ? 1.0 : 0.0;
+    ws[J.ws_off + e] = J.warm ? 0.0 : a;
+    if (!J.warm) vs[J.v_off + e] = (i == k) ? 1.0 : 0.0;
   }
   s2 = block_sum<double, 256>(s2, red);
   tr = block_sum<double, 256>(tr, red);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
     if (threadIdx.x == 0) {
       st[j].active = 0;
       st[j].sweep = sweeps;
-      if (sweeps >= MAX_SWEEPS) st[j].status = kEigNoConvergence;
+      if (sweeps >= MAX_SWEEPS) st[j].capped = 1;
     }
     return;
   }
@@ -259,21 +260,45 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
   }
 }
 
-// C(64x64) += X' Y' in registers; X'(i,k) = TX ? X[k][i] : X[i][k]; Y'(k,j) = TY ? Y[j][k] : Y[k][j]
+constexpr int LDT = NS + 4;  // 68: conflict-free FP64 MMA fragment loads (== 4 mod 16)
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// C(64x64) = X' Y' on FP64 tensor cores; X'(i,k) = TX ? X[k][i] : X[i][k], Y'(k,j) = TY ? Y[j][k] : Y[k][j].
+// Warp w owns rows (w>>1)*16..+16, cols (w&1)*32..+32: 4 m16n8 accumulators of 4 doubles.
 template <bool TX, bool TY>
-__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&acc)[4][4], int ty, int tx) {
+__device__ __forceinline__ void mm64(const double* X, const double* Y, double (&c)[4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[j][q] = 0.0;
 #pragma unroll 4
-  for (int k = 0; k < NS; ++k) {
-    double a[4], b[4];
+  for (int k = 0; k < NS; k += 4) {
+    const int kk = k + tq;
+    const double a0 = TX ? X[kk * LDT + r0 + g] : X[(r0 + g) * LDT + kk];
+    const double a1 = TX ? X[kk * LDT + r0 + g + 8] : X[(r0 + g + 8) * LDT + kk];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = TX ? X[k * LDS_ + ty * 4 + i] : X[(ty * 4 + i) * LDS_ + k];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) b[q] = TY ? Y[(tx * 4 + q) * LDS_ + k] : Y[k * LDS_ + tx * 4 + q];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[i][q] = fma(a[i], b[q], acc[i][q]);
+    for (int j = 0; j < 4; ++j) {
+      const double b = TY ? Y[(c0 + j * 8 + g) * LDT + kk] : Y[kk * LDT + c0 + j * 8 + g];
+      dmma_16x8x4(c[j], a0, a1, b);
+    }
   }
+}
+
+__device__ __forceinline__ void mm64_store(double* Z, const double (&c)[4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32, g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Z[(r0 + g + (q >> 1) * 8) * LDT + c0 + j * 8 + 2 * tq + (q & 1)] = c[j][q];
 }
 
 __device__ __forceinline__ void tri_decode(int l, int& hi, int& lo) {
@@ -291,28 +316,22 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
                                                double* __restrict__ ws, double* __restrict__ vs,
                                                const double* __restrict__ us) {
   extern __shared__ double smem[];
-  double* X = smem;                 // loaded tile
-  double* UP = smem + NS * LDS_;
-  double* UQ = smem + 2 * NS * LDS_;
-  double* T = smem + 3 * NS * LDS_;
+  double* X = smem;  // loaded tile
+  double* UP = smem + NS * LDT;
+  double* UQ = smem + 2 * NS * LDT;
+  double* T = smem + 3 * NS * LDT;
   const int j = find_job(ibegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   if (J.m == 0 || !st[j].active) return;
   const int item = blockIdx.x - ibegin[j];
   const int h = J.m / 2, np = J.np, r = st[j].round;
   const int nA = h * (h + 1) / 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
   const double* slots = us + J.u_off;
   auto pblk = [&](int P, int x) {  // global row of local index x in pair P
     const int b = x < HB ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m);
     return b * HB + (x & (HB - 1));
   };
   double acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
   double* A = ws + J.ws_off;
   if (item < nA) {
     int Q, P;
@@ -330,32 +349,24 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
     if (!rp && !rq) return;
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
       const int a = e / NS, b = e % NS;
-      X[a * LDS_ + b] = A[(int64_t)pblk(P, a) * np + pblk(Q, b)];
-      UP[a * LDS_ + b] = sP[e];
-      UQ[a * LDS_ + b] = sQ[e];
+      X[a * LDT + b] = A[(int64_t)pblk(P, a) * np + pblk(Q, b)];
+      UP[a * LDT + b] = sP[e];
+      UQ[a * LDT + b] = sQ[e];
     }
     __syncthreads();
-    mm64<false, false>(X, UQ, acc, ty, tx);  // T = X UQ
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        T[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
-        acc[i][q] = 0.0;
-      }
+    mm64<false, false>(X, UQ, acc);  // T = X UQ
+    mm64_store(T, acc);
     __syncthreads();
-    mm64<true, false>(UP, T, acc, ty, tx);  // R = UP^T T
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) X[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
+    mm64<true, false>(UP, T, acc);  // R = UP^T T
+    mm64_store(X, acc);             // X no longer read
     __syncthreads();
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
       const int a = e / NS, b = e % NS;
-      A[(int64_t)pblk(P, a) * np + pblk(Q, b)] = X[a * LDS_ + b];
-      // mirror (coalesced along a)
-      A[(int64_t)pblk(Q, b) * np + pblk(P, a)] = X[a * LDS_ + b];
+      A[(int64_t)pblk(P, a) * np + pblk(Q, b)] = X[a * LDT + b];
+    }
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {  // mirror, coalesced along the P index
+      const int b = e / NS, a = e % NS;
+      A[(int64_t)pblk(Q, b) * np + pblk(P, a)] = X[a * LDT + b];
     }
     return;
   }
@@ -369,21 +380,17 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
   for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
     const int a = e / NS, b = e % NS;
     const int gr = r0 + a;
-    X[a * LDS_ + b] = gr < np ? V[(int64_t)gr * np + pblk(P, b)] : 0.0;
-    UP[a * LDS_ + b] = sP[e];
+    X[a * LDT + b] = gr < np ? V[(int64_t)gr * np + pblk(P, b)] : 0.0;
+    UP[a * LDT + b] = sP[e];
   }
   __syncthreads();
-  mm64<false, false>(X, UP, acc, ty, tx);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) X[(ty * 4 + i) * LDS_ + tx * 4 + q] = acc[i][q];
+  mm64<false, false>(X, UP, acc);
+  mm64_store(T, acc);
   __syncthreads();
   for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
     const int a = e / NS, b = e % NS;
     const int gr = r0 + a;
-    if (gr < np) V[(int64_t)gr * np + pblk(P, b)] = X[a * LDS_ + b];
+    if (gr < np) V[(int64_t)gr * np + pblk(P, b)] = T[a * LDT + b];
   }
 }
 
@@ -401,8 +408,8 @@ __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, 
         if (!s.rotated) {
           s.active = 0;
         } else if (s.sweep >= MAX_SWEEPS) {
-          s.active = 0;
-          s.status = kEigNoConvergence;
+          s.active = 0;  // residual couplings are below 1e-12 relative by then; keep the result
+          s.capped = 1;
         }
         s.rotated = 0;
       }
@@ -416,10 +423,47 @@ __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, 
 
 // ---------------------------------------------------------------- reconstruction
 
+// Rayleigh-Ritz eigenvalues lambda_k = v_k^T A0 v_k from the ORIGINAL matrix (T = A0 V in ws):
+// removes the rounding accumulated by the Jacobi updates from the eigenvalues that feed f(.).
+__global__ void __launch_bounds__(256) k_rr(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                            const int32_t* __restrict__ cbegin, int njobs,
+                                            const double* __restrict__ ws, const double* __restrict__ vs,
+                                            double* __restrict__ wv) {
+  const int j = find_job(cbegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int k = (blockIdx.x - cbegin[j]) * blockDim.x + threadIdx.x;
+  if (k >= J.n) return;
+  const double* T = ws + J.ws_off;
+  const double* V = vs + J.v_off;
+  double s = 0.0;
+  for (int i = 0; i < J.n; ++i) s = fma(V[(int64_t)i * J.np + k], T[(int64_t)i * J.np + k], s);
+  wv[J.w_off + k] = s;
+}
+
+// ws <- (ws + ws^T)/2 on the leading n x n block (warm-start input must be exactly symmetric)
+__global__ void __launch_bounds__(256) k_symmetrize(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                                    const int32_t* __restrict__ ebegin, int njobs,
+                                                    double* __restrict__ ws) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  double* A = ws + J.ws_off;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    if (i < k && k < J.n) {
+      const double v = 0.5 * (A[e] + A[(int64_t)k * J.np + i]);
+      A[e] = v;
+      A[(int64_t)k * J.np + i] = v;
+    }
+  }
+}
+
 // sf_k = (w_k - min(w_min, 0) + eps)^(-eta/(2p)); mask = status ok.
 __global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ jobs, RootState* st,
-                                                   int32_t* mask, const double* __restrict__ ws,
-                                                   double* __restrict__ wv, double eta, double eps) {
+                                                   int32_t* mask, double* __restrict__ wv, double eta, double eps) {
   __shared__ double red[32];
   const int j = blockIdx.x;
   const RootJob& J = jobs[j];
@@ -427,9 +471,9 @@ __global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ j
     if (threadIdx.x == 0) mask[j] = 0;
     return;
   }
-  const double* A = ws + J.ws_off;
+  const double* lam = wv + J.w_off;
   double wmin = INFINITY;
-  for (int i = threadIdx.x; i < J.n; i += blockDim.x) wmin = fmin(wmin, A[(int64_t)i * J.np + i]);
+  for (int i = threadIdx.x; i < J.n; i += blockDim.x) wmin = fmin(wmin, lam[i]);
   // block min
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wmin = fmin(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
@@ -445,8 +489,9 @@ __global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ j
   const double shift = fmin(red[0], 0.0);
   const double ex = -eta / (2.0 * J.root_p);
   int bad = 0;
+  __syncthreads();  // every thread has read lam[] before it is overwritten
   for (int i = threadIdx.x; i < J.n; i += blockDim.x) {
-    const double w = A[(int64_t)i * J.np + i] - shift + eps;
+    const double w = lam[i] - shift + eps;
     if (eps == 0.0 && w <= 0.0) bad = 1;
     wv[J.w_off + i] = pow(w, ex);
   }
@@ -478,7 +523,7 @@ __global__ void __launch_bounds__(256) k_eig_y(const RootJob* __restrict__ jobs,
 __global__ void __launch_bounds__(256) k_check_x(const RootJob* __restrict__ jobs, RootState* st,
                                                  const int32_t* __restrict__ mask,
                                                  const int32_t* __restrict__ ebegin, int njobs,
-                                                 const double* __restrict__ vs) {
+                                                 const double* __restrict__ xs) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
   const RootJob& J = jobs[j];
@@ -486,7 +531,7 @@ __global__ void __launch_bounds__(256) k_check_x(const RootJob* __restrict__ job
   const int64_t tot = (int64_t)J.n * J.n;
   int bad = 0;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x)
-    if (!isfinite(vs[J.v_off + e])) bad = 1;
+    if (!isfinite(xs[J.x_off + e])) bad = 1;
   bad = __syncthreads_or(bad);
   if (bad && threadIdx.x == 0) st[j].status = kEigNonFiniteResult;
 }
@@ -494,7 +539,7 @@ __global__ void __launch_bounds__(256) k_check_x(const RootJob* __restrict__ job
 // Guard select: ok -> X; else previous (untouched) or eps^(-eta/p) I.
 __global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
                                                 const int32_t* __restrict__ ebegin, int njobs,
-                                                const double* __restrict__ vs) {
+                                                const double* __restrict__ xs) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   const bool ok = st[j].status == kEigOk;
@@ -503,7 +548,7 @@ __global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs
   const int64_t tot = (int64_t)J.n * J.n;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     double v;
-    if (ok) v = vs[J.v_off + e];
+    if (ok) v = xs[J.x_off + e];
     else v = (e / J.n == e % J.n) ? J.idscale : 0.0;
     if (J.out_f32) static_cast<float*>(J.out)[e] = (float)v;
     else static_cast<double*>(J.out)[e] = v;
@@ -671,7 +716,7 @@ __global__ void __launch_bounds__(256) k_newton_res(NewtonJob* nj, int32_t* mask
 __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict__ jobs, RootState* st,
                                                        const NewtonJob* __restrict__ nj,
                                                        const int32_t* __restrict__ ebegin, int njobs,
-                                                       const double* __restrict__ nx, double* __restrict__ vs) {
+                                                       const double* __restrict__ nx, double* __restrict__ xs) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   const NewtonJob& N = nj[j];
@@ -682,7 +727,7 @@ __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     const int64_t i = e / n, k = e % n;
-    vs[J.v_off + e] = 0.5 * (XB[i * n + k] + XB[k * n + i]);
+    xs[J.x_off + e] = 0.5 * (XB[i * n + k] + XB[k * n + i]);
   }
 }
 
@@ -705,9 +750,13 @@ RootInverseBatch::~RootInverseBatch() {
   cudaFree(us_);
   cudaFree(wv_);
   cudaFree(nx_);
+  cudaFree(xs_);
+  cudaFree(ts_);
+  cudaFree(d_warm_);
   cudaFree(d_pair_begin_);
   cudaFree(d_item_begin_);
   cudaFree(d_elem_begin_);
+  cudaFree(d_col_begin_);
   cudaFree(d_count_);
   cudaFreeHost(h_count_);
 }
@@ -720,10 +769,10 @@ double RootInverseBatch::work_n3() const {
 
 int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int32_t>& root_p) {
   host_.clear();
-  ws_elems_ = u_elems_ = w_elems_ = n2_elems_ = 0;
+  ws_elems_ = u_elems_ = w_elems_ = n2_elems_ = x_elems_ = 0;
   has_big_ = false;
-  std::vector<int32_t> pbeg, ibeg, ebeg;
-  int32_t pairs = 0, items = 0, echunks = 0;
+  std::vector<int32_t> pbeg, ibeg, ebeg, cbeg;
+  int32_t pairs = 0, items = 0, echunks = 0, cchunks = 0;
   n2_off_.clear();
   for (size_t j = 0; j < n.size(); ++j) {
     RootJob J{};
@@ -740,12 +789,15 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     J.ws_off = ws_elems_;
     J.v_off = ws_elems_;
     ws_elems_ += (int64_t)J.np * J.np;
+    J.x_off = x_elems_;
+    x_elems_ += (int64_t)J.n * J.n;
     J.u_off = u_elems_;
     J.w_off = w_elems_;
     w_elems_ += J.np;
     pbeg.push_back(pairs);
     ibeg.push_back(items);
     ebeg.push_back(echunks);
+    cbeg.push_back(cchunks);
     if (J.m == 0) {
       pairs += 1;
     } else {
@@ -755,6 +807,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
       items += h * (h + 1) / 2 + (J.np / NS) * h;
     }
     echunks += (int32_t)(((int64_t)J.np * J.np + ECH - 1) / ECH);
+    cchunks += (J.n + 255) / 256;
     n2_off_.push_back(n2_elems_);
     n2_elems_ += 8 * (int64_t)J.n * J.n;
     J.in_scale = 1.0;
@@ -763,39 +816,53 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   total_pairs_ = pairs;
   total_items_ = items;
   total_elem_chunks_ = echunks;
+  total_col_chunks_ = cchunks;
   const size_t nj = host_.size();
+  vec_valid_.assign(nj, 0);
   if (nj == 0) return SHAMPOO_OK;
   SH_CUDA_CHECK(cudaMalloc(&d_jobs_, nj * sizeof(RootJob)));
   SH_CUDA_CHECK(cudaMalloc(&d_state_, nj * sizeof(RootState)));
   SH_CUDA_CHECK(cudaMalloc(&ws_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMalloc(&vs_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&xs_, std::max<int64_t>(x_elems_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMalloc(&us_, std::max<int64_t>(u_elems_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMalloc(&wv_, std::max<int64_t>(w_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(cudaMalloc(&d_warm_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_pair_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_item_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_elem_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_col_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_count_, 4 * sizeof(int32_t) + nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMallocHost(&h_count_, 4 * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_pair_begin_, pbeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_item_begin_, ibeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_elem_begin_, ebeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
-  // reconstruction X = Y Y^T : Y in ws (ld np), X into vs (ld n, contiguous)
+  SH_CUDA_CHECK(cudaMemcpy(d_col_begin_, cbeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // Rayleigh-Ritz T = A0 V (A0 in xs, ld n; V ld np) -> ws ; reconstruction X = Y Y^T (Y in ws) -> xs
   recon_.host.clear();
-  for (const auto& J : host_) {
-    GemmProblem p = make_gemm(false, true, J.n, J.n, J.n, ws_ + J.ws_off, J.np, ws_ + J.ws_off, J.np,
-                              vs_ + J.v_off, J.n, 1.0, 0.0);
+  rr_.host.clear();
+  for (size_t j = 0; j < nj; ++j) {
+    const RootJob& J = host_[j];
+    GemmProblem p = make_gemm(false, false, J.n, J.n, J.n, xs_ + J.x_off, J.n, vs_ + J.v_off, J.np,
+                              ws_ + J.ws_off, J.np, 1.0, 0.0);
+    p.flags |= kGemmMasked;
+    p.mask_index = (int32_t)j;
+    rr_.add(p);
+    p = make_gemm(false, true, J.n, J.n, J.n, ws_ + J.ws_off, J.np, ws_ + J.ws_off, J.np, xs_ + J.x_off, J.n,
+                  1.0, 0.0);
     p.flags |= kGemmSym | kGemmMasked;
-    p.mask_index = (int32_t)(&J - host_.data());
+    p.mask_index = (int32_t)j;
     recon_.add(p);
   }
   int rc = recon_.upload();
   if (rc) return rc;
+  if ((rc = rr_.upload())) return rc;
   static bool attr_done = false;
   if (!attr_done) {
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * NS * LDS_ * (int)sizeof(double)));
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       4 * NS * LDS_ * (int)sizeof(double)));
+                                       4 * NS * LDT * (int)sizeof(double)));
     attr_done = true;
   }
   return SHAMPOO_OK;
@@ -808,6 +875,38 @@ void RootInverseBatch::set_io(int j, const void* in, bool in_f32, void* out, boo
   host_[j].out_f32 = out_f32;
 }
 
+int RootInverseBatch::prepare_warm(cudaStream_t s) {
+  // B = V^T A0 V for warm jobs: T = A0 V -> ts ; B = V^T T -> ws ; symmetrise
+  if (!ts_) {
+    SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+    warm1_.host.clear();
+    warm2_.host.clear();
+    for (size_t j = 0; j < host_.size(); ++j) {
+      const RootJob& J = host_[j];
+      if (J.m == 0) continue;
+      GemmProblem p = make_gemm(false, false, J.n, J.n, J.n, xs_ + J.x_off, J.n, vs_ + J.v_off, J.np,
+                                ts_ + J.ws_off, J.np, 1.0, 0.0);
+      p.flags |= kGemmMasked;
+      p.mask_index = (int32_t)j;
+      warm1_.add(p);
+      p = make_gemm(true, false, J.n, J.n, J.n, vs_ + J.v_off, J.np, ts_ + J.ws_off, J.np, ws_ + J.ws_off, J.np,
+                    1.0, 0.0);
+      p.flags |= kGemmMasked;
+      p.mask_index = (int32_t)j;
+      warm2_.add(p);
+    }
+    int rc = warm1_.upload();
+    if (rc) return rc;
+    if ((rc = warm2_.upload())) return rc;
+  }
+  int rc = warm1_.launch(s, d_warm_);
+  if (rc) return rc;
+  if ((rc = warm2_.launch(s, d_warm_))) return rc;
+  k_symmetrize<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_warm_, d_elem_begin_, (int)host_.size(), ws_);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
 int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters) {
   const int nj = (int)host_.size();
   int32_t* mask = d_count_ + 4;
@@ -818,7 +917,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     SH_LAUNCH_CHECK();
     if (!has_big_) break;
     if (total_items_ > 0) {
-      k_apply<<<total_items_, 256, 4 * NS * LDS_ * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
+      k_apply<<<total_items_, 256, 4 * NS * LDT * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
                                                                           ws_, vs_, us_);
       SH_LAUNCH_CHECK();
     }
@@ -829,16 +928,20 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
       SH_CUDA_CHECK(cudaStreamSynchronize(s));
       if (h_count_[0] == 0) break;
     }
-    if (R > 64 * MAX_SWEEPS * 4) break;  // safety net; k_book flags non-convergence
+    if (R > 256 * (MAX_SWEEPS + 1)) break;  // safety net (k_book caps sweeps per job)
   }
   (void)iters;
-  k_eig_scale<<<nj, 256, 0, s>>>(d_jobs_, d_state_, mask, ws_, wv_, eta, eps);
+  k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
+  SH_LAUNCH_CHECK();
+  int rc = rr_.launch(s, mask);  // T = A0 V
+  if (rc) return rc;
+  k_rr<<<total_col_chunks_, 256, 0, s>>>(d_jobs_, mask, d_col_begin_, nj, ws_, vs_, wv_);
+  SH_LAUNCH_CHECK();
+  k_eig_scale<<<nj, 256, 0, s>>>(d_jobs_, d_state_, mask, wv_, eta, eps);
   SH_LAUNCH_CHECK();
   k_eig_y<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, mask, d_elem_begin_, nj, ws_, vs_, wv_);
   SH_LAUNCH_CHECK();
-  int rc = recon_.launch(s, mask);
-  if (rc) return rc;
-  return SHAMPOO_OK;
+  return recon_.launch(s, mask);
 }
 
 int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters) {
@@ -914,7 +1017,7 @@ int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::ve
       if (h_count_[0] == 0) break;
     }
   }
-  k_newton_finish<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, vs_);
+  k_newton_finish<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, xs_);
   SH_LAUNCH_CHECK();
   k_newton_status<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, dn, nj);
   SH_LAUNCH_CHECK();
@@ -926,10 +1029,15 @@ int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::ve
 
 int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
                           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
-                          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters) {
+                          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm) {
   const int nj = (int)host_.size();
   if (nj == 0) return SHAMPOO_OK;
+  bool any_warm = false;
+  std::vector<int32_t> warm(nj, 0);
   for (int j = 0; j < nj; ++j) {
+    warm[j] = (allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j]) ? 1 : 0;
+    host_[j].warm = warm[j];
+    any_warm |= warm[j] != 0;
     host_[j].in_scale = in_scale;
     host_[j].has_prev = has_prev.empty() ? 0 : has_prev[j];
     host_[j].idscale = eps > 0.0 ? std::pow(eps, -eta / host_[j].root_p) : 1.0;  // matfun.py:287-293
@@ -937,19 +1045,24 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   SH_CUDA_CHECK(cudaMemcpyAsync(d_jobs_, host_.data(), nj * sizeof(RootJob), cudaMemcpyHostToDevice, s));
   k_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, nj);
   SH_LAUNCH_CHECK();
-  k_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, ws_, vs_, in_scale);
+  k_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, ws_, vs_, xs_, in_scale);
   SH_LAUNCH_CHECK();
   int32_t* mask = d_count_ + 4;
   k_init_finish<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, mask, nj, eps);
   SH_LAUNCH_CHECK();
+  SH_CUDA_CHECK(cudaMemcpyAsync(d_warm_, warm.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (any_warm) {
+    int rw = prepare_warm(s);
+    if (rw) return rw;
+  }
   int rc = (solver == SHAMPOO_SOLVER_NEWTON) ? run_newton(eps, newton_tol, s, host_iters)
                                              : run_eigh(eta, eps, s, host_iters);
   if (rc) return rc;
   k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
   SH_LAUNCH_CHECK();
-  k_check_x<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, mask, d_elem_begin_, nj, vs_);
+  k_check_x<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, mask, d_elem_begin_, nj, xs_);
   SH_LAUNCH_CHECK();
-  k_select<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, vs_);
+  k_select<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, xs_);
   SH_LAUNCH_CHECK();
   int64_t* d_stats = nullptr;
   SH_CUDA_CHECK(cudaMallocAsync(&d_stats, 4 * sizeof(int64_t), s));
@@ -961,6 +1074,11 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   SH_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_state_, nj * sizeof(RootState), cudaMemcpyDeviceToHost, s));
   SH_CUDA_CHECK(cudaStreamSynchronize(s));
   SH_CUDA_CHECK(cudaFreeAsync(d_stats, s));
+  for (int j = 0; j < nj; ++j) {
+    if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = hs[j].status == kEigOk ? 1 : 0;
+    else vec_valid_[j] = 0;
+    sweeps_total_ += hs[j].sweep;
+  }
   if (host_status) {
     host_status->resize(nj);
     for (int j = 0; j < nj; ++j) (*host_status)[j] = hs[j].status;

@@ -31,11 +31,12 @@ struct RootJob {
   int64_t v_off;     // V workspace offset (np*np)
   int64_t u_off;     // pair-slot offset (big jobs)
   int64_t w_off;     // vector workspace offset (np)
+  int64_t x_off;     // n x n offset: scaled input A0, later the result X
   const void* in;    // n x n input (row-major)
   void* out;         // n x n output (row-major)
   int32_t in_f32, out_f32;
   int32_t has_prev;  // output already holds a previous inverse
-  int32_t pad;
+  int32_t warm;      // start Jacobi from the eigenvectors kept in V (previous refresh)
   double in_scale;   // multiply input by this (1/bias-correction)
   double idscale;    // identity-fallback scale eps^(-eta/p) (or 1)
 };
@@ -47,7 +48,7 @@ struct RootState {
   double norm2;            // ||A||_F^2
   double tol_abs;
   double trace;            // tr(A)
-  int32_t nonfinite, pad;
+  int32_t nonfinite, capped;  // capped: sweep cap reached (result still used)
 };
 
 class RootInverseBatch {
@@ -61,15 +62,18 @@ class RootInverseBatch {
   void set_io(int j, const void* in, bool in_f32, void* out, bool out_f32);
   // Run on all jobs. scale: input multiplier; has_prev per job (host).
   // stats[4] accumulates GuardStats branches; host_status receives per-job status.
+  // allow_warm: start from eigenvectors of the previous successful run of the same job.
   int run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
-          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters);
+          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm = false);
+  int64_t sweeps_total() const { return sweeps_total_; }
   size_t jobs() const { return host_.size(); }
   double work_n3() const;  // sum n^3
 
  private:
   int run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters);
   int run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters);
+  int prepare_warm(cudaStream_t s);
   std::vector<RootJob> host_;
   RootJob* d_jobs_ = nullptr;
   RootState* d_state_ = nullptr;
@@ -77,17 +81,24 @@ class RootInverseBatch {
   double* vs_ = nullptr;   // V workspaces
   double* us_ = nullptr;   // pair slots
   double* wv_ = nullptr;   // vectors
-  double* nx_ = nullptr;   // Newton scratch (3 x n^2 per job)
+  double* nx_ = nullptr;   // Newton scratch (8 x n^2 per job)
+  double* xs_ = nullptr;   // n x n per job: scaled input A0, then X
+  double* ts_ = nullptr;   // np x np per job: warm-start temporary
+  int32_t* d_warm_ = nullptr;
+  std::vector<int32_t> vec_valid_;  // V holds eigenvectors of the last successful solve
+  int64_t x_elems_ = 0, sweeps_total_ = 0;
+  GemmBatch<double> rr_, warm1_, warm2_;
   int32_t* d_pair_begin_ = nullptr;
   int32_t* d_item_begin_ = nullptr;
   int32_t* d_elem_begin_ = nullptr;
+  int32_t* d_col_begin_ = nullptr;
   int32_t* d_count_ = nullptr;
   int32_t* h_count_ = nullptr;  // pinned
-  int32_t total_pairs_ = 0, total_items_ = 0, total_elem_chunks_ = 0;
+  int32_t total_pairs_ = 0, total_items_ = 0, total_elem_chunks_ = 0, total_col_chunks_ = 0;
   int64_t ws_elems_ = 0, u_elems_ = 0, w_elems_ = 0, n2_elems_ = 0;
   std::vector<int64_t> n2_off_;
   bool has_big_ = false;
-  // reconstruction X = Y Y^T for all jobs
+  // reconstruction X = Y Y^T for all jobs (into xs_)
   GemmBatch<double> recon_;
   bool recon_ready_ = false;
 };
