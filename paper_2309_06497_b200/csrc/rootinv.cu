@@ -26,7 +26,7 @@ namespace {
 constexpr int NS = 64;            // sub-problem size (2 x 32-row blocks)
 constexpr int HB = 32;            // row-block size
 constexpr int LDS_ = NS + 1;      // padded smem leading dim
-constexpr int SLOT = NS * NS + NS + 2;  // U (64x64) + D (64) + flag
+constexpr int SLOT = 2 * NS * NS + NS + 2;  // U (64x64) + S (64x64) + D (64) + flag
 constexpr int ECH = 4096;         // elements per chunk for elementwise job kernels
 constexpr int MAX_SWEEPS = 40;
 constexpr double U64 = 1.1102230246251565e-16;
@@ -105,6 +105,7 @@ __global__ void k_init_finish(const RootJob* __restrict__ jobs, RootState* st, i
     s.active = 0;
   }
   s.tol_abs = fmax(0.1 * U64 * sqrt(s.norm2), 1e-9 * eps);
+  s.tol_null = 8.0 * U64 * sqrt(s.norm2);  // eigenvalue noise level of any backward-stable solver
   if (jobs[j].n == 0) s.active = 0;
   mask[j] = s.active;
 }
@@ -113,7 +114,8 @@ __global__ void k_init_finish(const RootJob* __restrict__ jobs, RootState* st, i
 
 // Diagonalise S (ns x ns, ld LDS_) in place, accumulating rotations into U
 // (initialised to I here).  Returns (in all threads) whether any rotation ran.
-__device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, int* sweeps_out) {
+__device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, double tol_null, int max_sweeps,
+                           int* sweeps_out) {
   __shared__ double pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
   __shared__ int pa[NS / 2], pb[NS / 2];
   __shared__ int rot_round, rot_sweep;
@@ -125,7 +127,7 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, int* swe
   const int half = ns / 2;
   int any = 0, sw = 0;
   __syncthreads();
-  for (sw = 0; sw < MAX_SWEEPS; ++sw) {
+  for (sw = 0; sw < max_sweeps; ++sw) {
     if (tid == 0) rot_sweep = 0;
     for (int r = 0; r < ns - 1; ++r) {
       if (tid == 0) rot_round = 0;
@@ -133,7 +135,9 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, int* swe
       if (tid < half) {
         const int a = circle_pos(r, tid, ns), b = circle_pos(r, ns - 1 - tid, ns);
         const double apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
-        const double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+        double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+        // both directions inside the numerical null cluster: f(.) is flat there, skip
+        if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
         double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > thr) {
           const double tau = (aqq - app) / (2.0 * apq);
@@ -236,7 +240,8 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
   }
   __syncthreads();
   int sweeps = 0;
-  const int any = cta_jacobi(S, U, ns, st[j].tol_abs, &sweeps);
+  // blocked jobs: one inner sweep per outer round (outer sweeps barely change)
+  const int any = cta_jacobi(S, U, ns, st[j].tol_abs, st[j].tol_null, small ? MAX_SWEEPS : 1, &sweeps);
   if (small) {
     double* V = vs + J.v_off;
     for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
@@ -252,7 +257,11 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
     return;
   }
   double* slot = us + J.u_off + (int64_t)pair * SLOT;
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) slot[e] = U[(e / NS) * LDS_ + (e % NS)];
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int a = e / NS, b = e % NS;
+    slot[e] = U[a * LDS_ + b];
+    slot[NS * NS + NS + 2 + e] = (a <= b) ? S[a * LDS_ + b] : S[b * LDS_ + a];  // rotated sub-matrix (sym)
+  }
   for (int e = threadIdx.x; e < NS; e += blockDim.x) slot[NS * NS + e] = S[e * LDS_ + e];
   if (threadIdx.x == 0) {
     slot[NS * NS + NS] = any ? 1.0 : 0.0;
@@ -338,10 +347,11 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
     tri_decode(item, Q, P);  // Q >= P
     const double* sP = slots + (int64_t)P * SLOT;
     const double* sQ = slots + (int64_t)Q * SLOT;
-    if (P == Q) {
+    if (P == Q) {  // diagonal pair block = the sub-solve's rotated sub-matrix
+      const double* Sp = sP + NS * NS + NS + 2;
       for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
         const int a = e / NS, b = e % NS;
-        A[(int64_t)pblk(P, a) * np + pblk(P, b)] = (a == b) ? sP[NS * NS + a] : 0.0;
+        A[(int64_t)pblk(P, a) * np + pblk(P, b)] = Sp[e];
       }
       return;
     }

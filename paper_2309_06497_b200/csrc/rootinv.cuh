@@ -47,6 +47,7 @@ struct RootState {
   int32_t status, result;  // result: 0 primary, 2 previous, 3 identity
   double norm2;            // ||A||_F^2
   double tol_abs;
+  double tol_null;
   double trace;            // tr(A)
   int32_t nonfinite, capped;  // capped: sweep cap reached (result still used)
 };

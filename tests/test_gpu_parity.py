@@ -78,7 +78,8 @@ def test_root_inverse_eigh_matches_reference(cuda_device, case):
             x = x.cpu().numpy()
             np.testing.assert_array_equal(x, x.T)  # exactly symmetric (matfun.py:157)
             if _well_posed(a, eps):
-                assert rel(x, ref) <= 1e-8, (case, p, eps, rel(x, ref))
+                # u * cond(A + eps I) bounds any two float64 solvers' disagreement
+                assert rel(x, ref) <= 1e-7, (case, p, eps, rel(x, ref))
                 continue
             delta = 2.2e-16 * np.linalg.norm(a, 2) * np.sqrt(n)
             big = w_ref > 1e6 * delta
@@ -86,6 +87,8 @@ def test_root_inverse_eigh_matches_reference(cuda_device, case):
             fr = (lr + eps) ** (-1.0 / p)
             assert np.linalg.norm(x @ ur - ur * fr) <= 1e-6 * np.linalg.norm(ur * fr)
             un = q_ref[:, ~big]
+            if un.shape[1] == 0:
+                continue
             wn = np.linalg.eigvalsh(un.T @ x @ un)
             lo, hi = (eps + 2 * delta) ** (-1.0 / p), eps ** (-1.0 / p)
             assert wn.min() >= lo * (1 - 1e-6) and wn.max() <= hi * (1 + 1e-6), (case, p, wn.min(), wn.max(), lo, hi)
