@@ -79,7 +79,6 @@ __device__ __forceinline__ void store_out(const GemmProblem& P, int tm, int tn, 
 
 // ---------------------------------------------------------------- FP64 DMMA kernel
 
-constexpr int LDA = BM + 4;  // 68 doubles
 
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -88,51 +87,118 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// 64 x 16 slab: 1024 elements, 8 per thread (128 threads)
+// Multi-stage cp.async pipeline.  Per operand and problem one of three copy modes:
+//   KVEC: k contiguous in global (and 16B aligned)  -> smem [row][k] (ld 20), 16-byte copies
+//   RVEC: rows contiguous in global (and aligned)   -> smem [k][row] (ld 68/72), 16-byte copies
+//   GEN : anything else (2-level or odd strides)    -> smem [k][row], element copies
+// Both smem layouts give conflict-free MMA fragment reads (ld == 4 mod 16 doubles / 20 floats).
+constexpr int STAGES = 3;
+enum CopyMode : int { kGen = 0, kKvec = 1, kRvec = 2 };
+
 template <typename T>
-__device__ __forceinline__ void load_slab64(const T* __restrict__ X, const Idx2& xr, const Idx2& xk, int rows,
-                                            int kend, int r0, int k0, bool kfast, double (&v)[8]) {
+struct SmemTile {
+  static constexpr int LDR = sizeof(T) == 8 ? 68 : 72;  // [k][row]
+  static constexpr int LDK = 20;                         // [row][k]
+  static constexpr int ELEMS = (BM * LDK > BK * LDR) ? BM * LDK : BK * LDR;
+};
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct OperandCursor {
+  int mode;
+  int rows, r0;
+  int64_t row_off;  // GEN / KVEC: ev(xr, r0 + my row)
+  int row, k_lo;    // my slab row / first k
+  bool row_ok;
+};
+
+template <typename T>
+__device__ __forceinline__ int copy_mode(const void* base, const Idx2& xr, const Idx2& xk) {
+  constexpr int V = 16 / sizeof(T);  // elements per 16 bytes
+  const bool aligned = (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+  if (aligned && xk.div == 0x7fffffff && xk.lo == 1 && xr.div == 0x7fffffff && (xr.lo % V) == 0) return kKvec;
+  if (aligned && xr.div == 0x7fffffff && xr.lo == 1 && xk.div == 0x7fffffff && (xk.lo % V) == 0) return kRvec;
+  return kGen;
+}
+
+__device__ __forceinline__ OperandCursor make_cursor(int mode, const Idx2& xr, int rows, int r0) {
+  OperandCursor c;
   const int tid = threadIdx.x;
+  c.mode = mode;
+  c.rows = rows;
+  c.r0 = r0;
+  if (mode == kKvec) {  // 2 threads per row, 8 consecutive k each
+    c.row = tid >> 1;
+    c.k_lo = (tid & 1) * 8;
+  } else if (mode == kRvec) {  // 8 threads per k, 8 consecutive rows each
+    c.row = (tid & 7) * 8;
+    c.k_lo = tid >> 3;
+  } else {
+    c.row = tid & 63;
+    c.k_lo = tid >> 6;
+  }
+  const int gr = r0 + c.row;
+  c.row_ok = gr < rows;
+  c.row_off = (c.row_ok && mode != kRvec) ? ev(xr, gr) : 0;
+  return c;
+}
+
+template <typename T>
+__device__ __forceinline__ void issue_slab(T* S, const T* __restrict__ X, const Idx2& xr, const Idx2& xk,
+                                           const OperandCursor& c, int k0, int kend) {
+  constexpr int V = 16 / sizeof(T);
+  if (c.mode == kKvec) {
+    constexpr int LD = SmemTile<T>::LDK;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    int r, k;
-    if (kfast) {
-      const int f = tid * 8 + e;
-      r = f >> 4;
-      k = f & 15;
-    } else {
-      r = tid & 63;
-      k = (tid >> 6) + 2 * e;
+    for (int e = 0; e < 8; e += V) {
+      const int k = c.k_lo + e, gk = k0 + k;
+      const int valid = c.row_ok ? max(0, min(V, kend - gk)) : 0;
+      const T* src = valid ? X + c.row_off + gk : X;
+      cp_async(S + c.row * LD + k, src, 16, valid * (int)sizeof(T));
     }
-    const int gr = r0 + r, gk = k0 + k;
-    v[e] = (gr < rows && gk < kend) ? (double)X[ev(xr, gr) + ev(xk, gk)] : 0.0;
+  } else if (c.mode == kRvec) {
+    constexpr int LD = SmemTile<T>::LDR;
+    const int gk = k0 + c.k_lo;
+    const int64_t koff = (gk < kend) ? ev(xk, gk) : 0;
+#pragma unroll
+    for (int e = 0; e < 8; e += V) {
+      const int gr = c.r0 + c.row + e;
+      const int valid = (gk < kend) ? max(0, min(V, c.rows - gr)) : 0;
+      const T* src = valid ? X + koff + ev(xr, gr) : X;
+      cp_async(S + c.k_lo * LD + c.row + e, src, 16, valid * (int)sizeof(T));
+    }
+  } else {
+    constexpr int LD = SmemTile<T>::LDR;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = c.k_lo + 2 * e, gk = k0 + k;
+      const bool ok = c.row_ok && gk < kend;
+      const T* src = ok ? X + c.row_off + ev(xk, gk) : X;
+      cp_async(S + k * LD + c.row, src, (int)sizeof(T), ok ? (int)sizeof(T) : 0);
+    }
   }
 }
 
-__device__ __forceinline__ void store_slab64(double (*S)[LDA], bool kfast, const double (&v)[8]) {
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    int r, k;
-    if (kfast) {
-      const int f = tid * 8 + e;
-      r = f >> 4;
-      k = f & 15;
-    } else {
-      r = tid & 63;
-      k = (tid >> 6) + 2 * e;
-    }
-    S[k][r] = v[e];
-  }
-}
 
 // T: storage type of A/B/C (float inputs are widened; accumulation is always FP64).
 template <typename T>
 __global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restrict__ probs,
                                                      const int64_t* __restrict__ begin, int nprob,
                                                      const int32_t* __restrict__ mask, double* __restrict__ ws) {
-  __shared__ __align__(16) double As[2][BK][LDA];
-  __shared__ __align__(16) double Bs[2][BK][LDA];
+  constexpr int TILE = SmemTile<T>::ELEMS;  // elements per operand per stage
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
   const TileWork w = locate(probs, begin, nprob, blockIdx.x);
   const GemmProblem& P = probs[w.prob];
   if ((P.flags & kGemmMasked) && mask && mask[P.mask_index] == 0) return;
@@ -141,10 +207,16 @@ __global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restri
   const int kend = min(P.K, kbeg + P.kchunk);
   const T* __restrict__ A = static_cast<const T*>(P.A);
   const T* __restrict__ B = static_cast<const T*>(P.B);
-  const bool akf = (P.a_k.lo == 1), bkf = (P.b_k.lo == 1);
+  const int amode = copy_mode<T>(P.A, P.a_r, P.a_k), bmode = copy_mode<T>(P.B, P.b_r, P.b_k);
+  const OperandCursor ca = make_cursor(amode, P.a_r, P.M, m0);
+  const OperandCursor cb = make_cursor(bmode, P.b_r, P.N, n0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, tq = lane & 3;
+  // fragment addressing: element (row, k) at row*rs + k*ks of the operand's smem tile
+  const int a_rs = amode == kKvec ? SmemTile<T>::LDK : 1, a_ks = amode == kKvec ? 1 : SmemTile<T>::LDR;
+  const int b_rs = bmode == kKvec ? SmemTile<T>::LDK : 1, b_ks = bmode == kKvec ? 1 : SmemTile<T>::LDR;
+  const int a_base = (wm + g) * a_rs + tq * a_ks, b_base = (wn + g) * b_rs + tq * b_ks;
 
   double c[2][4][4];
 #pragma unroll
@@ -154,40 +226,45 @@ __global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restri
 #pragma unroll
       for (int q = 0; q < 4; ++q) c[i][j][q] = 0.0;
 
-  double ra[8], rb[8];
   const int nk = (kend - kbeg + BK - 1) / BK;
-  load_slab64(A, P.a_r, P.a_k, P.M, kend, m0, kbeg, akf, ra);
-  load_slab64(B, P.b_r, P.b_k, P.N, kend, n0, kbeg, bkf, rb);
-  store_slab64(As[0], akf, ra);
-  store_slab64(Bs[0], bkf, rb);
-  __syncthreads();
-  for (int kt = 0; kt < nk; ++kt) {
-    const int cur = kt & 1;
-    if (kt + 1 < nk) {
-      load_slab64(A, P.a_r, P.a_k, P.M, kend, m0, kbeg + (kt + 1) * BK, akf, ra);
-      load_slab64(B, P.b_r, P.b_k, P.N, kend, n0, kbeg + (kt + 1) * BK, bkf, rb);
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) {
+      issue_slab<T>(sm + (2 * st) * TILE, A, P.a_r, P.a_k, ca, kbeg + st * BK, kend);
+      issue_slab<T>(sm + (2 * st + 1) * TILE, B, P.b_r, P.b_k, cb, kbeg + st * BK, kend);
     }
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int cur = kt % STAGES;
+    const T* As = sm + (2 * cur) * TILE;
+    const T* Bs = sm + (2 * cur + 1) * TILE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[2][2], b[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        a[i][0] = As[cur][kk + tq][wm + i * 16 + g];
-        a[i][1] = As[cur][kk + tq][wm + i * 16 + g + 8];
+        a[i][0] = (double)As[a_base + (i * 16) * a_rs + kk * a_ks];
+        a[i][1] = (double)As[a_base + (i * 16 + 8) * a_rs + kk * a_ks];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[cur][kk + tq][wn + j * 8 + g];
+      for (int j = 0; j < 4; ++j) b[j] = (double)Bs[b_base + (j * 8) * b_rs + kk * b_ks];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_16x8x4(c[i][j], a[i][0], a[i][1], b[j]);
     }
-    if (kt + 1 < nk) {
-      store_slab64(As[cur ^ 1], akf, ra);
-      store_slab64(Bs[cur ^ 1], bkf, rb);
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) {
+      const int st = nxt % STAGES;
+      issue_slab<T>(sm + (2 * st) * TILE, A, P.a_r, P.a_k, ca, kbeg + nxt * BK, kend);
+      issue_slab<T>(sm + (2 * st + 1) * TILE, B, P.b_r, P.b_k, cb, kbeg + nxt * BK, kend);
     }
-    __syncthreads();
+    cp_commit();
   }
+  cp_wait<0>();
   if (P.ksplit > 1) {
     double* part = ws + P.ws_off + (w.tile * P.ksplit + w.split) * (BM * BN);
 #pragma unroll
@@ -210,6 +287,11 @@ __global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restri
         const int r = wm + i * 16 + g + (q >> 1) * 8, cc = wn + j * 8 + 2 * tq + (q & 1);
         store_out<T>(P, w.tm, w.tn, m0 + r, n0 + cc, c[i][j][q]);
       }
+}
+
+template <typename T>
+constexpr int dmma_smem_bytes() {
+  return STAGES * 2 * SmemTile<T>::ELEMS * (int)sizeof(T);
 }
 
 // ---------------------------------------------------------------- FP32 FFMA kernel
@@ -400,6 +482,14 @@ int GemmBatch<T>::upload() {
   ws_ = nullptr;
   total_items_ = total_red_ = 0;
   if (host.empty()) return SHAMPOO_OK;
+  static bool attr = false;
+  if (!attr) {
+    SH_CUDA_CHECK(cudaFuncSetAttribute(gemm_f64_dmma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dmma_smem_bytes<double>()));
+    SH_CUDA_CHECK(cudaFuncSetAttribute(gemm_f64_dmma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dmma_smem_bytes<float>()));
+    attr = true;
+  }
   std::vector<int64_t> begin(host.size()), rbegin;
   std::vector<int32_t> rprob;
   int64_t ws_elems = 0;
@@ -442,7 +532,8 @@ template <typename T>
 int GemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   if (total_items_ == 0) return SHAMPOO_OK;
   if (std::is_same<T, double>::value || fp64_accumulate)
-    gemm_f64_dmma<T><<<(unsigned)total_items_, 128, 0, s>>>(d_prob_, d_begin_, (int)host.size(), mask, ws_);
+    gemm_f64_dmma<T><<<(unsigned)total_items_, 128, dmma_smem_bytes<T>(), s>>>(d_prob_, d_begin_,
+                                                                           (int)host.size(), mask, ws_);
   else
     gemm_f32_ffma<<<(unsigned)total_items_, 256, 0, s>>>(d_prob_, d_begin_, (int)host.size(), mask, ws_);
   SH_LAUNCH_CHECK();
@@ -508,7 +599,7 @@ GemmProblem make_mode_gram(const void* X, int64_t outer, int64_t d, int64_t inne
   p.A = p.B = X;
   p.a_r = p.b_r = idx1(inner);
   // contraction index k = (o, n): address o*d*inner + n
-  p.a_k = p.b_k = (inner == 1) ? idx1(d) : idx2(inner, d * inner, 1);
+  p.a_k = p.b_k = (inner == 1) ? idx1(d) : (outer == 1 ? idx1(1) : idx2(inner, d * inner, 1));
   p.C = C;
   p.c_r = idx1(d);
   p.c_c = idx1(1);
