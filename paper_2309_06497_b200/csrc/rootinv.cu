@@ -318,17 +318,62 @@ __device__ __forceinline__ void tri_decode(int l, int& hi, int& lo) {
   lo = l - r * (r + 1) / 2;
 }
 
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp16_zero(void* smem, const void* any_global) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(sa), "l"(any_global));
+}
+__device__ __forceinline__ void cp_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// Copy a 64x64 block whose rows are (gr(a)) and whose 64 columns come in two contiguous runs of 32
+// (col0, col1) from a row-major matrix with leading dim ld, into smem (ld LDT), 16-byte copies.
+__device__ __forceinline__ void load_pair_tile(double* dst, const double* src, int64_t ld, const int* rows,
+                                               int col0, int col1) {
+  // 64 rows x 16 chunks of 4 doubles (2 x 16B each) = 1024 chunk-pairs / 256 threads
+  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
+    const int a = e >> 4, ch = e & 15;
+    const int b = ch * 4;
+    const int gc = (b < HB ? col0 + b : col1 + (b - HB));
+    double* d = dst + a * LDT + b;
+    if (rows[a] >= 0) {
+      const double* g = src + (int64_t)rows[a] * ld + gc;
+      cp16(d, g);
+      cp16(d + 2, g + 2);
+    } else {
+      cp16_zero(d, src);
+      cp16_zero(d + 2, src);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_slot(double* dst, const double* slot) {
+  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
+    const int a = e >> 4, b = (e & 15) * 4;
+    cp16(dst + a * LDT + b, slot + a * NS + b);
+    cp16(dst + a * LDT + b + 2, slot + a * NS + b + 2);
+  }
+}
+
 // A <- W^T A W (pair tiles P<=Q) and V <- V W (row chunk x pair), one CTA per item.
-__global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
-                                               const RootState* __restrict__ st,
-                                               const int32_t* __restrict__ ibegin, int njobs,
-                                               double* __restrict__ ws, double* __restrict__ vs,
-                                               const double* __restrict__ us) {
-  extern __shared__ double smem[];
-  double* X = smem;  // loaded tile
-  double* UP = smem + NS * LDT;
-  double* UQ = smem + 2 * NS * LDT;
-  double* T = smem + 3 * NS * LDT;
+// 3 shared buffers (104 KB -> 2 CTAs/SM); all global traffic is 16-byte cp.async.
+__global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jobs,
+                                                  const RootState* __restrict__ st,
+                                                  const int32_t* __restrict__ ibegin, int njobs,
+                                                  double* __restrict__ ws, double* __restrict__ vs,
+                                                  const double* __restrict__ us) {
+  extern __shared__ __align__(16) double smem[];
+  double* X = smem;              // loaded tile, later T = X UQ
+  double* U1 = smem + NS * LDT;  // UQ (A tile) or UP (V tile)
+  double* U2 = smem + 2 * NS * LDT;
+  __shared__ int rows[NS];
   const int j = find_job(ibegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   if (J.m == 0 || !st[j].active) return;
@@ -336,10 +381,7 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
   const int h = J.m / 2, np = J.np, r = st[j].round;
   const int nA = h * (h + 1) / 2;
   const double* slots = us + J.u_off;
-  auto pblk = [&](int P, int x) {  // global row of local index x in pair P
-    const int b = x < HB ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m);
-    return b * HB + (x & (HB - 1));
-  };
+  auto blk = [&](int P, int half) { return half == 0 ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m); };
   double acc[4][4];
   double* A = ws + J.ws_off;
   if (item < nA) {
@@ -347,36 +389,43 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
     tri_decode(item, Q, P);  // Q >= P
     const double* sP = slots + (int64_t)P * SLOT;
     const double* sQ = slots + (int64_t)Q * SLOT;
+    const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
     if (P == Q) {  // diagonal pair block = the sub-solve's rotated sub-matrix
       const double* Sp = sP + NS * NS + NS + 2;
       for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
         const int a = e / NS, b = e % NS;
-        A[(int64_t)pblk(P, a) * np + pblk(P, b)] = Sp[e];
+        A[(int64_t)(a < HB ? p0 + a : p1 + a - HB) * np + (b < HB ? p0 + b : p1 + b - HB)] = Sp[e];
       }
       return;
     }
     const bool rp = sP[NS * NS + NS] != 0.0, rq = sQ[NS * NS + NS] != 0.0;
     if (!rp && !rq) return;
+    const int q0 = blk(Q, 0) * HB, q1 = blk(Q, 1) * HB;
+    if (threadIdx.x < NS) rows[threadIdx.x] = threadIdx.x < HB ? p0 + threadIdx.x : p1 + threadIdx.x - HB;
+    __syncthreads();
+    load_pair_tile(X, A, np, rows, q0, q1);
+    load_slot(U1, sQ);
+    cp_commit();
+    load_slot(U2, sP);  // overlaps the first product
+    cp_commit();
+    cp_wait1();
+    __syncthreads();
+    mm64<false, false>(X, U1, acc);  // T = X UQ
+    __syncthreads();
+    mm64_store(X, acc);
+    cp_commit_wait_all();
+    __syncthreads();
+    mm64<true, false>(U2, X, acc);  // R = UP^T T
+    __syncthreads();
+    mm64_store(X, acc);
+    __syncthreads();
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
       const int a = e / NS, b = e % NS;
-      X[a * LDT + b] = A[(int64_t)pblk(P, a) * np + pblk(Q, b)];
-      UP[a * LDT + b] = sP[e];
-      UQ[a * LDT + b] = sQ[e];
-    }
-    __syncthreads();
-    mm64<false, false>(X, UQ, acc);  // T = X UQ
-    mm64_store(T, acc);
-    __syncthreads();
-    mm64<true, false>(UP, T, acc);  // R = UP^T T
-    mm64_store(X, acc);             // X no longer read
-    __syncthreads();
-    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-      const int a = e / NS, b = e % NS;
-      A[(int64_t)pblk(P, a) * np + pblk(Q, b)] = X[a * LDT + b];
+      A[(int64_t)rows[a] * np + (b < HB ? q0 + b : q1 + b - HB)] = X[a * LDT + b];
     }
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {  // mirror, coalesced along the P index
       const int b = e / NS, a = e % NS;
-      A[(int64_t)pblk(Q, b) * np + pblk(P, a)] = X[a * LDT + b];
+      A[(int64_t)(b < HB ? q0 + b : q1 + b - HB) * np + rows[a]] = X[a * LDT + b];
     }
     return;
   }
@@ -387,20 +436,20 @@ __global__ void __launch_bounds__(256) k_apply(const RootJob* __restrict__ jobs,
   if (sP[NS * NS + NS] == 0.0) return;
   double* V = vs + J.v_off;
   const int r0 = R * NS;
+  const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
+  if (threadIdx.x < NS) rows[threadIdx.x] = (r0 + threadIdx.x < np) ? r0 + threadIdx.x : -1;
+  __syncthreads();
+  load_pair_tile(X, V, np, rows, p0, p1);
+  load_slot(U1, sP);
+  cp_commit_wait_all();
+  __syncthreads();
+  mm64<false, false>(X, U1, acc);
+  __syncthreads();
+  mm64_store(X, acc);
+  __syncthreads();
   for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
     const int a = e / NS, b = e % NS;
-    const int gr = r0 + a;
-    X[a * LDT + b] = gr < np ? V[(int64_t)gr * np + pblk(P, b)] : 0.0;
-    UP[a * LDT + b] = sP[e];
-  }
-  __syncthreads();
-  mm64<false, false>(X, UP, acc);
-  mm64_store(T, acc);
-  __syncthreads();
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-    const int a = e / NS, b = e % NS;
-    const int gr = r0 + a;
-    if (gr < np) V[(int64_t)gr * np + pblk(P, b)] = T[a * LDT + b];
+    if (rows[a] >= 0) V[(int64_t)rows[a] * np + (b < HB ? p0 + b : p1 + b - HB)] = X[a * LDT + b];
   }
 }
 
@@ -872,7 +921,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * NS * LDS_ * (int)sizeof(double)));
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       4 * NS * LDT * (int)sizeof(double)));
+                                       3 * NS * LDT * (int)sizeof(double)));
     attr_done = true;
   }
   return SHAMPOO_OK;
@@ -927,7 +976,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     SH_LAUNCH_CHECK();
     if (!has_big_) break;
     if (total_items_ > 0) {
-      k_apply<<<total_items_, 256, 4 * NS * LDT * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
+      k_apply<<<total_items_, 256, 3 * NS * LDT * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
                                                                           ws_, vs_, us_);
       SH_LAUNCH_CHECK();
     }
