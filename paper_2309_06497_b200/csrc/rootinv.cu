@@ -141,8 +141,11 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, double t
         double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > thr) {
           const double tau = (aqq - app) / (2.0 * apq);
-          t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
-          c = 1.0 / sqrt(1.0 + t * t);
+          const double at = fabs(tau);
+          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)); for huge |tau|, t = 1/(2 tau) (no overflow)
+          const double den = at < 1e150 ? at + sqrt(fma(at, at, 1.0)) : 2.0 * at;
+          t = copysign(1.0, tau) / den;
+          c = rsqrt(fma(t, t, 1.0));
           s = t * c;
           rot_round = 1;
         }
