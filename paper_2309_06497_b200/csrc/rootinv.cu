@@ -172,30 +172,29 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, double t
           S[b * LDS_ + col] = s * xa + c * xb;
         }
         __syncthreads();
-        // columns: S <- S J, U <- U J
+        // columns: S <- S J, U <- U J; the 2x2 pair block gets the exact values
+        // (Golub & Van Loan sym.schur2: b_aa = a_aa - t a_ab, b_bb = a_bb + t a_ab, b_ab = 0)
         for (int w = tid; w < half * ns; w += blockDim.x) {
           const int q = w % half, row = w / half;
           const double s = ps[q];
           if (s == 0.0) continue;
           const double c = pc[q];
           const int a = pa[q], b = pb[q];
-          double xa = S[row * LDS_ + a], xb = S[row * LDS_ + b];
-          S[row * LDS_ + a] = c * xa - s * xb;
-          S[row * LDS_ + b] = s * xa + c * xb;
-          xa = U[row * LDS_ + a];
-          xb = U[row * LDS_ + b];
+          double xa = U[row * LDS_ + a], xb = U[row * LDS_ + b];
           U[row * LDS_ + a] = c * xa - s * xb;
           U[row * LDS_ + b] = s * xa + c * xb;
-        }
-        __syncthreads();
-        if (tid < half && ps[tid] != 0.0) {
-          // exact 2x2 update (Golub & Van Loan, sym.schur2): b_aa = a_aa - t a_ab, b_bb = a_bb + t a_ab
-          const int a = pa[tid], b = pb[tid];
-          const double t = pt[tid], apq = papq[tid];
-          S[a * LDS_ + a] = papp[tid] - t * apq;
-          S[b * LDS_ + b] = paqq[tid] + t * apq;
-          S[a * LDS_ + b] = 0.0;
-          S[b * LDS_ + a] = 0.0;
+          if (row == a) {
+            S[a * LDS_ + a] = papp[q] - pt[q] * papq[q];
+            S[a * LDS_ + b] = 0.0;
+          } else if (row == b) {
+            S[b * LDS_ + b] = paqq[q] + pt[q] * papq[q];
+            S[b * LDS_ + a] = 0.0;
+          } else {
+            xa = S[row * LDS_ + a];
+            xb = S[row * LDS_ + b];
+            S[row * LDS_ + a] = c * xa - s * xb;
+            S[row * LDS_ + b] = s * xa + c * xb;
+          }
         }
         if (tid == 0) rot_sweep = 1;
       }
@@ -243,8 +242,26 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
   }
   __syncthreads();
   int sweeps = 0;
+  const double tol_abs = st[j].tol_abs, tol_null = st[j].tol_null;
+  if (!small) {
+    // skip the sweep when no coupling exceeds its rotation threshold (late sweeps): U = I
+    int need = 0;
+    for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
+      const int i = e / ns, k = e % ns;
+      if (i >= k) continue;
+      const double app = S[i * LDS_ + i], aqq = S[k * LDS_ + k];
+      double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+      if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
+      if (fabs(S[i * LDS_ + k]) > thr) need = 1;
+    }
+    if (!__syncthreads_or(need)) {
+      double* slot = us + J.u_off + (int64_t)pair * SLOT;
+      if (threadIdx.x == 0) slot[NS * NS + NS] = 0.0;
+      return;  // k_apply skips every tile of an unrotated pair except its (unchanged) diagonal block
+    }
+  }
   // blocked jobs: one inner sweep per outer round (outer sweeps barely change)
-  const int any = cta_jacobi(S, U, ns, st[j].tol_abs, st[j].tol_null, small ? MAX_SWEEPS : 1, &sweeps);
+  const int any = cta_jacobi(S, U, ns, tol_abs, tol_null, small ? MAX_SWEEPS : 1, &sweeps);
   if (small) {
     double* V = vs + J.v_off;
     for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
@@ -394,6 +411,7 @@ __global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jo
     const double* sQ = slots + (int64_t)Q * SLOT;
     const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
     if (P == Q) {  // diagonal pair block = the sub-solve's rotated sub-matrix
+      if (sP[NS * NS + NS] == 0.0) return;  // unrotated (possibly skipped) pair: block unchanged
       const double* Sp = sP + NS * NS + NS + 2;
       for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
         const int a = e / NS, b = e % NS;
@@ -407,21 +425,25 @@ __global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jo
     if (threadIdx.x < NS) rows[threadIdx.x] = threadIdx.x < HB ? p0 + threadIdx.x : p1 + threadIdx.x - HB;
     __syncthreads();
     load_pair_tile(X, A, np, rows, q0, q1);
-    load_slot(U1, sQ);
+    if (rq) load_slot(U1, sQ);
     cp_commit();
-    load_slot(U2, sP);  // overlaps the first product
+    if (rp) load_slot(U2, sP);  // overlaps the first product
     cp_commit();
     cp_wait1();
     __syncthreads();
-    mm64<false, false>(X, U1, acc);  // T = X UQ
-    __syncthreads();
-    mm64_store(X, acc);
+    if (rq) {  // T = X UQ (an unrotated pair's U is the identity: skip)
+      mm64<false, false>(X, U1, acc);
+      __syncthreads();
+      mm64_store(X, acc);
+    }
     cp_commit_wait_all();
     __syncthreads();
-    mm64<true, false>(U2, X, acc);  // R = UP^T T
-    __syncthreads();
-    mm64_store(X, acc);
-    __syncthreads();
+    if (rp) {  // R = UP^T T
+      mm64<true, false>(U2, X, acc);
+      __syncthreads();
+      mm64_store(X, acc);
+      __syncthreads();
+    }
     for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
       const int a = e / NS, b = e % NS;
       A[(int64_t)rows[a] * np + (b < HB ? q0 + b : q1 + b - HB)] = X[a * LDT + b];
