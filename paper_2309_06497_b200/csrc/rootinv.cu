@@ -211,8 +211,110 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, double t
   return any;
 }
 
+// One inner cyclic-Jacobi sweep on a 64x64 sub-problem with 256 threads, laid out for ILP:
+// row phase: thread -> one pair, 8 columns; column phase: thread -> one row, 8 pairs; all
+// updates of a thread are independent and fully unrolled (loads batched ahead of stores).
+__device__ int cta_jacobi64_sweep(double* S, double* U, double tol_abs, double tol_null) {
+  __shared__ double pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
+  __shared__ int pa[NS / 2], pb[NS / 2];
+  __shared__ int rot_round, rot_any;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? 1.0 : 0.0;
+  if (tid == 0) rot_any = 0;
+  for (int r = 0; r < NS - 1; ++r) {
+    if (tid == 0) rot_round = 0;
+    __syncthreads();
+    if (tid < NS / 2) {
+      const int a = circle_pos(r, tid, NS), b = circle_pos(r, NS - 1 - tid, NS);
+      const double apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
+      double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+      if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
+      double c = 1.0, sn = 0.0, t = 0.0;
+      if (fabs(apq) > thr) {
+        const double tau = (aqq - app) / (2.0 * apq);
+        const double at = fabs(tau);
+        const double den = at < 1e150 ? at + sqrt(fma(at, at, 1.0)) : 2.0 * at;
+        t = copysign(1.0, tau) / den;
+        c = rsqrt(fma(t, t, 1.0));
+        sn = t * c;
+        rot_round = 1;
+      }
+      pa[tid] = a;
+      pb[tid] = b;
+      pc[tid] = c;
+      ps[tid] = sn;
+      pt[tid] = t;
+      papq[tid] = apq;
+      papp[tid] = app;
+      paqq[tid] = aqq;
+    }
+    __syncthreads();
+    if (!rot_round) continue;  // uniform: every thread read it after the barrier
+    {  // rows: S <- J^T S
+      const int q = tid >> 3, c0 = tid & 7;
+      const double sn = ps[q];
+      if (sn != 0.0) {
+        const double c = pc[q];
+        const int a = pa[q], b = pb[q];
+        double xa[8], xb[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          xa[k] = S[a * LDS_ + c0 + 8 * k];
+          xb[k] = S[b * LDS_ + c0 + 8 * k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          S[a * LDS_ + c0 + 8 * k] = c * xa[k] - sn * xb[k];
+          S[b * LDS_ + c0 + 8 * k] = sn * xa[k] + c * xb[k];
+        }
+      }
+    }
+    __syncthreads();
+    {  // columns: S <- S J, U <- U J; exact 2x2 pair block (sym.schur2); two halves of 4 pairs
+      const int row = tid >> 2, q0 = tid & 3;
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        double sa[4], sb[4], ua[4], ub[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int q = q0 + 4 * (k + 4 * hlf);
+          const int a = pa[q], b = pb[q];
+          sa[k] = S[row * LDS_ + a];
+          sb[k] = S[row * LDS_ + b];
+          ua[k] = U[row * LDS_ + a];
+          ub[k] = U[row * LDS_ + b];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int q = q0 + 4 * (k + 4 * hlf);
+          const double sn = ps[q];
+          if (sn == 0.0) continue;
+          const double c = pc[q];
+          const int a = pa[q], b = pb[q];
+          U[row * LDS_ + a] = c * ua[k] - sn * ub[k];
+          U[row * LDS_ + b] = sn * ua[k] + c * ub[k];
+          if (row == a) {
+            S[a * LDS_ + a] = papp[q] - pt[q] * papq[q];
+            S[a * LDS_ + b] = 0.0;
+          } else if (row == b) {
+            S[b * LDS_ + b] = paqq[q] + pt[q] * papq[q];
+            S[b * LDS_ + a] = 0.0;
+          } else {
+            S[row * LDS_ + a] = c * sa[k] - sn * sb[k];
+            S[row * LDS_ + b] = sn * sa[k] + c * sb[k];
+          }
+        }
+      }
+    }
+    if (tid == 0) rot_any = 1;
+    __syncthreads();
+  }
+  __syncthreads();
+  return rot_any;
+}
+
 // One CTA per (job, pair).  Small jobs are solved completely here.
-__global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jobs, RootState* st,
+__global__ void __launch_bounds__(256, 3) k_subsolve(const RootJob* __restrict__ jobs, RootState* st,
                                                   const int32_t* __restrict__ pbegin, int njobs,
                                                   double* __restrict__ ws, double* __restrict__ vs,
                                                   double* __restrict__ us) {
@@ -261,7 +363,8 @@ __global__ void __launch_bounds__(256) k_subsolve(const RootJob* __restrict__ jo
     }
   }
   // blocked jobs: one inner sweep per outer round (outer sweeps barely change)
-  const int any = cta_jacobi(S, U, ns, tol_abs, tol_null, small ? MAX_SWEEPS : 1, &sweeps);
+  const int any = small ? cta_jacobi(S, U, ns, tol_abs, tol_null, MAX_SWEEPS, &sweeps)
+                        : cta_jacobi64_sweep(S, U, tol_abs, tol_null);
   if (small) {
     double* V = vs + J.v_off;
     for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
@@ -316,6 +419,33 @@ __device__ __forceinline__ void mm64(const double* X, const double* Y, double (&
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const double b = TY ? Y[(c0 + j * 8 + g) * LDT + kk] : Y[kk * LDT + c0 + j * 8 + g];
+      dmma_16x8x4(c[j], a0, a1, b);
+    }
+  }
+}
+
+// Same product with one operand read straight from a global 64x64 slot (ld NS, read-only, L1-cached):
+// GX: X is global (else smem ld LDT); GY: Y is global.
+template <bool TX, bool TY, bool GX, bool GY>
+__device__ __forceinline__ void mm64g(const double* X, const double* Y, double (&c)[4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32, g = lane >> 2, tq = lane & 3;
+  constexpr int LX = GX ? NS : LDT, LY = GY ? NS : LDT;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[j][q] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < NS; k += 4) {
+    const int kk = k + tq;
+    const int ia0 = TX ? kk * LX + r0 + g : (r0 + g) * LX + kk;
+    const int ia1 = TX ? kk * LX + r0 + g + 8 : (r0 + g + 8) * LX + kk;
+    const double a0 = GX ? __ldg(X + ia0) : X[ia0];
+    const double a1 = GX ? __ldg(X + ia1) : X[ia1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ib = TY ? (c0 + j * 8 + g) * LY + kk : kk * LY + c0 + j * 8 + g;
+      const double b = GY ? __ldg(Y + ib) : Y[ib];
       dmma_16x8x4(c[j], a0, a1, b);
     }
   }
@@ -384,15 +514,13 @@ __device__ __forceinline__ void load_slot(double* dst, const double* slot) {
 
 // A <- W^T A W (pair tiles P<=Q) and V <- V W (row chunk x pair), one CTA per item.
 // 3 shared buffers (104 KB -> 2 CTAs/SM); all global traffic is 16-byte cp.async.
-__global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jobs,
+__global__ void __launch_bounds__(256, 4) k_apply(const RootJob* __restrict__ jobs,
                                                   const RootState* __restrict__ st,
                                                   const int32_t* __restrict__ ibegin, int njobs,
                                                   double* __restrict__ ws, double* __restrict__ vs,
                                                   const double* __restrict__ us) {
   extern __shared__ __align__(16) double smem[];
-  double* X = smem;              // loaded tile, later T = X UQ
-  double* U1 = smem + NS * LDT;  // UQ (A tile) or UP (V tile)
-  double* U2 = smem + 2 * NS * LDT;
+  double* X = smem;  // loaded tile, later T = X UQ; U slots are read from L1/L2 directly
   __shared__ int rows[NS];
   const int j = find_job(ibegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
@@ -425,21 +553,16 @@ __global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jo
     if (threadIdx.x < NS) rows[threadIdx.x] = threadIdx.x < HB ? p0 + threadIdx.x : p1 + threadIdx.x - HB;
     __syncthreads();
     load_pair_tile(X, A, np, rows, q0, q1);
-    if (rq) load_slot(U1, sQ);
-    cp_commit();
-    if (rp) load_slot(U2, sP);  // overlaps the first product
-    cp_commit();
-    cp_wait1();
-    __syncthreads();
-    if (rq) {  // T = X UQ (an unrotated pair's U is the identity: skip)
-      mm64<false, false>(X, U1, acc);
-      __syncthreads();
-      mm64_store(X, acc);
-    }
     cp_commit_wait_all();
     __syncthreads();
+    if (rq) {  // T = X UQ (an unrotated pair's U is the identity: skip)
+      mm64g<false, false, false, true>(X, sQ, acc);
+      __syncthreads();
+      mm64_store(X, acc);
+      __syncthreads();
+    }
     if (rp) {  // R = UP^T T
-      mm64<true, false>(U2, X, acc);
+      mm64g<true, false, true, false>(sP, X, acc);
       __syncthreads();
       mm64_store(X, acc);
       __syncthreads();
@@ -465,10 +588,9 @@ __global__ void __launch_bounds__(256, 2) k_apply(const RootJob* __restrict__ jo
   if (threadIdx.x < NS) rows[threadIdx.x] = (r0 + threadIdx.x < np) ? r0 + threadIdx.x : -1;
   __syncthreads();
   load_pair_tile(X, V, np, rows, p0, p1);
-  load_slot(U1, sP);
   cp_commit_wait_all();
   __syncthreads();
-  mm64<false, false>(X, U1, acc);
+  mm64g<false, false, false, true>(X, sP, acc);
   __syncthreads();
   mm64_store(X, acc);
   __syncthreads();
@@ -946,7 +1068,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * NS * LDS_ * (int)sizeof(double)));
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       3 * NS * LDT * (int)sizeof(double)));
+                                       NS * LDT * (int)sizeof(double)));
     attr_done = true;
   }
   return SHAMPOO_OK;
@@ -1001,7 +1123,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     SH_LAUNCH_CHECK();
     if (!has_big_) break;
     if (total_items_ > 0) {
-      k_apply<<<total_items_, 256, 3 * NS * LDT * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
+      k_apply<<<total_items_, 256, NS * LDT * sizeof(double), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
                                                                           ws_, vs_, us_);
       SH_LAUNCH_CHECK();
     }
