@@ -200,7 +200,8 @@ SHAMPOO_API int shampoo_work(shampoo_ctx* ctx, double* stats_flops, double* prec
 SHAMPOO_API int64_t shampoo_launch_count(void);
 
 /* ---- state export/import: device views into the context's arena.
- * name: "factor","inv_factor","graft_accumulator","filtered_grad","momentum".
+ * name: "factor","inv_factor","graft_accumulator","filtered_grad","momentum",
+ * "accumulator" (ADAGRAD fallback block), "diag" (DIAGONAL fallback block, per mode).
  * For factors, `mode` selects k.  Returns NULL if absent (not owned / not used).
  * *numel and *dtype describe the view; views stay valid until ctx destroy. */
 SHAMPOO_API void* shampoo_state_view(shampoo_ctx* ctx, int32_t block_id, const char* name, int32_t mode,

@@ -41,6 +41,7 @@ struct DevBlock {
   int64_t numel;
   int64_t gofs;        // gather-buffer offset (scalars)
   int64_t vofs;        // offset into per-element state arenas (owned only)
+  int64_t fofs;        // offset into the fallback-state arena (ADAGRAD: numel, DIAGONAL: sum d_k)
   int64_t dims[kMaxOrder];
   int64_t lo[kMaxOrder];
   int64_t mstride[kMaxOrder];

@@ -105,8 +105,15 @@ struct shampoo_ctx {
   std::vector<int64_t> last_inv;    // per owned: last_inverse_step
   std::vector<int32_t> ready_h;     // per owned: inverse present
   int64_t graft_step = 0;           // GraftState.step (identical for all owned blocks)
-  int64_t n_elem = 0, n_fac = 0;
+  int64_t n_elem = 0, n_fac = 0, n_fb = 0;
   bool any_order3 = false;
+  std::vector<int64_t> fb_off;      // per owned: offset into FB (fallback blocks)
+  void* FB = nullptr;               // fallback state (T)
+  double *dsum = nullptr, *dscale = nullptr;
+  Chunk* d_fb_chunks = nullptr;
+  int n_fb_chunks = 0;
+  int32_t* d_diag_blocks = nullptr;
+  int n_diag = 0;
   // arena
   char* arena = nullptr;
   size_t arena_bytes = 0;
@@ -137,6 +144,8 @@ struct shampoo_ctx {
     cudaFree(d_owned_chunks);
     cudaFree(d_all_chunks);
     cudaFree(d_param_chunks);
+    cudaFree(d_fb_chunks);
+    cudaFree(d_diag_blocks);
     cudaFree(d_ptrs);
     cudaFreeHost(h_flag);
   }
@@ -181,6 +190,24 @@ StepScalars make_scalars(const shampoo_ctx* c, int64_t t, int32_t dtype, int64_t
   sc.pdtype = dtype;
   sc.lr = k.lr;
   return sc;
+}
+
+FallbackArgs fallback_args(const shampoo_ctx* c, int64_t t) {
+  const shampoo_config& k = c->cfg;
+  FallbackArgs fa{};
+  fa.FB = c->FB;
+  fa.dsum = c->dsum;
+  fa.dscale = c->dscale;
+  fa.beta2 = k.beta2;
+  fa.one_minus_beta2 = 1.0 - k.beta2;
+  fa.ema = k.beta2 < 1.0;
+  // precond.py:318-319, 384-386: correction from the global step t, not the state step
+  fa.inv_corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 / (1.0 - std::pow(k.beta2, (double)(t + 1))) : 1.0;
+  fa.epsilon = k.epsilon;
+  fa.eta = k.exponent_multiplier;
+  fa.div_eps = k.grafting_epsilon;  // AdaGradFallbackState division_epsilon (optim.py:241)
+  fa.root_override = k.exponent_override;
+  return fa;
 }
 
 ElemArenas arenas(shampoo_ctx* c) {
@@ -321,11 +348,11 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   for (int i = 0; i < nb; ++i) {
     const BlockPlan& b = plan->blocks[i];
     if (b.owner != c->grank) continue;
-    if (b.kind == SHAMPOO_BLOCK_ADAGRAD || b.kind == SHAMPOO_BLOCK_DIAGONAL) {
-      set_error("large_dim_method ADAGRAD/DIAGONAL fallback blocks are not built in this release");
-      return SHAMPOO_ERR_UNSUPPORTED;
-    }
     c->local_of[i] = (int32_t)c->owned.size();
+    c->fb_off.push_back(c->n_fb);
+    if (b.kind == SHAMPOO_BLOCK_ADAGRAD) c->n_fb += b.var_count;
+    if (b.kind == SHAMPOO_BLOCK_DIAGONAL)
+      for (int64_t d : b.dims()) c->n_fb += d;
     c->owned.push_back(i);
     c->vofs.push_back(c->n_elem);
     c->n_elem += b.var_count;
@@ -352,6 +379,17 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     const BlockPlan& b = plan->blocks[i];
     for (int64_t s = 0; s < b.var_count; s += kChunk) ac.push_back(Chunk{i, 0, s, std::min<int64_t>(kChunk, b.var_count - s)});
   }
+  std::vector<Chunk> fc;
+  std::vector<int32_t> dblk;
+  for (size_t l = 0; l < no; ++l) {
+    const BlockPlan& b = plan->blocks[c->owned[l]];
+    if (b.kind != SHAMPOO_BLOCK_ADAGRAD && b.kind != SHAMPOO_BLOCK_DIAGONAL) continue;
+    for (int64_t s = 0; s < b.var_count; s += kChunk)
+      fc.push_back(Chunk{b.block_id, 0, s, std::min<int64_t>(kChunk, b.var_count - s)});
+    if (b.kind == SHAMPOO_BLOCK_DIAGONAL) dblk.push_back(b.block_id);
+  }
+  c->n_fb_chunks = (int)fc.size();
+  c->n_diag = (int)dblk.size();
   std::vector<DevBlock> db(nb), dp(c->nparams);
   for (int i = 0; i < nb; ++i) {
     const BlockPlan& b = plan->blocks[i];
@@ -365,6 +403,7 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     d.numel = b.var_count;
     d.gofs = b.gather_offset;
     d.vofs = d.local >= 0 ? c->vofs[d.local] : 0;
+    d.fofs = d.local >= 0 ? c->fb_off[d.local] : 0;
     for (int k = 0; k < b.order; ++k) {
       d.dims[k] = b.hi[k] - b.lo[k];
       d.lo[k] = b.lo[k];
@@ -408,6 +447,9 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
       {(void**)&c->d_cb, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_cc, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_flag, 16},
+      {&c->FB, (size_t)c->n_fb * es},
+      {(void**)&c->dsum, (size_t)c->n_fb * 8},
+      {(void**)&c->dscale, (size_t)c->n_fb * 8},
   };
   size_t total = 0;
   for (auto& s : slots) total += align_up(s.bytes);
@@ -429,6 +471,12 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   SH_CUDA_CHECK(cudaMalloc(&c->d_all_chunks, std::max<size_t>(ac.size(), 1) * sizeof(Chunk)));
   SH_CUDA_CHECK(cudaMalloc(&c->d_param_chunks, std::max<size_t>(pc.size(), 1) * sizeof(Chunk)));
   SH_CUDA_CHECK(cudaMalloc(&c->d_ptrs, std::max(2 * c->nparams, 1) * sizeof(void*)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_fb_chunks, std::max<size_t>(fc.size(), 1) * sizeof(Chunk)));
+  SH_CUDA_CHECK(cudaMalloc(&c->d_diag_blocks, std::max<size_t>(dblk.size(), 1) * sizeof(int32_t)));
+  if (!fc.empty())
+    SH_CUDA_CHECK(cudaMemcpy(c->d_fb_chunks, fc.data(), fc.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  if (!dblk.empty())
+    SH_CUDA_CHECK(cudaMemcpy(c->d_diag_blocks, dblk.data(), dblk.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMallocHost(&c->h_flag, 16));
   SH_CUDA_CHECK(cudaMemcpy(c->d_blocks, db.data(), nb * sizeof(DevBlock), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(c->d_params, dp.data(), c->nparams * sizeof(DevBlock), cudaMemcpyHostToDevice));
@@ -515,9 +563,17 @@ int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* c
   if ((rc = launch_block_reduce(c->d_cb, c->d_cc, no, c->part, c->pg2, s))) return rc;
   rc = c->f32 ? c->eng<float>().stats.launch(s) : c->eng<double>().stats.launch(s);
   if (rc) return rc;
+  if (c->n_fb_chunks) {
+    const FallbackArgs fa = fallback_args(c, t);
+    rc = c->f32 ? launch_fallback_update<float>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
+                                                 c->d_diag_blocks, c->n_diag, s)
+                : launch_fallback_update<double>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
+                                                  c->d_diag_blocks, c->n_diag, s);
+    if (rc) return rc;
+  }
   c->graft_step = gstep;
   for (size_t l = 0; l < c->owned.size(); ++l)
-    if (c->plan.blocks[c->owned[l]].kind == SHAMPOO_BLOCK_SHAMPOO) ++c->step[l];
+    if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_GRAFT_ONLY) ++c->step[l];
   return SHAMPOO_OK;
 }
 
@@ -553,6 +609,15 @@ int shampoo_precondition_graft(shampoo_ctx* c, const void* const* params, int32_
   const StepScalars sc = make_scalars(c, t, dtype, c->graft_step);
   if (sc.precond) {
     PhaseScope scope(&c->timer, 2, s);
+    if (c->n_fb_chunks) {  // fallback directions into PS before the norms
+      const FallbackArgs fa = fallback_args(c, t);
+      const ElemArenas ar = arenas(c);
+      rc = c->f32 ? launch_fallback_precondition<float>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
+                                                        c->d_diag_blocks, c->n_diag, sc.use_filter, s)
+                  : launch_fallback_precondition<double>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
+                                                         c->d_diag_blocks, c->n_diag, sc.use_filter, s);
+      if (rc) return rc;
+    }
     rc = c->f32 ? precondition_impl<float>(c, s) : precondition_impl<double>(c, s);
     if (rc) return rc;
   }
@@ -660,6 +725,18 @@ void* shampoo_state_view(shampoo_ctx* c, int32_t block_id, const char* name, int
     if (numel) *numel = d[mode] * d[mode];
     base = static_cast<char*>(n == "factor" ? c->FACT : c->INV);
     return base + off * c->esz;
+  }
+  if (n == "accumulator" && b.kind == SHAMPOO_BLOCK_ADAGRAD) {
+    if (numel) *numel = b.var_count;
+    return static_cast<char*>(c->FB) + c->fb_off[l] * c->esz;
+  }
+  if (n == "diag" && b.kind == SHAMPOO_BLOCK_DIAGONAL) {
+    const auto d = b.dims();
+    if (mode < 0 || mode >= b.order) return nullptr;
+    int64_t off = c->fb_off[l];
+    for (int m = 0; m < mode; ++m) off += d[m];
+    if (numel) *numel = d[mode];
+    return static_cast<char*>(c->FB) + off * c->esz;
   }
   void* arr = nullptr;
   if (n == "graft_accumulator") arr = c->GA;

@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
   T* M = static_cast<T*>(ar.MOM) + B.vofs;
   T* out = static_cast<T*>(ar.BUF) + B.gofs;
   const void* wp = params[B.param];
-  const bool use_ps = sc.precond && B.kind == SHAMPOO_BLOCK_SHAMPOO && ar.ready[B.local];
+  const bool use_ps = sc.precond && ((B.kind == SHAMPOO_BLOCK_SHAMPOO && ar.ready[B.local]) ||
+                                     B.kind == SHAMPOO_BLOCK_ADAGRAD || B.kind == SHAMPOO_BLOCK_DIAGONAL);
   double ratio = 0.0;
   bool ps_zero = false;
   if (use_ps) {
@@ -188,7 +189,124 @@ __global__ void __launch_bounds__(NT) k_apply(const Chunk* __restrict__ chunks,
   }
 }
 
+// multi-index component k of flat element e of a block
+__device__ __forceinline__ int64_t mode_index(const DevBlock& b, int64_t e, int k) {
+  int64_t inner = 1;
+  for (int q = b.order - 1; q > k; --q) inner *= b.dims[q];
+  return (e / inner) % b.dims[k];
+}
+
+// ADAGRAD: acc = acc + g^2 (or EMA); DIAGONAL: dsum[mode, i] += g^2 (precond.py:305-313, 355-364)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_fb_update(const Chunk* __restrict__ chunks,
+                                                  const DevBlock* __restrict__ blocks, ElemArenas ar,
+                                                  FallbackArgs fa) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  const T* G = static_cast<const T*>(ar.G) + B.vofs;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    const double g = (double)G[j];
+    const double sq = g * g;
+    if (B.kind == SHAMPOO_BLOCK_ADAGRAD) {
+      T* acc = static_cast<T*>(fa.FB) + B.fofs;
+      acc[j] = fa.ema ? T(fa.beta2 * (double)acc[j] + fa.one_minus_beta2 * (double)T(sq)) : T((double)acc[j] + (double)T(sq));
+    } else {
+      int64_t off = B.fofs;
+      for (int k = 0; k < B.order; ++k) {
+        atomicAdd(fa.dsum + off + mode_index(B, j, k), sq);
+        off += B.dims[k];
+      }
+    }
+  }
+}
+
+// DIAGONAL: diag = EMA(diag, dsum) ; dsum = 0 (one CTA per diagonal block)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_fb_diag_ema(const DevBlock* __restrict__ blocks,
+                                                    const int32_t* __restrict__ dblocks, FallbackArgs fa) {
+  const DevBlock& B = blocks[dblocks[blockIdx.x]];
+  int64_t n = 0;
+  for (int k = 0; k < B.order; ++k) n += B.dims[k];
+  T* diag = static_cast<T*>(fa.FB) + B.fofs;
+  for (int64_t e = threadIdx.x; e < n; e += NT) {
+    const double sq = (double)T(fa.dsum[B.fofs + e]);  // cast like mode_square_sums(...).astype
+    diag[e] = fa.ema ? T(fa.beta2 * (double)diag[e] + fa.one_minus_beta2 * sq) : T((double)diag[e] + sq);
+    fa.dsum[B.fofs + e] = 0.0;
+  }
+}
+
+// DIAGONAL: scale = (diag / corr + eps)^exponent (precond.py:384-395)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_fb_scale(const DevBlock* __restrict__ blocks,
+                                                 const int32_t* __restrict__ dblocks, FallbackArgs fa) {
+  const DevBlock& B = blocks[dblocks[blockIdx.x]];
+  int64_t n = 0;
+  for (int k = 0; k < B.order; ++k) n += B.dims[k];
+  const T* diag = static_cast<const T*>(fa.FB) + B.fofs;
+  const double exponent = -fa.eta / (fa.root_override ? fa.root_override : 2 * B.order);  // precond.py:349,380
+  for (int64_t e = threadIdx.x; e < n; e += NT)
+    fa.dscale[B.fofs + e] = pow((double)diag[e] * fa.inv_corr + fa.epsilon, exponent);
+}
+
+// PS = fallback direction of g_eff (precond.py:315-320, 366-396)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_fb_precondition(const Chunk* __restrict__ chunks,
+                                                        const DevBlock* __restrict__ blocks, ElemArenas ar,
+                                                        FallbackArgs fa, int use_filter) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  const T* GE = static_cast<const T*>(use_filter ? ar.GE : ar.G) + B.vofs;
+  T* PS = static_cast<T*>(ar.PS) + B.vofs;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    const double g = (double)GE[j];
+    double out;
+    if (B.kind == SHAMPOO_BLOCK_ADAGRAD) {
+      const double acc = (double)static_cast<const T*>(fa.FB)[B.fofs + j] * fa.inv_corr;
+      out = g / (sqrt(acc) + fa.div_eps);
+    } else {
+      out = g;
+      int64_t off = B.fofs;
+      for (int k = 0; k < B.order; ++k) {
+        out *= fa.dscale[off + mode_index(B, j, k)];
+        off += B.dims[k];
+      }
+    }
+    PS[j] = T(out);
+  }
+}
+
 }  // namespace
+
+template <typename T>
+int launch_fallback_update(const Chunk* chunks, int nchunks, const DevBlock* blocks, const ElemArenas& ar,
+                           const FallbackArgs& fa, const int32_t* dblocks, int ndiag, cudaStream_t s) {
+  if (nchunks) {
+    k_fb_update<T><<<nchunks, NT, 0, s>>>(chunks, blocks, ar, fa);
+    SH_LAUNCH_CHECK();
+  }
+  if (ndiag) {
+    k_fb_diag_ema<T><<<ndiag, NT, 0, s>>>(blocks, dblocks, fa);
+    SH_LAUNCH_CHECK();
+  }
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_fallback_precondition(const Chunk* chunks, int nchunks, const DevBlock* blocks, const ElemArenas& ar,
+                                 const FallbackArgs& fa, const int32_t* dblocks, int ndiag, int use_filter,
+                                 cudaStream_t s) {
+  if (ndiag) {
+    k_fb_scale<T><<<ndiag, NT, 0, s>>>(blocks, dblocks, fa);
+    SH_LAUNCH_CHECK();
+  }
+  if (nchunks) {
+    k_fb_precondition<T><<<nchunks, NT, 0, s>>>(chunks, blocks, ar, fa, use_filter);
+    SH_LAUNCH_CHECK();
+  }
+  return SHAMPOO_OK;
+}
 
 template <typename T>
 int launch_finite(const Chunk* chunks, int nchunks, const DevBlock* params, const void* const* grads,
@@ -254,7 +372,11 @@ int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void*
   template int launch_final<T>(const Chunk*, int, const DevBlock*, const void* const*,              \
                                const StepScalars&, const ElemArenas&, cudaStream_t);                 \
   template int launch_apply<T>(const Chunk*, int, const DevBlock*, void* const*, const void*,        \
-                               const StepScalars&, cudaStream_t);
+                               const StepScalars&, cudaStream_t);                                    \
+  template int launch_fallback_update<T>(const Chunk*, int, const DevBlock*, const ElemArenas&,      \
+                                         const FallbackArgs&, const int32_t*, int, cudaStream_t);    \
+  template int launch_fallback_precondition<T>(const Chunk*, int, const DevBlock*, const ElemArenas&, \
+                                               const FallbackArgs&, const int32_t*, int, int, cudaStream_t);
 SH_INST(double)
 SH_INST(float)
 

@@ -54,6 +54,22 @@ int launch_block_reduce(const int32_t* chunk_begin, const int32_t* chunk_count, 
 template <typename T>
 int launch_final(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* params,
                  const StepScalars& sc, const ElemArenas& ar, cudaStream_t s);
+// Large-dimension fallbacks (precond.py:282-396): AdaGrad accumulator or per-mode diagonals.
+struct FallbackArgs {
+  void* FB;         // T: ADAGRAD accumulator (numel) / DIAGONAL vectors (sum d_k) per block
+  double* dsum;     // DIAGONAL: per-step mode square sums (sum d_k, zero between steps)
+  double* dscale;   // DIAGONAL: (diag/corr + eps)^(-eta/p) (sum d_k)
+  double beta2, one_minus_beta2, inv_corr, epsilon, eta, div_eps;
+  int32_t ema;      // beta2 < 1
+  int32_t root_override;  // exponent_override (0: root p = 2 * order)
+};
+template <typename T>
+int launch_fallback_update(const Chunk* chunks, int nchunks, const DevBlock* blocks, const ElemArenas& ar,
+                           const FallbackArgs& fa, const int32_t* dblocks, int ndiag, cudaStream_t s);
+template <typename T>
+int launch_fallback_precondition(const Chunk* chunks, int nchunks, const DevBlock* blocks, const ElemArenas& ar,
+                                 const FallbackArgs& fa, const int32_t* dblocks, int ndiag, int use_filter,
+                                 cudaStream_t s);
 template <typename T>
 int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
                  const void* buf, const StepScalars& sc, cudaStream_t s);

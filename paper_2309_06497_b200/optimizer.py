@@ -265,6 +265,15 @@ class Shampoo:
                 v = self._view(info.block_id, name)
                 if v is not None:
                     entry[key] = v.detach().cpu().numpy().astype(np.float64).reshape(shape)
+            if info.kind in (N.BLOCK_ADAGRAD, N.BLOCK_DIAGONAL):  # optim.py:414-420
+                st, li, rd = C.c_int64(), C.c_int64(), C.c_int32()
+                lib.shampoo_state_scalars_get(self._ctx, info.block_id, C.byref(st), C.byref(li), C.byref(rd))
+                entry["step"] = int(st.value)
+                if info.kind == N.BLOCK_ADAGRAD:
+                    entry["accumulator"] = self._view(info.block_id, "accumulator").cpu().numpy().reshape(shape).copy()
+                else:
+                    for k in range(info.order):
+                        entry[f"diag{k}"] = self._view(info.block_id, "diag", k).cpu().numpy().copy()
             if info.kind == N.BLOCK_SHAMPOO:
                 st, li, rd = C.c_int64(), C.c_int64(), C.c_int32()
                 lib.shampoo_state_scalars_get(self._ctx, info.block_id, C.byref(st), C.byref(li), C.byref(rd))
@@ -294,6 +303,12 @@ class Shampoo:
                 v = self._view(info.block_id, name)
                 if v is not None:
                     v.copy_(torch.as_tensor(np.asarray(entry[name]).reshape(-1), dtype=v.dtype))
+            if info.kind in (N.BLOCK_ADAGRAD, N.BLOCK_DIAGONAL):
+                names = ["accumulator"] if info.kind == N.BLOCK_ADAGRAD else [f"diag{k}" for k in range(info.order)]
+                for k, key in enumerate(names):
+                    v = self._view(info.block_id, "accumulator" if key == "accumulator" else "diag", k)
+                    v.copy_(torch.as_tensor(np.asarray(entry[key]).reshape(-1), dtype=v.dtype))
+                N.check(lib.shampoo_state_scalars_set(self._ctx, info.block_id, int(entry["step"]), -1, 0), "state_set")
             if info.kind == N.BLOCK_SHAMPOO:
                 ready = 0
                 for k in range(info.order):

@@ -88,14 +88,30 @@ TRAJ_CONFIGS = {
 }
 TRAJ_STEPS = 6
 
+# large-dimension fallbacks: a dim above max_preconditioner_dim selects ADAGRAD / DIAGONAL
+# for that parameter (precond.py:114-158, 282-396); other params stay BLOCKING
+FALLBACK_SHAPES = [(9, 4), (13, 3), (2, 11, 3), (6,)]
+FALLBACK_CONFIGS = {
+    "fallback_adagrad": dict(grafting=GraftKind.ADAGRAD, large_dim_method=LargeDimMethod.ADAGRAD,
+                             precondition_frequency=2, max_preconditioner_dim=8, betas=(0.0, 0.99)),
+    "fallback_diagonal": dict(grafting=GraftKind.RMSPROP, large_dim_method=LargeDimMethod.DIAGONAL,
+                              precondition_frequency=2, max_preconditioner_dim=8, epsilon=1e-6,
+                              exponent_multiplier=0.5, betas=(0.5, 0.999)),
+    "fallback_diag_sum": dict(grafting=GraftKind.SGD, large_dim_method=LargeDimMethod.DIAGONAL,
+                              precondition_frequency=1, max_preconditioner_dim=8, epsilon=1e-8,
+                              betas=(0.0, 1.0), start_preconditioning_step=2),
+}
+
 
 def make_trajectories(out, meta):
-    for name, kw in TRAJ_CONFIGS.items():
+    cases = [(n, kw, TRAJ_SHAPES) for n, kw in TRAJ_CONFIGS.items()]
+    cases += [(n, kw, FALLBACK_SHAPES) for n, kw in FALLBACK_CONFIGS.items()]
+    for name, kw, shapes in cases:
         cfg = ShampooConfig(lr=0.05, **kw)
         rng = np.random.default_rng(0)
-        params = [(rng.standard_normal(s) * 0.5).astype(np.float32) for s in TRAJ_SHAPES]
+        params = [(rng.standard_normal(s) * 0.5).astype(np.float32) for s in shapes]
         grng = np.random.default_rng(1)
-        grads = [[(grng.standard_normal(s) * 0.1).astype(np.float32) for s in TRAJ_SHAPES]
+        grads = [[(grng.standard_normal(s) * 0.1).astype(np.float32) for s in shapes]
                  for _ in range(TRAJ_STEPS)]
         opt = Shampoo([p.astype(np.float64) for p in params], cfg)
         captured = {}
@@ -124,7 +140,7 @@ def make_trajectories(out, meta):
                     if isinstance(v, np.ndarray):
                         out[f"{name}/state/{i}/{b}/{k}"] = v
         meta[name] = {"config": {k: (v.value if hasattr(v, "value") else v) for k, v in kw.items()},
-                      "guard": vars(opt.guard_stats)}
+                      "guard": vars(opt.guard_stats), "shapes": [list(x) for x in shapes]}
 
 
 def make_rootinv(out):

@@ -41,6 +41,8 @@ def config_from_meta(name, **over) -> P.ShampooConfig:
         kw["grafting"] = P.GraftKind(kw["grafting"])
     if "solver" in kw:
         kw["solver"] = P.Solver(kw["solver"])
+    if "large_dim_method" in kw:
+        kw["large_dim_method"] = P.LargeDimMethod(kw["large_dim_method"])
     if "betas" in kw:
         kw["betas"] = tuple(kw["betas"])
     kw.update(over)
@@ -140,7 +142,7 @@ def test_root_inverse_guard_conventions(cuda_device):
 
 
 def _run_gpu_trajectory(name, cfg, device):
-    shapes = [tuple(s) for s in META["shapes"]]
+    shapes = [tuple(s) for s in META["configs"][name]["shapes"]]
     params = [torch.as_tensor(TRAJ[f"{name}/init/{i}"].astype(np.float64), device=device)
               for i in range(len(shapes))]
     opt = P.Shampoo(params, cfg)
@@ -188,7 +190,7 @@ def test_world_size_invariance_device(cuda_device):
     """test_dist.py:173-185 on the device: J ranks simulated by J contexts + region copies."""
     name = "adagrad_nesterov"
     cfg = config_from_meta(name, precondition_frequency=1)
-    shapes = [tuple(s) for s in META["shapes"]]
+    shapes = [tuple(s) for s in META["configs"][name]["shapes"]]
 
     def run(world, group):
         opts = []

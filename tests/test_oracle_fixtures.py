@@ -49,7 +49,7 @@ def _oracle_config(name):
 @pytest.mark.parametrize("name", sorted(META["configs"]))
 def test_oracle_trajectory_matches_reference(name):
     cfg = _oracle_config(name)
-    shapes = [tuple(s) for s in META["shapes"]]
+    shapes = [tuple(s) for s in META["configs"][name]["shapes"]]
     params = [TRAJ[f"{name}/init/{i}"].astype(np.float64) for i in range(len(shapes))]
     opt = O.OracleShampoo(params, cfg)
     for t in range(META["steps"]):
