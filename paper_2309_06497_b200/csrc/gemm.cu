@@ -12,6 +12,7 @@
 // C[j][i] from the same value, so factors stay exactly symmetric.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "gemm.cuh"
 
@@ -241,20 +242,22 @@ __global__ void __launch_bounds__(128) gemm_f64_dmma(const GemmProblem* __restri
     const int cur = kt % STAGES;
     const T* As = sm + (2 * cur) * TILE;
     const T* Bs = sm + (2 * cur + 1) * TILE;
+    {
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double a[2][2], b[4];
+      for (int kk = 0; kk < BK; kk += 4) {
+        double a[2][2], b[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        a[i][0] = (double)As[a_base + (i * 16) * a_rs + kk * a_ks];
-        a[i][1] = (double)As[a_base + (i * 16 + 8) * a_rs + kk * a_ks];
+        for (int i = 0; i < 2; ++i) {
+          a[i][0] = (double)As[a_base + (i * 16) * a_rs + kk * a_ks];
+          a[i][1] = (double)As[a_base + (i * 16 + 8) * a_rs + kk * a_ks];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = (double)Bs[b_base + (j * 8) * b_rs + kk * b_ks];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_16x8x4(c[i][j], a[i][0], a[i][1], b[j]);
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = (double)Bs[b_base + (j * 8) * b_rs + kk * b_ks];
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_16x8x4(c[i][j], a[i][0], a[i][1], b[j]);
     }
     const int nxt = kt + STAGES - 1;
     if (nxt < nk) {
