@@ -14,6 +14,8 @@
 // X = f(A) by < 1e-9 relative (the f'(lambda) bound near the eps floor).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -211,31 +213,39 @@ __device__ int cta_jacobi(double* S, double* U, int ns, double tol_abs, double t
   return any;
 }
 
+template <typename T> struct EigU;
+template <> struct EigU<double> { static constexpr double u = 1.1102230246251565e-16, big = 1e150; };
+template <> struct EigU<float> { static constexpr float u = 5.9604645e-8f, big = 1e18f; };
+__device__ __forceinline__ double eig_rsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ float eig_rsqrt(float x) { return rsqrtf(x); }
+
 // One inner cyclic-Jacobi sweep on a 64x64 sub-problem with 256 threads, laid out for ILP:
 // row phase: thread -> one pair, 8 columns; column phase: thread -> one row, 8 pairs; all
 // updates of a thread are independent and fully unrolled (loads batched ahead of stores).
-__device__ int cta_jacobi64_sweep(double* S, double* U, double tol_abs, double tol_null) {
-  __shared__ double pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
+template <typename T>
+__device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null) {
+  constexpr T UR = EigU<T>::u;
+  __shared__ T pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
   __shared__ int pa[NS / 2], pb[NS / 2];
   __shared__ int rot_round, rot_any;
   const int tid = threadIdx.x;
-  for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? 1.0 : 0.0;
+  for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? T(1) : T(0);
   if (tid == 0) rot_any = 0;
   for (int r = 0; r < NS - 1; ++r) {
     if (tid == 0) rot_round = 0;
     __syncthreads();
     if (tid < NS / 2) {
       const int a = circle_pos(r, tid, NS), b = circle_pos(r, NS - 1 - tid, NS);
-      const double apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
-      double thr = fmax(4.0 * U64 * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
+      const T apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
+      T thr = fmax(T(4) * UR * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
       if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
-      double c = 1.0, sn = 0.0, t = 0.0;
+      T c = 1, sn = 0, t = 0;
       if (fabs(apq) > thr) {
-        const double tau = (aqq - app) / (2.0 * apq);
-        const double at = fabs(tau);
-        const double den = at < 1e150 ? at + sqrt(fma(at, at, 1.0)) : 2.0 * at;
-        t = copysign(1.0, tau) / den;
-        c = rsqrt(fma(t, t, 1.0));
+        const T tau = (aqq - app) / (T(2) * apq);
+        const T at = fabs(tau);
+        const T den = at < EigU<T>::big ? at + sqrt(fma(at, at, T(1))) : T(2) * at;
+        t = copysign(T(1), tau) / den;
+        c = eig_rsqrt(fma(t, t, T(1)));
         sn = t * c;
         rot_round = 1;
       }
@@ -252,11 +262,11 @@ __device__ int cta_jacobi64_sweep(double* S, double* U, double tol_abs, double t
     if (!rot_round) continue;  // uniform: every thread read it after the barrier
     {  // rows: S <- J^T S
       const int q = tid >> 3, c0 = tid & 7;
-      const double sn = ps[q];
-      if (sn != 0.0) {
-        const double c = pc[q];
+      const T sn = ps[q];
+      if (sn != T(0)) {
+        const T c = pc[q];
         const int a = pa[q], b = pb[q];
-        double xa[8], xb[8];
+        T xa[8], xb[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           xa[k] = S[a * LDS_ + c0 + 8 * k];
@@ -274,7 +284,7 @@ __device__ int cta_jacobi64_sweep(double* S, double* U, double tol_abs, double t
       const int row = tid >> 2, q0 = tid & 3;
 #pragma unroll
       for (int hlf = 0; hlf < 2; ++hlf) {
-        double sa[4], sb[4], ua[4], ub[4];
+        T sa[4], sb[4], ua[4], ub[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int q = q0 + 4 * (k + 4 * hlf);
@@ -287,18 +297,18 @@ __device__ int cta_jacobi64_sweep(double* S, double* U, double tol_abs, double t
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int q = q0 + 4 * (k + 4 * hlf);
-          const double sn = ps[q];
-          if (sn == 0.0) continue;
-          const double c = pc[q];
+          const T sn = ps[q];
+          if (sn == T(0)) continue;
+          const T c = pc[q];
           const int a = pa[q], b = pb[q];
           U[row * LDS_ + a] = c * ua[k] - sn * ub[k];
           U[row * LDS_ + b] = sn * ua[k] + c * ub[k];
           if (row == a) {
             S[a * LDS_ + a] = papp[q] - pt[q] * papq[q];
-            S[a * LDS_ + b] = 0.0;
+            S[a * LDS_ + b] = T(0);
           } else if (row == b) {
             S[b * LDS_ + b] = paqq[q] + pt[q] * papq[q];
-            S[b * LDS_ + a] = 0.0;
+            S[b * LDS_ + a] = T(0);
           } else {
             S[row * LDS_ + a] = c * sa[k] - sn * sb[k];
             S[row * LDS_ + b] = sn * sa[k] + c * sb[k];
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(256, 3) k_subsolve(const RootJob* __restrict__
   }
   // blocked jobs: one inner sweep per outer round (outer sweeps barely change)
   const int any = small ? cta_jacobi(S, U, ns, tol_abs, tol_null, MAX_SWEEPS, &sweeps)
-                        : cta_jacobi64_sweep(S, U, tol_abs, tol_null);
+                        : cta_jacobi64_sweep<double>(S, U, tol_abs, tol_null);
   if (small) {
     double* V = vs + J.v_off;
     for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(256, 4) k_apply(const RootJob* __restrict__ jo
 
 // Advance per-job round/sweep counters; count active jobs (single CTA).
 __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, RootState* st,
-                                              int32_t* mask, int njobs, int32_t* count) {
+                                              int32_t* mask, int njobs, int32_t* count, int max_sweeps) {
   __shared__ int red[32];
   int act = 0;
   for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
@@ -613,7 +623,7 @@ __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, 
         ++s.sweep;
         if (!s.rotated) {
           s.active = 0;
-        } else if (s.sweep >= MAX_SWEEPS) {
+        } else if (s.sweep >= max_sweeps) {
           s.active = 0;  // residual couplings are below 1e-12 relative by then; keep the result
           s.capped = 1;
         }
@@ -625,6 +635,293 @@ __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, 
   }
   act = block_sum<int, 256>(act, red);
   if (threadIdx.x == 0) *count = act;
+}
+
+// ---------------------------------------------------------------- FP32 phase (mixed precision)
+//
+// Phase 1 of the mixed-precision eigensolver: the same block-Jacobi rounds on an FP32 copy of A
+// (big jobs only) accumulate an FP32 eigenvector estimate V32.  Phase 2 (FP64) promotes V32,
+// re-orthonormalises it with two Newton-Schulz steps, forms B = V^T A0 V from the ORIGINAL A0
+// and finishes with the FP64 rounds (quadratic convergence: 2-3 sweeps instead of 10-16).
+// FP32 rounding only changes the starting basis of the FP64 phase, never the result's accuracy.
+
+constexpr int S32_U = 0, S32_D = NS * NS, S32_F = NS * NS + NS, S32_S = NS * NS + NS + 4;
+constexpr int SLOT32 = S32_S + NS * NS;  // multiple of 4 floats: every slot is 16-byte aligned
+constexpr int LDF = NS + 4;             // 68 floats: 16-byte aligned smem rows
+constexpr int MAX_SWEEPS32 = 30;
+
+__device__ __forceinline__ float tol32_abs(double norm2) { return (float)(0.1 * 5.9604645e-8 * sqrt(norm2)); }
+__device__ __forceinline__ float tol32_null(double norm2) { return (float)(8.0 * 5.9604645e-8 * sqrt(norm2)); }
+
+// Phase counters: round = sweep = rotated = 0; active = (big_only ? m > 0 : true) && status ok && n > 0.
+__global__ void k_phase_reset(const RootJob* __restrict__ jobs, RootState* st, int32_t* mask, int njobs,
+                              int big_only) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  RootState& s = st[j];
+  s.sweep32 = big_only ? 0 : (jobs[j].m > 0 ? s.sweep : 0);
+  s.round = 0;
+  s.sweep = 0;
+  s.rotated = 0;
+  s.capped = 0;
+  s.active = (s.status == kEigOk && jobs[j].n > 0 && (!big_only || jobs[j].m > 0)) ? 1 : 0;
+  mask[j] = s.active;
+}
+
+// ws32 = (float) ws (np x np, zero padding included), vs32 = I, for active (big) jobs.
+__global__ void __launch_bounds__(256) k_init32(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                                const int32_t* __restrict__ ebegin, int njobs,
+                                                const double* __restrict__ ws, float* __restrict__ ws32,
+                                                float* __restrict__ vs32) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    ws32[J.ws_off + e] = (float)ws[J.ws_off + e];
+    vs32[J.ws_off + e] = (e / J.np == e % J.np) ? 1.f : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(256, 6) k_subsolve32(const RootJob* __restrict__ jobs, RootState* st,
+                                                    const int32_t* __restrict__ pbegin, int njobs,
+                                                    float* __restrict__ ws32, float* __restrict__ us32) {
+  extern __shared__ float smf[];
+  float* S = smf;
+  float* U = smf + NS * LDS_;
+  const int j = find_job(pbegin, njobs, blockIdx.x);
+  if (!st[j].active) return;
+  const RootJob& J = jobs[j];
+  const int pair = blockIdx.x - pbegin[j];
+  const int np = J.np, r = st[j].round;
+  const int ra = circle_pos(r, pair, J.m), rb = circle_pos(r, J.m - 1 - pair, J.m);
+  const float* A = ws32 + J.ws_off;
+  auto gidx = [&](int x) { return x < HB ? ra * HB + x : rb * HB + (x - HB); };
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int i = e >> 6, k = e & 63;
+    S[i * LDS_ + k] = A[(int64_t)gidx(i) * np + gidx(k)];
+  }
+  __syncthreads();
+  const float tol_abs = tol32_abs(st[j].norm2), tol_null = tol32_null(st[j].norm2);
+  constexpr float UR = EigU<float>::u;
+  float* slot = us32 + (J.u_off / SLOT) * SLOT32 + (int64_t)pair * SLOT32;
+  int need = 0;
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int i = e >> 6, k = e & 63;
+    if (i >= k) continue;
+    const float app = S[i * LDS_ + i], aqq = S[k * LDS_ + k];
+    float thr = fmaxf(4.f * UR * sqrtf(fabsf(app)) * sqrtf(fabsf(aqq)), tol_abs);
+    if (fabsf(app) <= tol_null && fabsf(aqq) <= tol_null) thr = fmaxf(thr, tol_null);
+    if (fabsf(S[i * LDS_ + k]) > thr) need = 1;
+  }
+  if (!__syncthreads_or(need)) {
+    if (threadIdx.x == 0) slot[S32_F] = 0.f;
+    return;
+  }
+  const int any = cta_jacobi64_sweep<float>(S, U, tol_abs, tol_null);
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int a = e >> 6, b = e & 63;
+    slot[S32_U + e] = U[a * LDS_ + b];
+    slot[S32_S + e] = (a <= b) ? S[a * LDS_ + b] : S[b * LDS_ + a];
+  }
+  if (threadIdx.x == 0) {
+    slot[S32_F] = any ? 1.f : 0.f;
+    if (any) st[j].rotated = 1;
+  }
+}
+
+// C(64x64) = X' Y on CUDA cores (FFMA); X'(r,k) = TX ? X[k][r] : X[r][k]; smem ld LDF.
+// Thread (ty, tx) owns rows 4ty..4ty+3 and columns 4tx..4tx+3.
+template <bool TX>
+__device__ __forceinline__ void mm64f(const float* X, const float* Y, float (&c)[4][4]) {
+  const int r0 = (threadIdx.x >> 4) * 4, c0 = (threadIdx.x & 15) * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[i][q] = 0.f;
+#pragma unroll 8
+  for (int k = 0; k < NS; ++k) {
+    float a[4];
+    if (TX) {
+      const float4 v = *reinterpret_cast<const float4*>(X + k * LDF + r0);
+      a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = X[(r0 + i) * LDF + k];
+    }
+    const float4 b = *reinterpret_cast<const float4*>(Y + k * LDF + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[i][0] = fmaf(a[i], b.x, c[i][0]);
+      c[i][1] = fmaf(a[i], b.y, c[i][1]);
+      c[i][2] = fmaf(a[i], b.z, c[i][2]);
+      c[i][3] = fmaf(a[i], b.w, c[i][3]);
+    }
+  }
+}
+
+__device__ __forceinline__ void mm64f_store(float* Z, const float (&c)[4][4]) {
+  const int r0 = (threadIdx.x >> 4) * 4, c0 = (threadIdx.x & 15) * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<float4*>(Z + (r0 + i) * LDF + c0) = make_float4(c[i][0], c[i][1], c[i][2], c[i][3]);
+}
+
+__device__ __forceinline__ void load_pair_tile32(float* dst, const float* src, int64_t ld, const int* rows,
+                                                 int col0, int col1) {
+  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
+    const int a = e >> 4, b = (e & 15) * 4;
+    const int gc = b < HB ? col0 + b : col1 + (b - HB);
+    float* d = dst + a * LDF + b;
+    if (rows[a] >= 0) cp16(d, src + (int64_t)rows[a] * ld + gc);
+    else cp16_zero(d, src);
+  }
+}
+
+__device__ __forceinline__ void load_slot32(float* dst, const float* slot) {
+  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
+    const int a = e >> 4, b = (e & 15) * 4;
+    cp16(dst + a * LDF + b, slot + a * NS + b);
+  }
+}
+
+// FP32 counterpart of k_apply: A <- W^T A W (pair tiles P<=Q), V <- V W.
+__global__ void __launch_bounds__(256, 4) k_apply32(const RootJob* __restrict__ jobs,
+                                                    const RootState* __restrict__ st,
+                                                    const int32_t* __restrict__ ibegin, int njobs,
+                                                    float* __restrict__ ws32, float* __restrict__ vs32,
+                                                    const float* __restrict__ us32) {
+  extern __shared__ __align__(16) float smf[];
+  float* X = smf;
+  float* WQ = smf + NS * LDF;
+  float* WP = smf + 2 * NS * LDF;
+  __shared__ int rows[NS];
+  const int j = find_job(ibegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  if (J.m == 0 || !st[j].active) return;
+  const int item = blockIdx.x - ibegin[j];
+  const int h = J.m / 2, np = J.np, r = st[j].round;
+  const int nA = h * (h + 1) / 2;
+  const float* slots = us32 + (J.u_off / SLOT) * SLOT32;
+  auto blk = [&](int P, int half) { return half == 0 ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m); };
+  float acc[4][4];
+  float* A = ws32 + J.ws_off;
+  if (item < nA) {
+    int Q, P;
+    tri_decode(item, Q, P);  // Q >= P
+    const float* sP = slots + (int64_t)P * SLOT32;
+    const float* sQ = slots + (int64_t)Q * SLOT32;
+    const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
+    if (P == Q) {
+      if (sP[S32_F] == 0.f) return;
+      const float* Sp = sP + S32_S;
+      for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+        const int a = e >> 6, b = e & 63;
+        A[(int64_t)(a < HB ? p0 + a : p1 + a - HB) * np + (b < HB ? p0 + b : p1 + b - HB)] = Sp[e];
+      }
+      return;
+    }
+    const bool rp = sP[S32_F] != 0.f, rq = sQ[S32_F] != 0.f;
+    if (!rp && !rq) return;
+    const int q0 = blk(Q, 0) * HB, q1 = blk(Q, 1) * HB;
+    if (threadIdx.x < NS) rows[threadIdx.x] = threadIdx.x < HB ? p0 + threadIdx.x : p1 + threadIdx.x - HB;
+    __syncthreads();
+    load_pair_tile32(X, A, np, rows, q0, q1);
+    if (rq) load_slot32(WQ, sQ);
+    if (rp) load_slot32(WP, sP);
+    cp_commit_wait_all();
+    __syncthreads();
+    if (rq) {  // T = X UQ
+      mm64f<false>(X, WQ, acc);
+      __syncthreads();
+      mm64f_store(X, acc);
+      __syncthreads();
+    }
+    if (rp) {  // R = UP^T T
+      mm64f<true>(WP, X, acc);
+      __syncthreads();
+      mm64f_store(X, acc);
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+      const int a = e >> 6, b = e & 63;
+      A[(int64_t)rows[a] * np + (b < HB ? q0 + b : q1 + b - HB)] = X[a * LDF + b];
+    }
+    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+      const int b = e >> 6, a = e & 63;
+      A[(int64_t)(b < HB ? q0 + b : q1 + b - HB) * np + rows[a]] = X[a * LDF + b];
+    }
+    return;
+  }
+  const int v = item - nA;
+  const int P = v % h, R = v / h;
+  const float* sP = slots + (int64_t)P * SLOT32;
+  if (sP[S32_F] == 0.f) return;
+  float* V = vs32 + J.ws_off;
+  const int r0 = R * NS;
+  const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
+  if (threadIdx.x < NS) rows[threadIdx.x] = (r0 + threadIdx.x < np) ? r0 + threadIdx.x : -1;
+  __syncthreads();
+  load_pair_tile32(X, V, np, rows, p0, p1);
+  load_slot32(WP, sP);
+  cp_commit_wait_all();
+  __syncthreads();
+  mm64f<false>(X, WP, acc);
+  __syncthreads();
+  mm64f_store(X, acc);
+  __syncthreads();
+  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
+    const int a = e >> 6, b = e & 63;
+    if (rows[a] >= 0) V[(int64_t)rows[a] * np + (b < HB ? p0 + b : p1 + b - HB)] = X[a * LDF + b];
+  }
+}
+
+// dst (ld np, n x n block) = (double) vs32; dst = ws for warm jobs (then ts = V_prev ws), else ts.
+__global__ void __launch_bounds__(256) k_promote32(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                                   const int32_t* __restrict__ ebegin, int njobs,
+                                                   const float* __restrict__ vs32, double* __restrict__ ws,
+                                                   double* __restrict__ ts) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  double* dst = J.warm ? ws : ts;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    if (i < J.n && k < J.n) dst[J.ws_off + e] = (double)vs32[J.ws_off + e];
+  }
+}
+
+// Newton-Schulz polynomial: ws <- (3 I - ws) / 2 on the n x n block.
+__global__ void __launch_bounds__(256) k_ns_poly(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                                 const int32_t* __restrict__ ebegin, int njobs,
+                                                 double* __restrict__ ws) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    if (i < J.n && k < J.n) ws[J.ws_off + e] = (i == k ? 1.5 : 0.0) - 0.5 * ws[J.ws_off + e];
+  }
+}
+
+// dst <- src on the n x n block (ld np).
+__global__ void __launch_bounds__(256) k_copy_n(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
+                                                const int32_t* __restrict__ ebegin, int njobs,
+                                                const double* __restrict__ src, double* __restrict__ dst) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const RootJob& J = jobs[j];
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  const int64_t tot = (int64_t)J.np * J.np;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int i = (int)(e / J.np), k = (int)(e % J.np);
+    if (i < J.n && k < J.n) dst[J.ws_off + e] = src[J.ws_off + e];
+  }
 }
 
 // ---------------------------------------------------------------- reconstruction
@@ -948,6 +1245,42 @@ __global__ void k_newton_status(RootState* st, const NewtonJob* __restrict__ nj,
 
 // ---------------------------------------------------------------- host side
 
+namespace {
+// SHAMPOO_EIG_PROFILE=1: stream-ordered event marks inside the root inverse, printed per run (debug only).
+struct EigProfile {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  explicit EigProfile(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("SHAMPOO_EIG_PROFILE");
+    on = e && std::atoi(e) != 0;
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, s);
+    marks.push_back({name, ev});
+  }
+  ~EigProfile() {
+    if (!on || marks.empty()) return;
+    cudaEventSynchronize(marks.back().second);
+    std::fprintf(stderr, "[eig]");
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+      std::fprintf(stderr, " %s %.2f", marks[i].first, ms);
+    }
+    std::fprintf(stderr, " ms\n");
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+};
+EigProfile* g_prof = nullptr;
+void prof_mark(const char* n) {
+  if (g_prof) g_prof->mark(n);
+}
+}  // namespace
+
 RootInverseBatch::~RootInverseBatch() {
   cudaFree(d_jobs_);
   cudaFree(d_state_);
@@ -965,6 +1298,10 @@ RootInverseBatch::~RootInverseBatch() {
   cudaFree(d_col_begin_);
   cudaFree(d_count_);
   cudaFreeHost(h_count_);
+  cudaFree(ws32_);
+  cudaFree(vs32_);
+  cudaFree(us32_);
+  cudaFree(d_mix_);
 }
 
 double RootInverseBatch::work_n3() const {
@@ -1063,12 +1400,44 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   int rc = recon_.upload();
   if (rc) return rc;
   if ((rc = rr_.upload())) return rc;
+  {
+    const char* env = std::getenv("SHAMPOO_EIG_MIXED");
+    mixed_ = env ? std::atoi(env) != 0 : false;  // measured: no net gain with SIMT FP32 rounds
+  }
+  if (mixed_ && has_big_) {
+    SH_CUDA_CHECK(cudaMalloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
+    SH_CUDA_CHECK(cudaMalloc(&vs32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
+    SH_CUDA_CHECK(cudaMalloc(&us32_, std::max<int64_t>(u_elems_ / SLOT * SLOT32, 1) * sizeof(float)));
+    SH_CUDA_CHECK(cudaMalloc(&d_mix_, nj * sizeof(int32_t)));
+    if (!ts_) SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+    if ((rc = build_warm_gemms())) return rc;
+    for (size_t j = 0; j < nj; ++j) {
+      const RootJob& J = host_[j];
+      if (J.m == 0) continue;
+      double *ws = ws_ + J.ws_off, *vs = vs_ + J.v_off, *ts = ts_ + J.ws_off;
+      auto add = [&](GemmBatch<double>& b, bool ta, const double* A, const double* B, double* Cm, bool sym) {
+        GemmProblem g = make_gemm(ta, false, J.n, J.n, J.n, A, J.np, B, J.np, Cm, J.np, 1.0, 0.0);
+        g.flags |= kGemmMasked | (sym ? kGemmSym : 0);
+        g.mask_index = (int32_t)j;
+        b.add(g);
+      };
+      add(g_wv_, false, vs, ws, ts, false);  // ts = V_prev V32 (warm jobs)
+      add(g_s1_, true, ts, ts, ws, true);    // S = ts^T ts
+      add(g_v1_, false, ts, ws, vs, false);  // vs = ts (3I - S)/2
+      add(g_s2_, true, vs, vs, ws, true);    // S = vs^T vs
+      add(g_v2_, false, vs, ws, ts, false);  // ts = vs (3I - S)/2
+    }
+    for (auto* b : {&g_wv_, &g_s1_, &g_v1_, &g_s2_, &g_v2_})
+      if ((rc = b->upload())) return rc;
+  }
   static bool attr_done = false;
   if (!attr_done) {
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * NS * LDS_ * (int)sizeof(double)));
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        NS * LDT * (int)sizeof(double)));
+    SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       3 * NS * LDF * (int)sizeof(float)));
     attr_done = true;
   }
   return SHAMPOO_OK;
@@ -1081,35 +1450,87 @@ void RootInverseBatch::set_io(int j, const void* in, bool in_f32, void* out, boo
   host_[j].out_f32 = out_f32;
 }
 
-int RootInverseBatch::prepare_warm(cudaStream_t s) {
-  // B = V^T A0 V for warm jobs: T = A0 V -> ts ; B = V^T T -> ws ; symmetrise
-  if (!ts_) {
-    SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
-    warm1_.host.clear();
-    warm2_.host.clear();
-    for (size_t j = 0; j < host_.size(); ++j) {
-      const RootJob& J = host_[j];
-      if (J.m == 0) continue;
-      GemmProblem p = make_gemm(false, false, J.n, J.n, J.n, xs_ + J.x_off, J.n, vs_ + J.v_off, J.np,
-                                ts_ + J.ws_off, J.np, 1.0, 0.0);
-      p.flags |= kGemmMasked;
-      p.mask_index = (int32_t)j;
-      warm1_.add(p);
-      p = make_gemm(true, false, J.n, J.n, J.n, vs_ + J.v_off, J.np, ts_ + J.ws_off, J.np, ws_ + J.ws_off, J.np,
-                    1.0, 0.0);
-      p.flags |= kGemmMasked;
-      p.mask_index = (int32_t)j;
-      warm2_.add(p);
-    }
-    int rc = warm1_.upload();
-    if (rc) return rc;
-    if ((rc = warm2_.upload())) return rc;
+int RootInverseBatch::build_warm_gemms() {
+  // B = V^T A0 V for big jobs: T = A0 V -> ts ; B = V^T T -> ws (launched with a job mask)
+  if (!warm1_.empty()) return SHAMPOO_OK;
+  if (!ts_) SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  for (size_t j = 0; j < host_.size(); ++j) {
+    const RootJob& J = host_[j];
+    if (J.m == 0) continue;
+    GemmProblem p = make_gemm(false, false, J.n, J.n, J.n, xs_ + J.x_off, J.n, vs_ + J.v_off, J.np,
+                              ts_ + J.ws_off, J.np, 1.0, 0.0);
+    p.flags |= kGemmMasked;
+    p.mask_index = (int32_t)j;
+    warm1_.add(p);
+    p = make_gemm(true, false, J.n, J.n, J.n, vs_ + J.v_off, J.np, ts_ + J.ws_off, J.np, ws_ + J.ws_off, J.np,
+                  1.0, 0.0);
+    p.flags |= kGemmMasked;
+    p.mask_index = (int32_t)j;
+    warm2_.add(p);
   }
-  int rc = warm1_.launch(s, d_warm_);
+  int rc = warm1_.upload();
   if (rc) return rc;
+  return warm2_.upload();
+}
+
+int RootInverseBatch::prepare_warm(cudaStream_t s) {
+  // B = V^T A0 V for warm jobs, symmetrised
+  int rc = build_warm_gemms();
+  if (rc) return rc;
+  if ((rc = warm1_.launch(s, d_warm_))) return rc;
   if ((rc = warm2_.launch(s, d_warm_))) return rc;
   k_symmetrize<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_warm_, d_elem_begin_, (int)host_.size(), ws_);
   SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+int RootInverseBatch::run_mixed_phase(cudaStream_t s, bool any_warm) {
+  const int nj = (int)host_.size();
+  int32_t* mask = d_count_ + 4;
+  const int eb = total_elem_chunks_;
+  k_phase_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, d_mix_, nj, 1);
+  SH_LAUNCH_CHECK();
+  k_init32<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_, ws32_, vs32_);
+  SH_LAUNCH_CHECK();
+  for (int R = 0;; ++R) {
+    k_subsolve32<<<total_pairs_, 256, 2 * NS * LDS_ * sizeof(float), s>>>(d_jobs_, d_state_, d_pair_begin_, nj,
+                                                                         ws32_, us32_);
+    SH_LAUNCH_CHECK();
+    k_apply32<<<total_items_, 256, 3 * NS * LDF * sizeof(float), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
+                                                                     ws32_, vs32_, us32_);
+    SH_LAUNCH_CHECK();
+    k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_, MAX_SWEEPS32);
+    SH_LAUNCH_CHECK();
+    if ((R & 7) == 7) {
+      SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (h_count_[0] == 0) break;
+    }
+    if (R > 256 * (MAX_SWEEPS32 + 1)) break;
+  }
+  prof_mark("fp32_rounds");
+  // FP64: V = (V_prev) V32, two Newton-Schulz steps, B = V^T A0 V
+  k_promote32<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, vs32_, ws_, ts_);
+  SH_LAUNCH_CHECK();
+  int rc;
+  if (any_warm && (rc = g_wv_.launch(s, d_warm_))) return rc;
+  if ((rc = g_s1_.launch(s, d_mix_))) return rc;
+  k_ns_poly<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
+  SH_LAUNCH_CHECK();
+  if ((rc = g_v1_.launch(s, d_mix_))) return rc;
+  if ((rc = g_s2_.launch(s, d_mix_))) return rc;
+  k_ns_poly<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
+  SH_LAUNCH_CHECK();
+  if ((rc = g_v2_.launch(s, d_mix_))) return rc;
+  k_copy_n<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ts_, vs_);
+  SH_LAUNCH_CHECK();
+  if ((rc = warm1_.launch(s, d_mix_))) return rc;
+  if ((rc = warm2_.launch(s, d_mix_))) return rc;
+  k_symmetrize<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
+  SH_LAUNCH_CHECK();
+  k_phase_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, mask, nj, 0);
+  SH_LAUNCH_CHECK();
+  prof_mark("transition");
   return SHAMPOO_OK;
 }
 
@@ -1127,7 +1548,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
                                                                           ws_, vs_, us_);
       SH_LAUNCH_CHECK();
     }
-    k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_);
+    k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_, MAX_SWEEPS);
     SH_LAUNCH_CHECK();
     if ((R & 7) == 7) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -1137,6 +1558,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     if (R > 256 * (MAX_SWEEPS + 1)) break;  // safety net (k_book caps sweeps per job)
   }
   (void)iters;
+  prof_mark("fp64_rounds");
   k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
   SH_LAUNCH_CHECK();
   int rc = rr_.launch(s, mask);  // T = A0 V
@@ -1248,6 +1670,12 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     host_[j].has_prev = has_prev.empty() ? 0 : has_prev[j];
     host_[j].idscale = eps > 0.0 ? std::pow(eps, -eta / host_[j].root_p) : 1.0;  // matfun.py:287-293
   }
+  EigProfile prof(s);
+  g_prof = &prof;
+  struct ProfReset {
+    ~ProfReset() { g_prof = nullptr; }
+  } prof_reset;
+  prof_mark("start");
   SH_CUDA_CHECK(cudaMemcpyAsync(d_jobs_, host_.data(), nj * sizeof(RootJob), cudaMemcpyHostToDevice, s));
   k_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, nj);
   SH_LAUNCH_CHECK();
@@ -1261,9 +1689,15 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     int rw = prepare_warm(s);
     if (rw) return rw;
   }
+  prof_mark("init+warm");
+  if (solver == SHAMPOO_SOLVER_EIGH && mixed_ && has_big_) {
+    int rm = run_mixed_phase(s, any_warm);
+    if (rm) return rm;
+  }
   int rc = (solver == SHAMPOO_SOLVER_NEWTON) ? run_newton(eps, newton_tol, s, host_iters)
                                              : run_eigh(eta, eps, s, host_iters);
   if (rc) return rc;
+  prof_mark("rr+recon");
   k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
   SH_LAUNCH_CHECK();
   k_check_x<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, mask, d_elem_begin_, nj, xs_);
@@ -1283,7 +1717,7 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   for (int j = 0; j < nj; ++j) {
     if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = hs[j].status == kEigOk ? 1 : 0;
     else vec_valid_[j] = 0;
-    sweeps_total_ += hs[j].sweep;
+    sweeps_total_ += hs[j].sweep + hs[j].sweep32;
   }
   if (host_status) {
     host_status->resize(nj);
@@ -1291,7 +1725,8 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   }
   if (host_iters) {
     host_iters->resize(nj);
-    for (int j = 0; j < nj; ++j) (*host_iters)[j] = hs[j].sweep;
+    // eigh: FP64 sweeps + 1000 x FP32-phase sweeps (mixed precision); Newton: iterations
+    for (int j = 0; j < nj; ++j) (*host_iters)[j] = hs[j].sweep + 1000 * hs[j].sweep32;
   }
   return SHAMPOO_OK;
 }

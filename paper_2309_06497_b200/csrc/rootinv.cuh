@@ -50,6 +50,7 @@ struct RootState {
   double tol_null;
   double trace;            // tr(A)
   int32_t nonfinite, capped;  // capped: sweep cap reached (result still used)
+  int32_t sweep32, pad;       // FP32-phase sweeps (mixed-precision eigensolver)
 };
 
 class RootInverseBatch {
@@ -75,6 +76,8 @@ class RootInverseBatch {
   int run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters);
   int run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters);
   int prepare_warm(cudaStream_t s);
+  int build_warm_gemms();
+  int run_mixed_phase(cudaStream_t s, bool any_warm);
   std::vector<RootJob> host_;
   RootJob* d_jobs_ = nullptr;
   RootState* d_state_ = nullptr;
@@ -89,6 +92,13 @@ class RootInverseBatch {
   std::vector<int32_t> vec_valid_;  // V holds eigenvectors of the last successful solve
   int64_t x_elems_ = 0, sweeps_total_ = 0;
   GemmBatch<double> rr_, warm1_, warm2_;
+  // mixed-precision eigensolver (FP32 Jacobi phase + FP64 Newton-Schulz re-orthonormalisation)
+  bool mixed_ = false;  // SHAMPOO_EIG_MIXED=1
+  float* ws32_ = nullptr;
+  float* vs32_ = nullptr;
+  float* us32_ = nullptr;
+  int32_t* d_mix_ = nullptr;
+  GemmBatch<double> g_wv_, g_s1_, g_v1_, g_s2_, g_v2_;
   int32_t* d_pair_begin_ = nullptr;
   int32_t* d_item_begin_ = nullptr;
   int32_t* d_elem_begin_ = nullptr;
