@@ -227,6 +227,16 @@ SHAMPOO_API int shampoo_batched_root_inverse(const double* const* mats, double* 
                                  double newton_tolerance, int32_t* status, int32_t* iters,
                                  void* stream);
 
+/* ---- tensor-core GEMM utility: C (M x N) = alpha * A B^T + beta * C on tcgen05.mma kind::i8 with
+ * Ozaki operand splitting (per-row power-of-two scaling, 7-bit int8 slices, exact int32
+ * accumulation in TMEM, slice diagonals combined in FP64): 8 slices for dtype F64 (operand
+ * truncation 2^-56 of each row's maximum), 5 for F32 (2^-35).  A (M x K), B (N x K), C row-major
+ * device buffers of `dtype`.  symmetric != 0 requires A == B, M == N: tiles on/below the diagonal
+ * are computed and mirrored (exactly symmetric C).  This engine runs the factor statistics and the
+ * mode products of the optimizer step (precond.py:161-174).  Synchronous. */
+SHAMPOO_API int shampoo_tc_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                int32_t symmetric, double alpha, double beta, int32_t dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

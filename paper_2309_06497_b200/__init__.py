@@ -18,7 +18,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent pieces load lazily so planning works without CUDA initialisation
-    if name in ("Shampoo", "GuardStats", "batched_root_inverse", "launch_count"):
+    if name in ("Shampoo", "GuardStats", "batched_root_inverse", "launch_count", "tc_gemm"):
         from . import optimizer
         return getattr(optimizer, name)
     if name in ("DistributedShampoo", "GroupExchange"):
@@ -31,7 +31,7 @@ __all__ = [
     "AssignmentPlan", "BlockPlan", "BlockRegion", "BlockSpec", "BufferOverflowError", "DistributedShampoo",
     "DivergedReplicasError", "GlobalBlock", "GraftKind", "GroupExchange", "GuardStats",
     "InvalidGroupSizeError", "LargeDimMethod", "NativeError", "NativePlan", "NonFiniteGradientError",
-    "OutOfRangeError", "Shampoo", "ShampooConfig", "Solver", "batched_root_inverse", "block_partition",
+    "OutOfRangeError", "Shampoo", "ShampooConfig", "Solver", "batched_root_inverse", "tc_gemm", "block_partition",
     "buffer_size", "enumerate_blocks", "greedy_assign", "launch_count", "lr_at", "merge_dims",
     "plan_parameter", "state_scalar_count",
 ]

@@ -100,6 +100,7 @@ SIGNATURES = {
     "shampoo_graft_step_set": (C.c_int, [_P, _I64]),
     "shampoo_batched_root_inverse": (C.c_int, [C.POINTER(_P), C.POINTER(_P), _PI32, _I32, _I32, _D, _D,
                                                _I32, _D, _PI32, _PI32, _P]),
+    "shampoo_tc_gemm": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _I32, _P]),
 }
 
 _lib = None

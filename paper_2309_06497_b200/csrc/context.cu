@@ -16,6 +16,8 @@
 
 #include "elementwise.cuh"
 #include "gemm.cuh"
+#include "tcgen05.cuh"
+#include "thin.cuh"
 #include "rootinv.cuh"
 
 namespace shampoo {
@@ -32,8 +34,13 @@ struct EngineBase {
 
 template <typename T>
 struct Engine : EngineBase {
-  GemmBatch<T> stats;                  // factor EMA updates, all owned blocks x modes
-  GemmBatch<T> prec[kMaxOrder];        // mode-k products, k = 0..order-1 (order >= 2)
+  // tcgen05 int8 tensor cores, Ozaki split (exact accumulation; 8 slices for double, 5 for single)
+  OzakiGemmBatch<T> stats;             // factor EMA updates, all owned blocks x modes
+  OzakiGemmBatch<T> prec[kMaxOrder];   // mode-k products, k = 0..order-1 (order >= 2)
+  // problems too thin for a 128 x 64 tensor-core tile (rank-1 factor updates of vector blocks,
+  // 3 x 3 / 7 x 7 kernel modes): HBM-bound CUDA-core kernels, exact products, FP64 sums
+  ThinGemmBatch<T> stats_thin;
+  ThinGemmBatch<T> prec_thin[kMaxOrder];
   GemvBatch<T> prec1;                  // order-1 blocks: P = X g
 };
 
@@ -227,6 +234,9 @@ ElemArenas arenas(shampoo_ctx* c) {
   return a;
 }
 
+// A problem too thin for the 128 x 64 tensor-core tiles.
+bool thin(const GemmProblem& p) { return ThinGemmBatch_accepts(p); }
+
 template <typename T>
 int build_engine(shampoo_ctx* c) {
   auto* e = new Engine<T>();
@@ -250,7 +260,11 @@ int build_engine(shampoo_ctx* c) {
       int64_t outer = 1, inner = 1;
       for (int q = 0; q < m; ++q) outer *= d[q];
       for (int q = m + 1; q < order; ++q) inner *= d[q];
-      e->stats.add(make_mode_gram(G + c->vofs[l], outer, d[m], inner, FACT + off, alpha, beta));
+      {
+        GemmProblem g = make_mode_gram(G + c->vofs[l], outer, d[m], inner, FACT + off, alpha, beta);
+        if (thin(g)) e->stats_thin.add(g);
+        else e->stats.add(g);
+      }
       if (order == 1) {
         GemvProblem gp{};
         gp.n = (int32_t)d[0];
@@ -266,18 +280,19 @@ int build_engine(shampoo_ctx* c) {
         GemmProblem p = make_mode_product(INV + off, in, out, outer, d[m], inner, 1.0);
         p.flags |= kGemmMasked;
         p.mask_index = (int32_t)l;
-        e->prec[m].add(p);
+        if (thin(p)) e->prec_thin[m].add(p);
+        else e->prec[m].add(p);
       }
       off += d[m] * d[m];
     }
   }
-  // single precision keeps float factors but accumulates the contraction in FP64, like the
-  // reference's float64 tensordot followed by one cast (precond.py:236)
-  e->stats.fp64_accumulate = true;
   int rc = e->stats.upload();
   if (rc) return rc;
-  for (int m = 0; m < kMaxOrder; ++m)
+  if ((rc = e->stats_thin.upload())) return rc;
+  for (int m = 0; m < kMaxOrder; ++m) {
     if ((rc = e->prec[m].upload())) return rc;
+    if ((rc = e->prec_thin[m].upload())) return rc;
+  }
   return e->prec1.upload();
 }
 
@@ -286,8 +301,10 @@ int precondition_impl(shampoo_ctx* c, cudaStream_t s) {
   Engine<T>& e = c->eng<T>();
   int rc;
   if ((rc = e.prec1.launch(s, c->d_ready))) return rc;
-  for (int m = 0; m < kMaxOrder; ++m)
+  for (int m = 0; m < kMaxOrder; ++m) {
     if ((rc = e.prec[m].launch(s, c->d_ready))) return rc;
+    if ((rc = e.prec_thin[m].launch(s, c->d_ready))) return rc;
+  }
   if ((rc = launch_sumsq<T>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, c->PS, c->part, s))) return rc;
   return launch_block_reduce(c->d_cb, c->d_cc, (int)c->owned.size(), c->part, c->ps2, s);
 }
@@ -563,6 +580,8 @@ int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* c
   if ((rc = launch_block_reduce(c->d_cb, c->d_cc, no, c->part, c->pg2, s))) return rc;
   rc = c->f32 ? c->eng<float>().stats.launch(s) : c->eng<double>().stats.launch(s);
   if (rc) return rc;
+  rc = c->f32 ? c->eng<float>().stats_thin.launch(s) : c->eng<double>().stats_thin.launch(s);
+  if (rc) return rc;
   if (c->n_fb_chunks) {
     const FallbackArgs fa = fallback_args(c, t);
     rc = c->f32 ? launch_fallback_update<float>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
@@ -667,14 +686,14 @@ int shampoo_timing_get(shampoo_ctx* c, double* ms, int64_t* counts) {
 
 int shampoo_work(shampoo_ctx* c, double* stats_flops, double* precond_flops, double* sum_n3) {
   if (c->f32) {
-    *stats_flops = c->eng<float>().stats.flops();
+    *stats_flops = c->eng<float>().stats.flops() + c->eng<float>().stats_thin.flops();
     double f = 0;
-    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<float>().prec[m].flops();
+    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<float>().prec[m].flops() + c->eng<float>().prec_thin[m].flops();
     *precond_flops = f;
   } else {
-    *stats_flops = c->eng<double>().stats.flops();
+    *stats_flops = c->eng<double>().stats.flops() + c->eng<double>().stats_thin.flops();
     double f = 0;
-    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<double>().prec[m].flops();
+    for (int m = 0; m < kMaxOrder; ++m) f += c->eng<double>().prec[m].flops() + c->eng<double>().prec_thin[m].flops();
     *precond_flops = f;
   }
   // order-1 matvecs: 2 n^2 each

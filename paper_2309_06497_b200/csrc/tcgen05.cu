@@ -1,0 +1,620 @@
+// Grouped Ozaki-split int8 GEMM on tcgen05 tensor cores (see tcgen05.cuh).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "tcgen05.cuh"
+
+namespace shampoo {
+
+namespace {
+
+constexpr int TM = 128, TN = 64, TKB = 32;    // CTA tile; 32 int8 (= one MMA K) per pipeline stage
+constexpr int GEMM_THREADS = 192;             // warp 0 bulk copies, warp 1 MMA, warps 2-5 epilogue
+constexpr int64_t kOzSplitStages = 256;       // 8192 k per split: int32 sums stay exact (< 2^31)
+constexpr int PACK_UNITS = 256;               // pack threads per CTA (one unit = 16 k of one row)
+constexpr int EXP_CHUNK = 64;                 // k per rowexp thread
+constexpr int kExpFloor = -1100;              // exponent of an all-zero row (ldexp -> 0)
+
+template <int S>
+struct OzCfg {
+  static constexpr int A_BYTES = (TM / 8) * S * 256;     // one stage of a 128-row tile, all slices
+  static constexpr int B_BYTES = (TN / 8) * S * 256;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE < 6 ? (200 * 1024) / STAGE : 6;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
+  static constexpr uint32_t TMEM_COLS = 512;             // S * TN <= 512
+  // kind::i8: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1), K-major, M = 128; N (bits 17-22)
+  // is set per instruction
+  static constexpr uint32_t IDESC_BASE = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TM >> 4) << 24);
+};
+
+__device__ __forceinline__ int64_t evx(const Idx2& x, int64_t v) {
+  if (x.div == 0x7fffffff) return v * x.lo;
+  return (v / x.div) * x.hi + (v % x.div) * x.lo;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ---- mbarrier / bulk copy (async proxy) ----
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// ---- tcgen05 ----
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, no swizzle, K-major: rows of 16 B inside an 8-row core
+// matrix, the two K cores LBO apart, consecutive 8-row cores SBO apart.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+}
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (int32_t)r[i];
+}
+
+template <typename P>
+__device__ __forceinline__ int find64(const int64_t* __restrict__ begin, int n, int64_t x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// SYM problems: 128 x 64 tiles that touch the lower triangle, tn <= 2 tm + 1, row-major order.
+__host__ __device__ __forceinline__ int64_t sym_tiles_before(int tm, int nt) {
+  int64_t c = 0;
+  for (int t = 0; t < tm; ++t) c += (2 * t + 2 < nt) ? 2 * t + 2 : nt;
+  return c;
+}
+__device__ __forceinline__ void sym_decode(int64_t l, int nt, int& tm, int& tn) {
+  int t = 0;
+  int64_t c = 0;
+  for (;; ++t) {
+    const int w = (2 * t + 2 < nt) ? 2 * t + 2 : nt;
+    if (l < c + w) break;
+    c += w;
+  }
+  tm = t;
+  tn = (int)(l - c);
+}
+
+// Epilogue for one element (same semantics as GemmBatch): SYM problems write i >= j and mirror
+// every off-diagonal value, so factors stay exactly symmetric.
+template <typename T>
+__device__ __forceinline__ void oz_store(const GemmProblem& P, int gi, int gj, double acc) {
+  if (gi >= P.M || gj >= P.N) return;
+  const bool sym = (P.flags & kGemmSym) != 0;
+  if (sym && gi < gj) return;
+  T* __restrict__ C = static_cast<T*>(P.C);
+  const int64_t at = evx(P.c_r, gi) + evx(P.c_c, gj);
+  double v = P.alpha * acc;
+  if (P.flags & kGemmReadC) v = fma(P.beta, (double)C[at], v);
+  const T o = (T)v;
+  C[at] = o;
+  if (sym && gi != gj) C[evx(P.c_r, gj) + evx(P.c_c, gi)] = o;
+}
+
+// Row exponents: e_r = max_k frexp-exponent(x_rk) (|x_rk| < 2^e_r).
+template <typename T>
+__global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__ jobs, const int64_t* __restrict__ ebegin,
+                                                   int njobs, const int32_t* __restrict__ mask, int32_t* __restrict__ exps) {
+  const int j = find64<OzPackJob>(ebegin, njobs, blockIdx.x);
+  const OzPackJob& J = jobs[j];
+  if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
+  const int64_t u = (int64_t)(blockIdx.x - ebegin[j]) * 256 + threadIdx.x;
+  if (u >= J.echunks) return;
+  const int nkc = (J.K + EXP_CHUNK - 1) / EXP_CHUNK;
+  const int row = (int)(u / nkc), k0 = (int)(u % nkc) * EXP_CHUNK;
+  const T* __restrict__ src = static_cast<const T*>(J.src);
+  const int64_t rb = evx(J.r, row);
+  double m = 0.0;
+  const int k1 = min(J.K, k0 + EXP_CHUNK);
+  for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)src[rb + evx(J.k, k)]));
+  if (m > 0.0) {
+    int e;
+    frexp(m, &e);
+    atomicMax(exps + J.exp + row, e);
+  }
+}
+
+// Operands -> int8 slice planes, slice-major per stage: byte offset
+// ((stage * S + s) * rc + core) * 256 + kc * 128 + r8 * 16 holds row 8 core + r8,
+// k = 32 stage + 16 kc .. +15 of slice s.  Unit u = ((stage * rc + core) * 2 + kc) * 8 + r8.
+template <typename T, int S>
+__global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restrict__ jobs,
+                                                        const int64_t* __restrict__ pbegin, int njobs,
+                                                        const int32_t* __restrict__ mask,
+                                                        const int32_t* __restrict__ exps, int8_t* __restrict__ arena) {
+  const int j = find64<OzPackJob>(pbegin, njobs, blockIdx.x);
+  const OzPackJob& J = jobs[j];
+  if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
+  const int64_t u = (int64_t)(blockIdx.x - pbegin[j]) * PACK_UNITS + threadIdx.x;
+  if (u >= J.units) return;
+  const int r8 = (int)(u & 7), kc = (int)((u >> 3) & 1);
+  const int64_t sc = u >> 4;  // stage * rc + core
+  const int core = (int)(sc % J.rc), stage = (int)(sc / J.rc);
+  const int row = core * 8 + r8;
+  const int k0 = stage * TKB + kc * 16;
+  uint32_t w[S][4];
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[s][q] = 0u;
+  if (row < J.rows) {
+    const T* __restrict__ src = static_cast<const T*>(J.src);
+    const int64_t rb = evx(J.r, row);
+    const int e = max(exps[J.exp + row], kExpFloor);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = k0 + i;
+      double y = (k < J.K) ? ldexp((double)src[rb + evx(J.k, k)], -e) : 0.0;  // |y| < 1, exact
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double t = y * 128.0;
+        const double q = trunc(t);   // |q| <= 127
+        y = t - q;                   // exact
+        w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)q) << (8 * (i & 3));
+      }
+    }
+  }
+  int8_t* dst = arena + J.dst + ((int64_t)stage * S * J.rc + core) * 256 + kc * 128 + r8 * 16;
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    *reinterpret_cast<uint4*>(dst + (int64_t)s * J.rc * 256) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+}
+
+// 2^e for e in the normal range (exact).
+__device__ __forceinline__ double pow2i(int e) {
+  e = max(-1022, min(1023, e));
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+constexpr int LDE = TN + 1;  // staged epilogue tile leading dim (doubles)
+
+template <typename T, int S>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_oz_gemm(const GemmProblem* __restrict__ probs,
+                                                            const OzProb* __restrict__ tps,
+                                                            const int64_t* __restrict__ begin, int nprob,
+                                                            const int32_t* __restrict__ mask,
+                                                            const int8_t* __restrict__ arena,
+                                                            const int32_t* __restrict__ exps, double* __restrict__ ws) {
+  using Cfg = OzCfg<S>;
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES], empty_bar[Cfg::STAGES], done_bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ double col_scale[TN];
+  __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
+  const int pi = find64<GemmProblem>(begin, nprob, blockIdx.x);
+  const GemmProblem& P = probs[pi];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const OzProb& T_ = tps[pi];
+  const int64_t l = blockIdx.x - begin[pi];
+  const int split = (int)(l % T_.ksplit);
+  const int64_t tile = l / T_.ksplit;
+  int tm, tn;
+  if (P.flags & kGemmSym) sym_decode(tile, T_.nt, tm, tn);
+  else {
+    tm = (int)(tile / T_.nt);
+    tn = (int)(tile % T_.nt);
+  }
+  const int s0 = split * T_.kst;
+  const int nk = min(T_.ks, s0 + T_.kst) - s0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
+  // row cores present in this tile (rows beyond M / N are never stored: their smem stays stale)
+  const int a_cores = min(TM / 8, T_.a_rc - tm * (TM / 8));
+  const int b_cores = min(TN / 8, T_.b_rc - tn * (TN / 8));
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    mbar_init(&done_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "n"(Cfg::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: per stage and slice, the tile's row cores (contiguous) of A and B
+      const int64_t a_plane = (int64_t)T_.a_rc * 256, b_plane = (int64_t)T_.b_rc * 256;
+      const int8_t* a_src = arena + T_.a_pack + (int64_t)s0 * S * a_plane + (int64_t)tm * (TM / 8) * 256;
+      const int8_t* b_src = arena + T_.b_pack + (int64_t)s0 * S * b_plane + (int64_t)tn * (TN / 8) * 256;
+      const uint32_t a_bytes = (uint32_t)a_cores * 256, b_bytes = (uint32_t)b_cores * 256;
+      for (int it = 0; it < nk; ++it) {
+        const int st = it % Cfg::STAGES;
+        const uint32_t use = (uint32_t)(it / Cfg::STAGES);
+        if (it >= Cfg::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
+        uint8_t* sb = sbase + (size_t)st * Cfg::STAGE;
+        mbar_expect_tx(&full_bar[st], (uint32_t)S * (a_bytes + b_bytes));
+        const int8_t* as = a_src + (int64_t)it * S * a_plane;
+        const int8_t* bs = b_src + (int64_t)it * S * b_plane;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st]);
+          bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // MMA issuer.  A slice sa times the B slices sb = 0 .. S-1-sa stacked along N (slice-major in
+      // smem): output column block sb lands at TMEM column (sa + sb) * 64 = accumulator of diagonal
+      // d = sa + sb.  N <= 256 per instruction.
+      for (int it = 0; it < nk; ++it) {
+        const int st = it % Cfg::STAGES;
+        mbar_wait(&full_bar[st], (uint32_t)(it / Cfg::STAGES) & 1u);
+        tc_fence_after();
+        const uint32_t sa_base = smem_u32(sbase + (size_t)st * Cfg::STAGE);
+        const uint32_t sb_base = sa_base + Cfg::A_BYTES;
+#pragma unroll
+        for (int sa = 0; sa < S; ++sa) {
+          const uint64_t ad = sdesc(sa_base + sa * (TM / 8) * 256, 128, 256);
+#pragma unroll
+          for (int sb0 = 0; sb0 < S - sa; sb0 += 4) {
+            const int nsl = min(4, S - sa - sb0);
+            const uint64_t bd = sdesc(sb_base + sb0 * (TN / 8) * 256, 128, 256);
+            const uint32_t idesc = Cfg::IDESC_BASE | ((uint32_t)(nsl * TN >> 3) << 17);
+            tc_mma_i8(tmem + (uint32_t)((sa + sb0) * TN), ad, bd, idesc, (it > 0 || sa > 0) ? 1u : 0u);
+          }
+        }
+        tc_commit(&empty_bar[st]);  // frees the stage once these MMAs have read it
+      }
+      tc_commit(&done_bar);
+    }
+  } else {
+    // epilogue (128 threads): TMEM -> FP64 diagonal combination -> smem tile -> coalesced stores
+    const int et = threadIdx.x - 64;
+    const int lg = warp & 3;
+    const int rl = lg * 32 + lane;
+    double* tileS = reinterpret_cast<double*>(sbase);  // pipeline smem is free once done_bar fires
+    if (et < TN) {
+      const int gj = tn * TN + et;
+      col_scale[et] = pow2i(exps[T_.b_exp + min(gj, T_.b_rc * 8 - 1)]);
+      col_off[et] = evx(P.c_c, gj);
+      mrow_off[et] = evx(P.c_r, gj);
+    }
+    {
+      const int gi = tm * TM + et;
+      row_off[et] = evx(P.c_r, gi);
+      mcol_off[et] = evx(P.c_c, gi);
+    }
+    mbar_wait(&done_bar, 0);
+    tc_fence_after();
+    const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
+    int32_t v[16];
+    for (int c0 = 0; c0 < TN; c0 += 16) {
+      double acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+      if (nk > 0) {
+#pragma unroll
+        for (int d = S - 1; d >= 0; --d) {  // smallest contributions first
+          tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * TN + c0), v);
+          const double wd = pow2i(-7 * (d + 2));
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[q] = fma((double)v[q], wd, acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) tileS[rl * LDE + c0 + q] = acc[q] * rscale;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const bool sym = (P.flags & kGemmSym) != 0;
+    if (T_.ksplit == 1) {
+      T* __restrict__ C = static_cast<T*>(P.C);
+      const bool readc = (P.flags & kGemmReadC) != 0;
+      for (int e0 = et; e0 < TM * TN; e0 += 8 * 128) {  // row-major over the tile: coalesced along columns
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // independent loads first (8 in flight per thread)
+          const int e = e0 + u * 128, r = e / TN, c = e % TN;
+          const int gi = tm * TM + r, gj = tn * TN + c;
+          const bool live = gi < P.M && gj < P.N && !(sym && gi < gj);
+          cv[u] = (readc && live) ? (double)C[row_off[r] + col_off[c]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * 128, r = e / TN, c = e % TN;
+          const int gi = tm * TM + r, gj = tn * TN + c;
+          if (gi >= P.M || gj >= P.N || (sym && gi < gj)) continue;
+          double val = P.alpha * (tileS[r * LDE + c] * col_scale[c]);
+          if (readc) val = fma(P.beta, cv[u], val);
+          tileS[r * LDE + c] = val;
+          C[row_off[r] + col_off[c]] = (T)val;
+        }
+      }
+      if (sym) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int e = et; e < TM * TN; e += 128) {  // mirror: coalesced along the tile's rows
+          const int c = e / TM, r = e % TM;
+          const int gi = tm * TM + r, gj = tn * TN + c;
+          if (gi >= P.M || gj >= P.N || gi <= gj) continue;
+          C[mrow_off[c] + mcol_off[r]] = (T)tileS[r * LDE + c];
+        }
+      }
+    } else {
+      double* dst = ws + T_.ws_off + (tile * T_.ksplit + split) * (int64_t)(TM * TN);
+      for (int e = et; e < TM * TN; e += 128) {
+        const int r = e / TN, c = e % TN;
+        dst[e] = tileS[r * LDE + c] * col_scale[c];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS) : "memory");
+  }
+}
+
+// Split-K: scaled partial tiles summed in split order in FP64, then the epilogue.
+template <typename T>
+__global__ void __launch_bounds__(256) k_oz_reduce(const GemmProblem* __restrict__ probs, const OzProb* __restrict__ tps,
+                                                   const int64_t* __restrict__ rbegin, const int32_t* __restrict__ rprob,
+                                                   int nred, const int32_t* __restrict__ mask,
+                                                   const double* __restrict__ ws) {
+  const int r = find64<int32_t>(rbegin, nred, blockIdx.x);
+  const int pi = rprob[r];
+  const GemmProblem& P = probs[pi];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const OzProb& T_ = tps[pi];
+  const int64_t tile = blockIdx.x - rbegin[r];
+  int tm, tn;
+  if (P.flags & kGemmSym) sym_decode(tile, T_.nt, tm, tn);
+  else {
+    tm = (int)(tile / T_.nt);
+    tn = (int)(tile % T_.nt);
+  }
+  const double* base = ws + T_.ws_off + tile * T_.ksplit * (int64_t)(TM * TN);
+  for (int e = threadIdx.x; e < TM * TN; e += blockDim.x) {
+    const int gi = tm * TM + e / TN, gj = tn * TN + e % TN;
+    if (gi >= P.M || gj >= P.N) continue;
+    double acc = 0.0;
+    for (int sp = 0; sp < T_.ksplit; ++sp) acc += base[(int64_t)sp * TM * TN + e];
+    oz_store<T>(P, gi, gj, acc);
+  }
+}
+
+}  // namespace
+
+template <typename T>
+OzakiGemmBatch<T>::~OzakiGemmBatch() {
+  cudaFree(d_prob_);
+  cudaFree(d_tp_);
+  cudaFree(d_begin_);
+  cudaFree(d_pack_);
+  cudaFree(d_pbegin_);
+  cudaFree(d_ebegin_);
+  cudaFree(d_rbegin_);
+  cudaFree(d_rprob_);
+  cudaFree(arena_);
+  cudaFree(exps_);
+  cudaFree(ws_);
+}
+
+template <typename T>
+int OzakiGemmBatch<T>::upload() {
+  if (host.empty()) return SHAMPOO_OK;
+  static bool attr = false;
+  if (!attr) {
+    SH_CUDA_CHECK(cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)OzCfg<S>::SMEM));
+    attr = true;
+  }
+  std::vector<OzProb> tp(host.size());
+  std::vector<int64_t> begin(host.size()), rbegin, pbegin, ebegin;
+  std::vector<int32_t> rprob;
+  std::vector<OzPackJob> jobs;
+  int64_t arena = 0, wsz = 0;
+  exp_elems_ = 0;
+  total_items_ = total_red_ = total_pack_ctas_ = total_exp_ctas_ = 0;
+  mma_count_ = 0;
+  auto add_pack = [&](const void* src, Idx2 r, Idx2 k, int rows, int K, int ks, int mask_index, int64_t& off,
+                      int32_t& rc, int64_t& exp) {
+    rc = std::max(1, (rows + 7) / 8);
+    off = arena;
+    arena += (int64_t)ks * rc * S * 256;
+    exp = exp_elems_;
+    exp_elems_ += rc * 8;
+    OzPackJob J{};
+    J.src = src;
+    J.r = r;
+    J.k = k;
+    J.rows = rows;
+    J.K = K;
+    J.ks = ks;
+    J.rc = rc;
+    J.mask_index = mask_index;
+    J.dst = off;
+    J.exp = exp;
+    J.units = (int64_t)ks * rc * 16;
+    J.echunks = (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
+    pbegin.push_back(total_pack_ctas_);
+    total_pack_ctas_ += (J.units + PACK_UNITS - 1) / PACK_UNITS;
+    ebegin.push_back(total_exp_ctas_);
+    total_exp_ctas_ += std::max<int64_t>(1, (J.echunks + 255) / 256);
+    jobs.push_back(J);
+  };
+  for (size_t i = 0; i < host.size(); ++i) {
+    GemmProblem& p = host[i];
+    OzProb& t = tp[i];
+    t.mt = (p.M + TM - 1) / TM;
+    t.nt = (p.N + TN - 1) / TN;
+    t.ks = std::max(1, (p.K + TKB - 1) / TKB);
+    t.ksplit = (int32_t)std::max<int64_t>(1, (t.ks + kOzSplitStages - 1) / kOzSplitStages);
+    t.kst = (t.ks + t.ksplit - 1) / t.ksplit;
+    t.ksplit = (t.ks + t.kst - 1) / t.kst;
+    const bool sym = (p.flags & kGemmSym) != 0;
+    if (p.M == 0 || p.N == 0) t.tiles = 0;
+    else t.tiles = sym ? sym_tiles_before(t.mt, t.nt) : (int64_t)t.mt * t.nt;
+    const int mi = (p.flags & kGemmMasked) ? p.mask_index : -1;
+    add_pack(p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp);
+    if (sym) {
+      t.b_pack = t.a_pack;
+      t.b_rc = t.a_rc;
+      t.b_exp = t.a_exp;
+    } else {
+      add_pack(p.B, p.b_r, p.b_k, p.N, p.K, t.ks, mi, t.b_pack, t.b_rc, t.b_exp);
+    }
+    t.ws_off = 0;
+    if (t.ksplit > 1 && t.tiles > 0) {
+      t.ws_off = wsz;
+      wsz += t.tiles * t.ksplit * (int64_t)(TM * TN);
+      rbegin.push_back(total_red_);
+      rprob.push_back((int32_t)i);
+      total_red_ += t.tiles;
+    }
+    begin[i] = total_items_;
+    total_items_ += t.tiles * t.ksplit;
+    mma_count_ += (double)t.tiles * t.ks * (S * (S + 1) / 2);
+  }
+  npack_ = (int)jobs.size();
+  nred_ = (int)rbegin.size();
+  SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemmProblem)));
+  SH_CUDA_CHECK(cudaMalloc(&d_tp_, tp.size() * sizeof(OzProb)));
+  SH_CUDA_CHECK(cudaMalloc(&d_begin_, begin.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_pack_, jobs.size() * sizeof(OzPackJob)));
+  SH_CUDA_CHECK(cudaMalloc(&d_pbegin_, pbegin.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_ebegin_, ebegin.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(cudaMalloc(&arena_, std::max<int64_t>(arena, 256)));
+  SH_CUDA_CHECK(cudaMalloc(&exps_, std::max<int64_t>(exp_elems_, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_tp_, tp.data(), tp.size() * sizeof(OzProb), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_pack_, jobs.data(), jobs.size() * sizeof(OzPackJob), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_pbegin_, pbegin.data(), pbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  SH_CUDA_CHECK(cudaMemcpy(d_ebegin_, ebegin.data(), ebegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (nred_ > 0) {
+    SH_CUDA_CHECK(cudaMalloc(&ws_, wsz * sizeof(double)));
+    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMalloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rbegin.data(), rbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_rprob_, rprob.data(), rprob.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
+  if (total_items_ == 0) return SHAMPOO_OK;
+  SH_CUDA_CHECK(cudaMemsetAsync(exps_, 0x80, exp_elems_ * sizeof(int32_t), s));  // very negative
+  k_oz_rowexp<T><<<(unsigned)total_exp_ctas_, 256, 0, s>>>(d_pack_, d_ebegin_, npack_, mask, exps_);
+  SH_LAUNCH_CHECK();
+  k_oz_pack<T, S><<<(unsigned)total_pack_ctas_, PACK_UNITS, 0, s>>>(d_pack_, d_pbegin_, npack_, mask, exps_, arena_);
+  SH_LAUNCH_CHECK();
+  k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_,
+                                                                              (int)host.size(), mask, arena_, exps_, ws_);
+  SH_LAUNCH_CHECK();
+  if (total_red_ > 0) {
+    k_oz_reduce<T><<<(unsigned)total_red_, 256, 0, s>>>(d_prob_, d_tp_, d_rbegin_, d_rprob_, nred_, mask, ws_);
+    SH_LAUNCH_CHECK();
+  }
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+double OzakiGemmBatch<T>::flops() const {
+  double f = 0;
+  for (const auto& p : host) f += 2.0 * p.M * (double)p.N * p.K;
+  return f;
+}
+
+template <typename T>
+double OzakiGemmBatch<T>::int8_ops() const {
+  return mma_count_ * 2.0 * TM * TN * TKB;
+}
+
+template class OzakiGemmBatch<float>;
+template class OzakiGemmBatch<double>;
+
+}  // namespace shampoo
+
+// ---------------------------------------------------------------- C ABI utility
+
+extern "C" int shampoo_tc_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                               int32_t symmetric, double alpha, double beta, int32_t dtype, void* stream) {
+  using namespace shampoo;
+  if (M < 0 || N < 0 || K < 0 || (symmetric && (A != B || M != N)) ||
+      (dtype != SHAMPOO_DTYPE_F32 && dtype != SHAMPOO_DTYPE_F64)) {
+    set_error("tc_gemm: invalid arguments");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  GemmProblem p = make_gemm(false, true, M, N, K, A, K, B, K, C, N, alpha, beta);
+  if (symmetric) p.flags |= kGemmSym;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc;
+  if (dtype == SHAMPOO_DTYPE_F32) {
+    OzakiGemmBatch<float> b;
+    b.add(p);
+    if ((rc = b.upload()) || (rc = b.launch(s))) return rc;
+    SH_CUDA_CHECK(cudaStreamSynchronize(s));
+  } else {
+    OzakiGemmBatch<double> b;
+    b.add(p);
+    if ((rc = b.upload()) || (rc = b.launch(s))) return rc;
+    SH_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  return SHAMPOO_OK;
+}

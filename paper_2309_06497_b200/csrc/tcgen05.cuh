@@ -1,0 +1,100 @@
+// Grouped GEMM on the 5th-generation tensor cores (sm_100a tcgen05.mma kind::i8) with
+// exact integer accumulation: Ozaki-style operand splitting.
+//
+// Why integers: Shampoo's factors feed an inverse 4th/6th root whose small
+// eigenvalues amplify any bias in the statistics.  fp32 tensor-core accumulation
+// (3xTF32 / bf16x3) rounds toward zero at every MMA step; over K = 4096 that is a
+// coherent ~3e-5 relative bias -- measured here: 4e-5 factor error and 1.4e-2
+// direction error against the reference at eps = 1e-6 on ResNet-50 blocks.
+// int8 x int8 products summed in int32 are exact, so the only error left is the
+// operand truncation, which is controlled by the number of slices.
+//
+// Scheme (per operand row r, e_r = frexp exponent of max_k |x_rk|):
+//   x_rk = 2^e_r * sum_{s=0}^{S-1} q_rks 2^(-7(s+1)) + O(2^(e_r - 7S)),  q in [-127, 127]
+//   C_ij = 2^(e_i + f_j) * sum_{d=0}^{S-1} 2^(-7(d+2)) * acc_d[i][j],
+//   acc_d = sum over slice pairs (s, t), s + t = d, of the exact int32 dot products.
+// Pairs with s + t >= S are dropped (below the truncation error).  S = 8 for
+// precision "double" (operand truncation 2^-56 of the row maximum: FP64 class),
+// S = 5 for "single" (2^-35).  Used for the factor statistics (precond.py:161-165,
+// 232-242) and the mode products (precond.py:168-174) of both precisions.
+//
+// Pipeline per launch (one launch set covers every block of a phase):
+//   k_oz_rowexp  per-row exponents (atomicMax of frexp exponents);
+//   k_oz_pack    operands -> int8 slice planes in the canonical no-swizzle K-major UMMA
+//                layout, [stage][8-row core][slice][2 K cores][8 rows][16 B], so one
+//                cp.async.bulk moves all slices of a tile's stage;
+//   k_oz_gemm    one CTA per (problem, 128x64 tile, K split): warp 0 issues the bulk
+//                copies (mbarrier complete_tx), warp 1 owns TMEM and issues
+//                tcgen05.mma (one elected thread; S(S+1)/2 MMAs per 32-wide k step, one
+//                TMEM accumulator per slice diagonal d), warps 2-5 drain TMEM with
+//                tcgen05.ld and combine the diagonals in FP64 (alpha, beta*C, SYRK
+//                mirror, split-K partials);
+//   k_oz_reduce  split-K partials summed in FP64 in a fixed order (deterministic).
+#pragma once
+
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace shampoo {
+
+struct OzProb {
+  int32_t mt, nt;       // 128-row tiles along M, 64-row tiles along N
+  int32_t ks;           // 32-wide K stages
+  int32_t ksplit;       // K splits (exact int32 accumulation bound)
+  int32_t kst;          // stages per split
+  int32_t pad;
+  int64_t tiles;        // output tiles (SYM: tiles on or below the diagonal)
+  int64_t a_pack, b_pack;   // byte offsets of the packed operands
+  int32_t a_rc, b_rc;       // 8-row cores per stage of each operand (rows padded to 128)
+  int64_t a_exp, b_exp;     // row-exponent offsets (int32 units)
+  int64_t ws_off;           // split-K partials (doubles)
+};
+
+struct OzPackJob {
+  const void* src;
+  Idx2 r, k;
+  int32_t rows, K;
+  int32_t ks, rc;        // stages, 8-row cores (padded rows / 8)
+  int32_t mask_index;    // -1: unmasked
+  int32_t pad;
+  int64_t dst;           // byte offset of the packed planes
+  int64_t exp;           // row-exponent offset
+  int64_t units;         // pack threads: rc * 8 * ks * 2 (row, stage, K core)
+  int64_t echunks;       // rowexp threads: rows * ceil(K / 64)
+};
+
+template <typename T>
+class OzakiGemmBatch {
+ public:
+  static constexpr int S = sizeof(T) == 8 ? 8 : 5;  // slices per operand
+  std::vector<GemmProblem> host;
+  OzakiGemmBatch() = default;
+  OzakiGemmBatch(const OzakiGemmBatch&) = delete;
+  OzakiGemmBatch& operator=(const OzakiGemmBatch&) = delete;
+  ~OzakiGemmBatch();
+  void add(const GemmProblem& p) { host.push_back(p); }
+  bool empty() const { return host.empty(); }
+  int upload();
+  int launch(cudaStream_t s, const int32_t* mask = nullptr) const;
+  double flops() const;      // algorithmic 2*M*N*K (SYM counted as full)
+  double int8_ops() const;   // executed tensor-core int8 ops (2 * 128 * 64 * 32 per MMA)
+
+ private:
+  GemmProblem* d_prob_ = nullptr;
+  OzProb* d_tp_ = nullptr;
+  int64_t* d_begin_ = nullptr;     // item prefix per problem
+  OzPackJob* d_pack_ = nullptr;
+  int64_t* d_pbegin_ = nullptr;    // pack CTA prefix per job
+  int64_t* d_ebegin_ = nullptr;    // rowexp CTA prefix per job
+  int64_t* d_rbegin_ = nullptr;    // reduce tile prefix
+  int32_t* d_rprob_ = nullptr;
+  int8_t* arena_ = nullptr;        // packed slice planes
+  int32_t* exps_ = nullptr;        // row exponents
+  double* ws_ = nullptr;           // split-K partial tiles
+  int64_t total_items_ = 0, total_pack_ctas_ = 0, total_exp_ctas_ = 0, total_red_ = 0, exp_elems_ = 0;
+  int npack_ = 0, nred_ = 0;
+  double mma_count_ = 0;
+};
+
+}  // namespace shampoo

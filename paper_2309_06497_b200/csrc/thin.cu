@@ -1,0 +1,206 @@
+// Thin problems of the grouped GEMM phases (see thin.cuh): HBM-bound CUDA-core kernels with
+// exact products and FP64 accumulation in a fixed order (deterministic).
+#include <algorithm>
+
+#include "thin.cuh"
+
+namespace shampoo {
+
+namespace {
+
+constexpr int KRED_CHUNK = 4096;  // k per CTA of the small-M/N reduction
+constexpr int TMAX = 8;           // M, N <= 8 for the reduction kernel
+
+__device__ __forceinline__ int64_t ev(const Idx2& x, int64_t v) {
+  if (x.div == 0x7fffffff) return v * x.lo;
+  return (v / x.div) * x.hi + (v % x.div) * x.lo;
+}
+
+__device__ __forceinline__ int find64(const int64_t* __restrict__ begin, int n, int64_t x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ void thin_store(const GemmProblem& P, int i, int j, double acc) {
+  T* __restrict__ C = static_cast<T*>(P.C);
+  const int64_t at = ev(P.c_r, i) + ev(P.c_c, j);
+  double v = P.alpha * acc;
+  if (P.flags & kGemmReadC) v = fma(P.beta, (double)C[at], v);
+  C[at] = (T)v;
+}
+
+// Small K: one thread per output element.  SYM problems are computed on the full square: the
+// (i,j) and (j,i) sums see the same products in the same order, so C stays exactly symmetric
+// with fully coalesced stores (no mirror writes).
+template <typename T>
+__global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict__ probs,
+                                                   const int64_t* __restrict__ begin, int nprob,
+                                                   const int32_t* __restrict__ mask) {
+  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = find64(begin, nprob, item);
+  const GemmProblem& P = probs[p];
+  const int64_t l = item - begin[p];
+  if (l >= (int64_t)P.M * P.N) return;
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const int i = (int)(l / P.N), j = (int)(l % P.N);
+  const T* __restrict__ A = static_cast<const T*>(P.A);
+  const T* __restrict__ B = static_cast<const T*>(P.B);
+  const int64_t ai = ev(P.a_r, i), bj = ev(P.b_r, j);
+  double acc = 0.0;
+  for (int k = 0; k < P.K; ++k) acc = fma((double)A[ai + ev(P.a_k, k)], (double)B[bj + ev(P.b_k, k)], acc);
+  thin_store<T>(P, i, j, acc);
+}
+
+// Small M and N (<= 8), any K: CTA per (problem, 4096-wide k chunk) -> FP64 partials.
+template <typename T>
+__global__ void __launch_bounds__(256) k_thin_kred(const GemmProblem* __restrict__ probs,
+                                                   const int64_t* __restrict__ begin, int nprob,
+                                                   const int32_t* __restrict__ mask, const int64_t* __restrict__ woff,
+                                                   double* __restrict__ ws) {
+  __shared__ double red[TMAX * TMAX][8];
+  const int p = find64(begin, nprob, blockIdx.x);
+  const GemmProblem& P = probs[p];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const int chunk = (int)(blockIdx.x - begin[p]);
+  const T* __restrict__ A = static_cast<const T*>(P.A);
+  const T* __restrict__ B = static_cast<const T*>(P.B);
+  double acc[TMAX][TMAX];
+#pragma unroll
+  for (int i = 0; i < TMAX; ++i)
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j) acc[i][j] = 0.0;
+  const int k0 = chunk * KRED_CHUNK, k1 = min(P.K, k0 + KRED_CHUNK);
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    double a[TMAX], b[TMAX];
+    const int64_t ak = ev(P.a_k, k), bk = ev(P.b_k, k);
+#pragma unroll
+    for (int i = 0; i < TMAX; ++i) {
+      a[i] = i < P.M ? (double)A[ev(P.a_r, i) + ak] : 0.0;
+      b[i] = i < P.N ? (double)B[ev(P.b_r, i) + bk] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < TMAX; ++i)
+#pragma unroll
+      for (int j = 0; j < TMAX; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+  }
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < TMAX; ++i)
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j) {
+      const double v = warp_sum(acc[i][j]);
+      if (ln == 0) red[i * TMAX + j][w] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < TMAX * TMAX) {
+    double v = 0.0;
+    for (int q = 0; q < 8; ++q) v += red[threadIdx.x][q];
+    ws[woff[p] + (int64_t)chunk * TMAX * TMAX + threadIdx.x] = v;
+  }
+}
+
+template <typename T>
+__global__ void k_thin_kred_final(const GemmProblem* __restrict__ probs, int nprob, const int32_t* __restrict__ mask,
+                                  const int64_t* __restrict__ woff, const int32_t* __restrict__ nchunks,
+                                  const double* __restrict__ ws) {
+  const int p = blockIdx.x;
+  const GemmProblem& P = probs[p];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const int e = threadIdx.x;
+  const int i = e / TMAX, j = e % TMAX;
+  if (i >= P.M || j >= P.N) return;
+  double acc = 0.0;
+  for (int c = 0; c < nchunks[p]; ++c) acc += ws[woff[p] + (int64_t)c * TMAX * TMAX + e];
+  thin_store<T>(P, i, j, acc);
+}
+
+}  // namespace
+
+bool ThinGemmBatch_accepts(const GemmProblem& p) { return p.K <= 32 || (p.M <= TMAX && p.N <= TMAX); }
+
+template <typename T>
+ThinGemmBatch<T>::~ThinGemmBatch() {
+  cudaFree(d_out_);
+  cudaFree(d_obegin_);
+  cudaFree(d_red_);
+  cudaFree(d_rbegin_);
+  cudaFree(d_woff_);
+  cudaFree(d_nch_);
+  cudaFree(ws_);
+}
+
+template <typename T>
+int ThinGemmBatch<T>::upload() {
+  std::vector<GemmProblem> outp, redp;
+  for (const auto& p : host) (p.K <= 32 ? outp : redp).push_back(p);
+  std::vector<int64_t> ob, rb, wo;
+  std::vector<int32_t> nch;
+  n_out_items_ = 0;
+  for (const auto& p : outp) {
+    ob.push_back(n_out_items_);
+    n_out_items_ += (int64_t)p.M * p.N;
+  }
+  n_red_ctas_ = 0;
+  int64_t wsz = 0;
+  for (const auto& p : redp) {
+    const int c = std::max(1, (p.K + KRED_CHUNK - 1) / KRED_CHUNK);
+    rb.push_back(n_red_ctas_);
+    wo.push_back(wsz);
+    nch.push_back(c);
+    n_red_ctas_ += c;
+    wsz += (int64_t)c * TMAX * TMAX;
+  }
+  n_out_ = (int)outp.size();
+  n_red_ = (int)redp.size();
+  if (n_out_) {
+    SH_CUDA_CHECK(cudaMalloc(&d_out_, outp.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(cudaMalloc(&d_obegin_, ob.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMemcpy(d_out_, outp.data(), outp.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_obegin_, ob.data(), ob.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  if (n_red_) {
+    SH_CUDA_CHECK(cudaMalloc(&d_red_, redp.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rb.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMalloc(&d_woff_, wo.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMalloc(&d_nch_, nch.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(cudaMalloc(&ws_, wsz * sizeof(double)));
+    SH_CUDA_CHECK(cudaMemcpy(d_red_, redp.data(), redp.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rb.data(), rb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_woff_, wo.data(), wo.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_nch_, nch.data(), nch.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int ThinGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
+  if (n_out_) {
+    k_thin_kout<T><<<(unsigned)((n_out_items_ + 255) / 256), 256, 0, s>>>(d_out_, d_obegin_, n_out_, mask);
+    SH_LAUNCH_CHECK();
+  }
+  if (n_red_) {
+    k_thin_kred<T><<<(unsigned)n_red_ctas_, 256, 0, s>>>(d_red_, d_rbegin_, n_red_, mask, d_woff_, ws_);
+    SH_LAUNCH_CHECK();
+    k_thin_kred_final<T><<<n_red_, TMAX * TMAX, 0, s>>>(d_red_, n_red_, mask, d_woff_, d_nch_, ws_);
+    SH_LAUNCH_CHECK();
+  }
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+double ThinGemmBatch<T>::flops() const {
+  double f = 0;
+  for (const auto& p : host) f += 2.0 * p.M * (double)p.N * p.K;
+  return f;
+}
+
+template class ThinGemmBatch<float>;
+template class ThinGemmBatch<double>;
+
+}  // namespace shampoo

@@ -1,0 +1,43 @@
+// Thin problems of the grouped GEMM phases: a dimension too small for a 128 x 64 tensor-core tile.
+//   K <= 32          (rank-1 factor updates of vector blocks, 3x3 / 7x7 kernel-mode products):
+//                    one thread per output element;
+//   M, N <= 8        (factors of 3x3 / 7x7 kernel modes, K up to 786k): CTA per 4096-wide k
+//                    chunk, FP64 partials reduced in chunk order.
+// Both are HBM-bound; products are exact and sums FP64 (deterministic), for float or double
+// storage.  SYM problems are computed on the full square (bitwise symmetric, coalesced).
+#pragma once
+
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace shampoo {
+
+bool ThinGemmBatch_accepts(const GemmProblem& p);
+
+template <typename T>
+class ThinGemmBatch {
+ public:
+  std::vector<GemmProblem> host;
+  ThinGemmBatch() = default;
+  ThinGemmBatch(const ThinGemmBatch&) = delete;
+  ThinGemmBatch& operator=(const ThinGemmBatch&) = delete;
+  ~ThinGemmBatch();
+  void add(const GemmProblem& p) { host.push_back(p); }
+  int upload();
+  int launch(cudaStream_t s, const int32_t* mask = nullptr) const;
+  double flops() const;
+
+ private:
+  GemmProblem* d_out_ = nullptr;
+  int64_t* d_obegin_ = nullptr;
+  GemmProblem* d_red_ = nullptr;
+  int64_t* d_rbegin_ = nullptr;
+  int64_t* d_woff_ = nullptr;
+  int32_t* d_nch_ = nullptr;
+  double* ws_ = nullptr;
+  int64_t n_out_items_ = 0, n_red_ctas_ = 0;
+  int n_out_ = 0, n_red_ = 0;
+};
+
+}  // namespace shampoo

@@ -352,3 +352,26 @@ def batched_root_inverse(mats: Sequence[torch.Tensor], root_p: int, *, exponent_
         int(root_p), float(exponent_multiplier), float(epsilon), 1 if solver == "newton" else 0,
         float(tolerance), st, it, s), "batched_root_inverse")
     return outs, [st[i] for i in range(len(mats))], [it[i] for i in range(len(mats))]
+
+
+def tc_gemm(a: torch.Tensor, b: torch.Tensor, c: Optional[torch.Tensor] = None, *, symmetric: bool = False,
+            alpha: float = 1.0, beta: float = 0.0) -> torch.Tensor:
+    """C = alpha A B^T + beta C on the tcgen05 int8 tensor cores (Ozaki split, exact int32 accumulation).
+
+    a (M x K), b (N x K), c (M x N): contiguous float32 or float64 CUDA tensors of one dtype.
+    symmetric requires a is b (SYRK: tiles on/below the diagonal computed and mirrored).
+    """
+    for t in (a, b):
+        if t.dtype not in (torch.float32, torch.float64) or t.device.type != "cuda" or t.dim() != 2 \
+                or not t.is_contiguous() or t.dtype != a.dtype:
+            raise ValueError("expected contiguous 2-D float32/float64 CUDA tensors of one dtype")
+    m, k = a.shape
+    n = b.shape[0]
+    if b.shape[1] != k:
+        raise ValueError("inner dimensions differ")
+    if c is None:
+        c = torch.zeros((m, n), dtype=a.dtype, device=a.device)
+    s = torch.cuda.current_stream(a.device).cuda_stream
+    N.check(N.lib().shampoo_tc_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, 1 if symmetric else 0,
+                                    float(alpha), float(beta), _dtype_code(a), s), "tc_gemm")
+    return c

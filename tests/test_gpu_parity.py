@@ -316,5 +316,6 @@ def test_resnet_shapes_vs_oracle(cuda_device, precision, eps):
         for b, st in enumerate(row):
             for k, f in enumerate(st.factors):
                 worst["factor"] = max(worst["factor"], rel(tree["params"][i][b][f"factor{k}"], f))
+    print(f"{precision}: worst factor rel {worst['factor']:.2e}, worst direction rel {worst['dir']:.2e}")
     assert worst["factor"] <= 1e-4, worst
     assert worst["dir"] <= 1e-3, worst
