@@ -30,6 +30,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct EngineBase {
   virtual ~EngineBase() = default;
+  virtual void inverses_changed() = 0;  // cached tensor-core packs of the inverse factors are stale
 };
 
 template <typename T>
@@ -42,6 +43,9 @@ struct Engine : EngineBase {
   ThinGemmBatch<T> stats_thin;
   ThinGemmBatch<T> prec_thin[kMaxOrder];
   GemvBatch<T> prec1;                  // order-1 blocks: P = X g
+  void inverses_changed() override {
+    for (auto& b : prec) b.invalidate_cached();
+  }
 };
 
 // Event pairs per phase; elapsed times are collected lazily in shampoo_timing_get.
@@ -616,6 +620,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   }
   SH_CUDA_CHECK(cudaMemcpyAsync(c->d_ready, c->ready_h.data(), c->ready_h.size() * sizeof(int32_t),
                                 cudaMemcpyHostToDevice, s));
+  c->engine->inverses_changed();
   if (refreshed) *refreshed = 1;
   return SHAMPOO_OK;
 }
@@ -742,6 +747,7 @@ void* shampoo_state_view(shampoo_ctx* c, int32_t block_id, const char* name, int
     const auto d = b.dims();
     for (int m = 0; m < mode; ++m) off += d[m] * d[m];
     if (numel) *numel = d[mode] * d[mode];
+    if (n == "inv_factor" && c->engine) c->engine->inverses_changed();  // the caller may write through it
     base = static_cast<char*>(n == "factor" ? c->FACT : c->INV);
     return base + off * c->esz;
   }
@@ -791,6 +797,7 @@ int shampoo_state_scalars_set(shampoo_ctx* c, int32_t block_id, int64_t step, in
   c->ready_h[l] = ready;
   SH_CUDA_CHECK(cudaMemcpy(c->d_ready, c->ready_h.data(), c->ready_h.size() * sizeof(int32_t),
                            cudaMemcpyHostToDevice));
+  if (c->engine) c->engine->inverses_changed();
   return SHAMPOO_OK;
 }
 

@@ -630,12 +630,14 @@ GemmProblem make_mode_product(const void* Mat, const void* X, void* Y, int64_t o
     p.C = Y;
     p.c_r = idx1(d);
     p.c_c = idx1(1);
+    p.flags |= kGemmConstB;
     return p;
   }
   // Y(i, c) with c = (o, n): sum_j Mat(i, j) X(c, j)
   p.M = (int32_t)d;
   p.N = (int32_t)(outer * inner);
   p.K = (int32_t)d;
+  p.flags |= kGemmConstA;
   p.A = Mat;
   p.a_r = idx1(d);
   p.a_k = idx1(1);

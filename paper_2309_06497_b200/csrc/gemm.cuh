@@ -23,6 +23,8 @@ enum GemmFlags : int32_t {
   kGemmSym = 1,    // C symmetric and A==B: compute tiles tm >= tn, mirror-write the rest
   kGemmReadC = 2,  // C = alpha*AB + beta*C (else beta ignored)
   kGemmMasked = 4, // skip unless mask[mask_index] != 0
+  kGemmConstA = 8,  // operand A changes rarely (an inverse factor): tensor-core packs are cached
+  kGemmConstB = 16, // same for operand B
 };
 
 struct Idx2 {

@@ -444,9 +444,11 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
   cudaFree(d_prob_);
   cudaFree(d_tp_);
   cudaFree(d_begin_);
-  cudaFree(d_pack_);
-  cudaFree(d_pbegin_);
-  cudaFree(d_ebegin_);
+  for (auto& ps : sets_) {
+    cudaFree(ps.d_jobs);
+    cudaFree(ps.d_pbegin);
+    cudaFree(ps.d_ebegin);
+  }
   cudaFree(d_rbegin_);
   cudaFree(d_rprob_);
   cudaFree(arena_);
@@ -464,20 +466,22 @@ int OzakiGemmBatch<T>::upload() {
     attr = true;
   }
   std::vector<OzProb> tp(host.size());
-  std::vector<int64_t> begin(host.size()), rbegin, pbegin, ebegin;
+  std::vector<int> a_set(host.size(), 0), b_set(host.size(), 0);
+  std::vector<int64_t> begin(host.size()), rbegin, pbegin[2], ebegin[2];
   std::vector<int32_t> rprob;
-  std::vector<OzPackJob> jobs;
-  int64_t arena = 0, wsz = 0;
-  exp_elems_ = 0;
-  total_items_ = total_red_ = total_pack_ctas_ = total_exp_ctas_ = 0;
+  std::vector<OzPackJob> jobs[2];
+  int64_t arena = 0, wsz = 0, exp_count[2] = {0, 0};
+  total_items_ = total_red_ = 0;
   mma_count_ = 0;
-  auto add_pack = [&](const void* src, Idx2 r, Idx2 k, int rows, int K, int ks, int mask_index, int64_t& off,
-                      int32_t& rc, int64_t& exp) {
+  for (auto& ps : sets_) ps = PackSet{};
+  // exponent offsets are relative to the set; fixed up once both sets are sized
+  auto add_pack = [&](int set, const void* src, Idx2 r, Idx2 k, int rows, int K, int ks, int mask_index,
+                      int64_t& off, int32_t& rc, int64_t& exp) {
     rc = std::max(1, (rows + 7) / 8);
     off = arena;
     arena += (int64_t)ks * rc * S * 256;
-    exp = exp_elems_;
-    exp_elems_ += rc * 8;
+    exp = exp_count[set];
+    exp_count[set] += rc * 8;
     OzPackJob J{};
     J.src = src;
     J.r = r;
@@ -491,11 +495,12 @@ int OzakiGemmBatch<T>::upload() {
     J.exp = exp;
     J.units = (int64_t)ks * rc * 16;
     J.echunks = (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
-    pbegin.push_back(total_pack_ctas_);
-    total_pack_ctas_ += (J.units + PACK_UNITS - 1) / PACK_UNITS;
-    ebegin.push_back(total_exp_ctas_);
-    total_exp_ctas_ += std::max<int64_t>(1, (J.echunks + 255) / 256);
-    jobs.push_back(J);
+    PackSet& ps = sets_[set];
+    pbegin[set].push_back(ps.pack_ctas);
+    ps.pack_ctas += (J.units + PACK_UNITS - 1) / PACK_UNITS;
+    ebegin[set].push_back(ps.exp_ctas);
+    ps.exp_ctas += std::max<int64_t>(1, (J.echunks + 255) / 256);
+    jobs[set].push_back(J);
   };
   for (size_t i = 0; i < host.size(); ++i) {
     GemmProblem& p = host[i];
@@ -510,13 +515,17 @@ int OzakiGemmBatch<T>::upload() {
     if (p.M == 0 || p.N == 0) t.tiles = 0;
     else t.tiles = sym ? sym_tiles_before(t.mt, t.nt) : (int64_t)t.mt * t.nt;
     const int mi = (p.flags & kGemmMasked) ? p.mask_index : -1;
-    add_pack(p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp);
+    const int aset = (p.flags & kGemmConstA) ? 1 : 0;
+    add_pack(aset, p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp);
+    a_set[i] = aset;
     if (sym) {
       t.b_pack = t.a_pack;
       t.b_rc = t.a_rc;
       t.b_exp = t.a_exp;
     } else {
-      add_pack(p.B, p.b_r, p.b_k, p.N, p.K, t.ks, mi, t.b_pack, t.b_rc, t.b_exp);
+      const int bset = (p.flags & kGemmConstB) ? 1 : 0;
+      add_pack(bset, p.B, p.b_r, p.b_k, p.N, p.K, t.ks, mi, t.b_pack, t.b_rc, t.b_exp);
+      b_set[i] = bset;
     }
     t.ws_off = 0;
     if (t.ksplit > 1 && t.tiles > 0) {
@@ -530,22 +539,39 @@ int OzakiGemmBatch<T>::upload() {
     total_items_ += t.tiles * t.ksplit;
     mma_count_ += (double)t.tiles * t.ks * (S * (S + 1) / 2);
   }
-  npack_ = (int)jobs.size();
+  // exponent layout: set 0 first, then set 1
+  sets_[0].exp_begin = 0;
+  sets_[0].exp_elems = exp_count[0];
+  sets_[1].exp_begin = exp_count[0];
+  sets_[1].exp_elems = exp_count[1];
+  for (size_t i = 0; i < host.size(); ++i) {
+    if (a_set[i] == 1) tp[i].a_exp += exp_count[0];
+    if (host[i].flags & kGemmSym) tp[i].b_exp = tp[i].a_exp;
+    else if (b_set[i] == 1) tp[i].b_exp += exp_count[0];
+  }
+  for (int q = 0; q < 2; ++q)
+    for (auto& J : jobs[q]) J.exp += sets_[q].exp_begin;
   nred_ = (int)rbegin.size();
   SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemmProblem)));
   SH_CUDA_CHECK(cudaMalloc(&d_tp_, tp.size() * sizeof(OzProb)));
   SH_CUDA_CHECK(cudaMalloc(&d_begin_, begin.size() * sizeof(int64_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_pack_, jobs.size() * sizeof(OzPackJob)));
-  SH_CUDA_CHECK(cudaMalloc(&d_pbegin_, pbegin.size() * sizeof(int64_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_ebegin_, ebegin.size() * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMalloc(&arena_, std::max<int64_t>(arena, 256)));
-  SH_CUDA_CHECK(cudaMalloc(&exps_, std::max<int64_t>(exp_elems_, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&exps_, std::max<int64_t>(exp_count[0] + exp_count[1], 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_tp_, tp.data(), tp.size() * sizeof(OzProb), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-  SH_CUDA_CHECK(cudaMemcpy(d_pack_, jobs.data(), jobs.size() * sizeof(OzPackJob), cudaMemcpyHostToDevice));
-  SH_CUDA_CHECK(cudaMemcpy(d_pbegin_, pbegin.data(), pbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-  SH_CUDA_CHECK(cudaMemcpy(d_ebegin_, ebegin.data(), ebegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  for (int q = 0; q < 2; ++q) {
+    PackSet& ps = sets_[q];
+    ps.njobs = (int)jobs[q].size();
+    if (!ps.njobs) continue;
+    SH_CUDA_CHECK(cudaMalloc(&ps.d_jobs, jobs[q].size() * sizeof(OzPackJob)));
+    SH_CUDA_CHECK(cudaMalloc(&ps.d_pbegin, pbegin[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMalloc(&ps.d_ebegin, ebegin[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_jobs, jobs[q].data(), jobs[q].size() * sizeof(OzPackJob), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_pbegin, pbegin[q].data(), pbegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_ebegin, ebegin[q].data(), ebegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  cached_valid_ = false;
   if (nred_ > 0) {
     SH_CUDA_CHECK(cudaMalloc(&ws_, wsz * sizeof(double)));
     SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
@@ -557,13 +583,25 @@ int OzakiGemmBatch<T>::upload() {
 }
 
 template <typename T>
+int OzakiGemmBatch<T>::launch_pack(const PackSet& ps, cudaStream_t s, const int32_t* mask) const {
+  if (!ps.njobs) return SHAMPOO_OK;
+  SH_CUDA_CHECK(cudaMemsetAsync(exps_ + ps.exp_begin, 0x80, ps.exp_elems * sizeof(int32_t), s));  // very negative
+  k_oz_rowexp<T><<<(unsigned)ps.exp_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_ebegin, ps.njobs, mask, exps_);
+  SH_LAUNCH_CHECK();
+  k_oz_pack<T, S><<<(unsigned)ps.pack_ctas, PACK_UNITS, 0, s>>>(ps.d_jobs, ps.d_pbegin, ps.njobs, mask, exps_, arena_);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
 int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   if (total_items_ == 0) return SHAMPOO_OK;
-  SH_CUDA_CHECK(cudaMemsetAsync(exps_, 0x80, exp_elems_ * sizeof(int32_t), s));  // very negative
-  k_oz_rowexp<T><<<(unsigned)total_exp_ctas_, 256, 0, s>>>(d_pack_, d_ebegin_, npack_, mask, exps_);
-  SH_LAUNCH_CHECK();
-  k_oz_pack<T, S><<<(unsigned)total_pack_ctas_, PACK_UNITS, 0, s>>>(d_pack_, d_pbegin_, npack_, mask, exps_, arena_);
-  SH_LAUNCH_CHECK();
+  int rc;
+  if (!cached_valid_) {
+    if ((rc = launch_pack(sets_[1], s, mask))) return rc;
+    cached_valid_ = true;
+  }
+  if ((rc = launch_pack(sets_[0], s, mask))) return rc;
   k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_,
                                                                               (int)host.size(), mask, arena_, exps_, ws_);
   SH_LAUNCH_CHECK();

@@ -21,14 +21,16 @@
 // Pipeline per launch (one launch set covers every block of a phase):
 //   k_oz_rowexp  per-row exponents (atomicMax of frexp exponents);
 //   k_oz_pack    operands -> int8 slice planes in the canonical no-swizzle K-major UMMA
-//                layout, [stage][8-row core][slice][2 K cores][8 rows][16 B], so one
-//                cp.async.bulk moves all slices of a tile's stage;
+//                layout, [stage][slice][8-row core][2 K cores][8 rows][16 B]; a tile's
+//                row cores of one slice are one contiguous cp.async.bulk;
 //   k_oz_gemm    one CTA per (problem, 128x64 tile, K split): warp 0 issues the bulk
 //                copies (mbarrier complete_tx), warp 1 owns TMEM and issues
-//                tcgen05.mma (one elected thread; S(S+1)/2 MMAs per 32-wide k step, one
-//                TMEM accumulator per slice diagonal d), warps 2-5 drain TMEM with
-//                tcgen05.ld and combine the diagonals in FP64 (alpha, beta*C, SYRK
-//                mirror, split-K partials);
+//                tcgen05.mma (one elected thread): A slice sa against the B slices
+//                0..S-1-sa stacked along N, so output block sb lands in the TMEM
+//                accumulator of diagonal d = sa + sb (12 MMAs per 32-wide k step for
+//                S = 8); warps 2-5 drain TMEM with tcgen05.ld, combine the diagonals in
+//                FP64 and store through a shared-memory tile (coalesced; alpha, beta*C,
+//                SYRK mirror, split-K partials);
 //   k_oz_reduce  split-K partials summed in FP64 in a fixed order (deterministic).
 #pragma once
 
@@ -46,7 +48,7 @@ struct OzProb {
   int32_t pad;
   int64_t tiles;        // output tiles (SYM: tiles on or below the diagonal)
   int64_t a_pack, b_pack;   // byte offsets of the packed operands
-  int32_t a_rc, b_rc;       // 8-row cores per stage of each operand (rows padded to 128)
+  int32_t a_rc, b_rc;       // 8-row cores per stage and slice of each operand (rows padded to 8)
   int64_t a_exp, b_exp;     // row-exponent offsets (int32 units)
   int64_t ws_off;           // split-K partials (doubles)
 };
@@ -77,23 +79,33 @@ class OzakiGemmBatch {
   bool empty() const { return host.empty(); }
   int upload();
   int launch(cudaStream_t s, const int32_t* mask = nullptr) const;
+  // operands flagged kGemmConstA/B (inverse factors: they change once per refresh) are packed
+  // on the first launch after upload() or invalidate_cached() only
+  void invalidate_cached() { cached_valid_ = false; }
   double flops() const;      // algorithmic 2*M*N*K (SYM counted as full)
-  double int8_ops() const;   // executed tensor-core int8 ops (2 * 128 * 64 * 32 per MMA)
+  double int8_ops() const;   // executed tensor-core int8 ops
 
  private:
+  struct PackSet {           // operands packed together (row exponents + slice planes)
+    OzPackJob* d_jobs = nullptr;
+    int64_t* d_pbegin = nullptr;   // pack CTA prefix per job
+    int64_t* d_ebegin = nullptr;   // rowexp CTA prefix per job
+    int64_t exp_begin = 0, exp_elems = 0, pack_ctas = 0, exp_ctas = 0;
+    int njobs = 0;
+  };
+  int launch_pack(const PackSet& ps, cudaStream_t s, const int32_t* mask) const;
   GemmProblem* d_prob_ = nullptr;
   OzProb* d_tp_ = nullptr;
   int64_t* d_begin_ = nullptr;     // item prefix per problem
-  OzPackJob* d_pack_ = nullptr;
-  int64_t* d_pbegin_ = nullptr;    // pack CTA prefix per job
-  int64_t* d_ebegin_ = nullptr;    // rowexp CTA prefix per job
+  PackSet sets_[2];                // [0] every launch, [1] cached (const) operands
+  mutable bool cached_valid_ = false;
   int64_t* d_rbegin_ = nullptr;    // reduce tile prefix
   int32_t* d_rprob_ = nullptr;
   int8_t* arena_ = nullptr;        // packed slice planes
   int32_t* exps_ = nullptr;        // row exponents
   double* ws_ = nullptr;           // split-K partial tiles
-  int64_t total_items_ = 0, total_pack_ctas_ = 0, total_exp_ctas_ = 0, total_red_ = 0, exp_elems_ = 0;
-  int npack_ = 0, nred_ = 0;
+  int64_t total_items_ = 0, total_red_ = 0;
+  int nred_ = 0;
   double mma_count_ = 0;
 };
 

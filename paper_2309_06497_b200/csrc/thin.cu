@@ -10,6 +10,7 @@ namespace {
 
 constexpr int KRED_CHUNK = 4096;  // k per CTA of the small-M/N reduction
 constexpr int TMAX = 8;           // M, N <= 8 for the reduction kernel
+constexpr int KOUT_ITEMS = 2048;  // outputs per CTA of the small-K kernel
 
 __device__ __forceinline__ int64_t ev(const Idx2& x, int64_t v) {
   if (x.div == 0x7fffffff) return v * x.lo;
@@ -35,26 +36,34 @@ __device__ __forceinline__ void thin_store(const GemmProblem& P, int i, int j, d
   C[at] = (T)v;
 }
 
-// Small K: one thread per output element.  SYM problems are computed on the full square: the
-// (i,j) and (j,i) sums see the same products in the same order, so C stays exactly symmetric
-// with fully coalesced stores (no mirror writes).
+// Small K: one thread per output element; a CTA covers rows [r0, r0 + R) of one problem
+// (R * N ~ 2048 outputs).  SYM problems are computed on the full square: the (i,j) and (j,i)
+// sums see the same products in the same order, so C stays exactly symmetric with fully
+// coalesced stores (no mirror writes).
 template <typename T>
 __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict__ probs,
                                                    const int64_t* __restrict__ begin, int nprob,
                                                    const int32_t* __restrict__ mask) {
-  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int p = find64(begin, nprob, item);
+  const int p = find64(begin, nprob, blockIdx.x);
   const GemmProblem& P = probs[p];
-  const int64_t l = item - begin[p];
-  if (l >= (int64_t)P.M * P.N) return;
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
-  const int i = (int)(l / P.N), j = (int)(l % P.N);
+  const int R = max(1, KOUT_ITEMS / P.N);
+  const int r0 = (int)(blockIdx.x - begin[p]) * R;
+  const int rows = min(R, P.M - r0);
   const T* __restrict__ A = static_cast<const T*>(P.A);
   const T* __restrict__ B = static_cast<const T*>(P.B);
-  const int64_t ai = ev(P.a_r, i), bj = ev(P.b_r, j);
-  double acc = 0.0;
-  for (int k = 0; k < P.K; ++k) acc = fma((double)A[ai + ev(P.a_k, k)], (double)B[bj + ev(P.b_k, k)], acc);
-  thin_store<T>(P, i, j, acc);
+  T* __restrict__ C = static_cast<T*>(P.C);
+  const bool readc = (P.flags & kGemmReadC) != 0;
+  for (int e = threadIdx.x; e < rows * P.N; e += blockDim.x) {
+    const int i = r0 + e / P.N, j = e % P.N;
+    const int64_t ai = ev(P.a_r, i), bj = ev(P.b_r, j);
+    double acc = 0.0;
+    for (int k = 0; k < P.K; ++k) acc = fma((double)A[ai + ev(P.a_k, k)], (double)B[bj + ev(P.b_k, k)], acc);
+    const int64_t at = ev(P.c_r, i) + ev(P.c_c, j);
+    double v = P.alpha * acc;
+    if (readc) v = fma(P.beta, (double)C[at], v);
+    C[at] = (T)v;
+  }
 }
 
 // Small M and N (<= 8), any K: CTA per (problem, 4096-wide k chunk) -> FP64 partials.
@@ -141,10 +150,11 @@ int ThinGemmBatch<T>::upload() {
   for (const auto& p : host) (p.K <= 32 ? outp : redp).push_back(p);
   std::vector<int64_t> ob, rb, wo;
   std::vector<int32_t> nch;
-  n_out_items_ = 0;
+  n_out_items_ = 0;  // CTAs
   for (const auto& p : outp) {
     ob.push_back(n_out_items_);
-    n_out_items_ += (int64_t)p.M * p.N;
+    const int R = std::max(1, KOUT_ITEMS / std::max(p.N, 1));
+    n_out_items_ += (p.M + R - 1) / R;
   }
   n_red_ctas_ = 0;
   int64_t wsz = 0;
@@ -181,7 +191,7 @@ int ThinGemmBatch<T>::upload() {
 template <typename T>
 int ThinGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   if (n_out_) {
-    k_thin_kout<T><<<(unsigned)((n_out_items_ + 255) / 256), 256, 0, s>>>(d_out_, d_obegin_, n_out_, mask);
+    k_thin_kout<T><<<(unsigned)n_out_items_, 256, 0, s>>>(d_out_, d_obegin_, n_out_, mask);
     SH_LAUNCH_CHECK();
   }
   if (n_red_) {
