@@ -196,6 +196,10 @@ SHAMPOO_API int shampoo_timing_get(shampoo_ctx* ctx, double* ms, int64_t* counts
 /* algorithmic work of one plain step for the owned blocks: flops of the factor GEMMs,
  * flops of the preconditioner GEMMs, sum n^3 over owned factors (root-inverse work) */
 SHAMPOO_API int shampoo_work(shampoo_ctx* ctx, double* stats_flops, double* precond_flops, double* sum_n3);
+/* the tensor-core (tcgen05 int8, Ozaki) share of the two GEMM phases: executed int8 ops per step
+ * (2 * 128 * N * 32 per MMA instruction) and the algorithmic FP64 flops they carry */
+SHAMPOO_API int shampoo_work_tc(shampoo_ctx* ctx, double* stats_int8_ops, double* precond_int8_ops,
+                                double* stats_tc_flops, double* precond_tc_flops);
 /* number of kernel launches issued by this library since load (bench evidence) */
 SHAMPOO_API int64_t shampoo_launch_count(void);
 

@@ -93,6 +93,8 @@ SIGNATURES = {
     "shampoo_timing_enable": (C.c_int, [_P, _I32]),
     "shampoo_timing_get": (C.c_int, [_P, C.POINTER(C.c_double), _PI64]),
     "shampoo_work": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "shampoo_work_tc": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]),
     "shampoo_state_view": (_P, [_P, _I32, C.c_char_p, _I32, _PI64, _PI32]),
     "shampoo_state_scalars_get": (C.c_int, [_P, _I32, _PI64, _PI64, _PI32]),
     "shampoo_state_scalars_set": (C.c_int, [_P, _I32, _I64, _I64, _I32]),

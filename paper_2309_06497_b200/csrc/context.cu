@@ -13,6 +13,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -27,6 +28,8 @@ int64_t g_launches = 0;
 namespace {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+constexpr int kRootGroups = 2;  // measured: 2 -> 1234 ms, 4 -> 1221 ms per t=50 refresh (ResNet-50)
 
 struct EngineBase {
   virtual ~EngineBase() = default;
@@ -142,8 +145,12 @@ struct shampoo_ctx {
   int32_t* d_flag = nullptr;
   int32_t* h_flag = nullptr;
   std::unique_ptr<EngineBase> engine;
-  RootInverseBatch rinv;
-  std::vector<int32_t> job_block;   // root-inverse job -> owned local block
+  // root-inverse jobs in kRootGroups load-balanced groups solved concurrently on their own streams
+  // (host thread per group): one group's latency-bound sub-solves overlap another's DMMA rounds
+  RootInverseBatch rinv[kRootGroups];
+  std::vector<int32_t> job_block[kRootGroups];  // root-inverse job -> owned local block
+  cudaStream_t side[kRootGroups] = {};          // side[0] unused (group 0 runs on the caller's stream)
+  cudaEvent_t ev_fork = nullptr, ev_join[kRootGroups] = {};
   int64_t guard[4] = {0, 0, 0, 0};
   PhaseTimer timer;
 
@@ -159,6 +166,11 @@ struct shampoo_ctx {
     cudaFree(d_diag_blocks);
     cudaFree(d_ptrs);
     cudaFreeHost(h_flag);
+    for (int g = 1; g < kRootGroups; ++g) {
+      if (side[g]) cudaStreamDestroy(side[g]);
+      if (ev_join[g]) cudaEventDestroy(ev_join[g]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
   }
   template <typename T>
   Engine<T>& eng() { return *static_cast<Engine<T>*>(engine.get()); }
@@ -508,30 +520,50 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   SH_CUDA_CHECK(cudaMemcpy(c->d_cc, cc.data(), no * sizeof(int32_t), cudaMemcpyHostToDevice));
   rc = c->f32 ? build_engine<float>(c.get()) : build_engine<double>(c.get());
   if (rc) return rc;
-  // root-inverse jobs: every (owned shampoo block, mode)
-  std::vector<int32_t> jn, jp;
+  // root-inverse jobs: every (owned shampoo block, mode), split into two groups by LPT on n^3
+  struct JobDesc {
+    int32_t n, p, l;
+    int64_t off;
+  };
+  std::vector<JobDesc> all;
   for (size_t l = 0; l < no; ++l) {
     const BlockPlan& b = plan->blocks[c->owned[l]];
     if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
     const int p = cfg->exponent_override ? cfg->exponent_override : 2 * b.order;  // precond.py:217
-    for (int64_t d : b.dims()) {
-      jn.push_back((int32_t)d);
-      jp.push_back(p);
-      c->job_block.push_back((int32_t)l);
-    }
-  }
-  if ((rc = c->rinv.setup(jn, jp))) return rc;
-  size_t j = 0;
-  for (size_t l = 0; l < no; ++l) {
-    const BlockPlan& b = plan->blocks[c->owned[l]];
-    if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
     int64_t off = c->fac_off[l];
     for (int64_t d : b.dims()) {
-      char* f = static_cast<char*>(c->FACT) + off * c->esz;
-      char* x = static_cast<char*>(c->INV) + off * c->esz;
-      c->rinv.set_io((int)j++, f, c->f32, x, c->f32);
+      all.push_back({(int32_t)d, p, (int32_t)l, off});
       off += d * d;
     }
+  }
+  std::vector<size_t> order(all.size());
+  for (size_t q = 0; q < order.size(); ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return all[a].n > all[b].n; });
+  std::vector<JobDesc> grp[kRootGroups];
+  double load[kRootGroups] = {};
+  for (size_t q : order) {
+    const int g = (int)(std::min_element(load, load + kRootGroups) - load);
+    grp[g].push_back(all[q]);
+    load[g] += (double)all[q].n * all[q].n * all[q].n;
+  }
+  for (int g = 0; g < kRootGroups; ++g) {
+    std::vector<int32_t> jn, jp;
+    for (const auto& J : grp[g]) {
+      jn.push_back(J.n);
+      jp.push_back(J.p);
+      c->job_block[g].push_back(J.l);
+    }
+    if ((rc = c->rinv[g].setup(jn, jp))) return rc;
+    for (size_t q = 0; q < grp[g].size(); ++q) {
+      char* f = static_cast<char*>(c->FACT) + grp[g][q].off * c->esz;
+      char* x = static_cast<char*>(c->INV) + grp[g][q].off * c->esz;
+      c->rinv[g].set_io((int)q, f, c->f32, x, c->f32);
+    }
+  }
+  SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  for (int g = 1; g < kRootGroups; ++g) {
+    SH_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side[g], cudaStreamNonBlocking));
+    SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join[g], cudaEventDisableTiming));
   }
   SH_CUDA_CHECK(cudaDeviceSynchronize());
   *out = c.release();
@@ -605,14 +637,45 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   if (refreshed) *refreshed = 0;
   const shampoo_config& k = c->cfg;
   if ((double)t < k.start_preconditioning_step || t % k.precondition_frequency != 0) return SHAMPOO_OK;
-  if (c->rinv.jobs() == 0) return SHAMPOO_OK;
+  size_t njobs = 0;
+  for (const auto& r : c->rinv) njobs += r.jobs();
+  if (njobs == 0) return SHAMPOO_OK;
   const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
   PhaseScope scope(&c->timer, 1, s);
-  std::vector<int32_t> has_prev(c->rinv.jobs());
-  for (size_t j = 0; j < has_prev.size(); ++j) has_prev[j] = c->ready_h[c->job_block[j]];
-  int rc = c->rinv.run(1.0 / corr, has_prev, k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance, s,
-                       c->guard, nullptr, nullptr, /*allow_warm=*/true);
-  if (rc) return rc;
+  std::vector<int32_t> has_prev[kRootGroups];
+  for (int g = 0; g < kRootGroups; ++g) {
+    has_prev[g].resize(c->rinv[g].jobs());
+    for (size_t j = 0; j < has_prev[g].size(); ++j) has_prev[g][j] = c->ready_h[c->job_block[g][j]];
+  }
+  // group g > 0 on side stream g (after everything already queued on s), group 0 on s
+  SH_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
+  int64_t gstats[kRootGroups][4] = {};
+  int grc[kRootGroups] = {};
+  std::string gerr[kRootGroups];
+  auto solve = [&](int g, cudaStream_t st) {
+    if (c->rinv[g].jobs() == 0) return;
+    grc[g] = c->rinv[g].run(1.0 / corr, has_prev[g], k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance,
+                            st, gstats[g], nullptr, nullptr, /*allow_warm=*/true);
+    if (grc[g]) gerr[g] = shampoo_last_error();
+  };
+  std::vector<std::thread> threads;
+  for (int g = 1; g < kRootGroups; ++g) {
+    SH_CUDA_CHECK(cudaStreamWaitEvent(c->side[g], c->ev_fork, 0));
+    threads.emplace_back(solve, g, c->side[g]);
+  }
+  solve(0, s);
+  for (auto& th : threads) th.join();
+  for (int g = 1; g < kRootGroups; ++g) {
+    SH_CUDA_CHECK(cudaEventRecord(c->ev_join[g], c->side[g]));
+    SH_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_join[g], 0));
+  }
+  for (int g = 0; g < kRootGroups; ++g)
+    if (grc[g]) {
+      set_error(gerr[g]);
+      return grc[g];
+    }
+  for (int g = 0; g < kRootGroups; ++g)
+    for (int q = 0; q < 4; ++q) c->guard[q] += gstats[g][q];
   for (size_t l = 0; l < c->owned.size(); ++l) {
     if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_SHAMPOO) continue;
     c->ready_h[l] = 1;
@@ -706,7 +769,28 @@ int shampoo_work(shampoo_ctx* c, double* stats_flops, double* precond_flops, dou
     const BlockPlan& b = c->plan.blocks[c->owned[l]];
     if (b.kind == SHAMPOO_BLOCK_SHAMPOO && b.order == 1) *precond_flops += 2.0 * b.var_count * b.var_count;
   }
-  *sum_n3 = c->rinv.work_n3();
+  *sum_n3 = 0;
+  for (const auto& r : c->rinv) *sum_n3 += r.work_n3();
+  return SHAMPOO_OK;
+}
+
+int shampoo_work_tc(shampoo_ctx* c, double* stats_int8_ops, double* precond_int8_ops, double* stats_tc_flops,
+                    double* precond_tc_flops) {
+  double so = 0, po = 0, sf = 0, pf = 0;
+  auto acc = [&](auto& e) {
+    so = e.stats.int8_ops();
+    sf = e.stats.flops();
+    for (int m = 0; m < kMaxOrder; ++m) {
+      po += e.prec[m].int8_ops();
+      pf += e.prec[m].flops();
+    }
+  };
+  if (c->f32) acc(c->eng<float>());
+  else acc(c->eng<double>());
+  if (stats_int8_ops) *stats_int8_ops = so;
+  if (precond_int8_ops) *precond_int8_ops = po;
+  if (stats_tc_flops) *stats_tc_flops = sf;
+  if (precond_tc_flops) *precond_tc_flops = pf;
   return SHAMPOO_OK;
 }
 

@@ -1275,7 +1275,7 @@ struct EigProfile {
     for (auto& m : marks) cudaEventDestroy(m.second);
   }
 };
-EigProfile* g_prof = nullptr;
+thread_local EigProfile* g_prof = nullptr;
 void prof_mark(const char* n) {
   if (g_prof) g_prof->mark(n);
 }
@@ -1415,7 +1415,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
       const RootJob& J = host_[j];
       if (J.m == 0) continue;
       double *ws = ws_ + J.ws_off, *vs = vs_ + J.v_off, *ts = ts_ + J.ws_off;
-      auto add = [&](GemmBatch<double>& b, bool ta, const double* A, const double* B, double* Cm, bool sym) {
+      auto add = [&](OzakiGemmBatch<double>& b, bool ta, const double* A, const double* B, double* Cm, bool sym) {
         GemmProblem g = make_gemm(ta, false, J.n, J.n, J.n, A, J.np, B, J.np, Cm, J.np, 1.0, 0.0);
         g.flags |= kGemmMasked | (sym ? kGemmSym : 0);
         g.mask_index = (int32_t)j;
@@ -1590,10 +1590,10 @@ int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::ve
   // GEMM sets for cur = 0/1: X_nxt = X_cur T ; powers ; M_nxt = T^p M_cur
   int maxp = 1;
   for (const auto& J : host_) maxp = std::max(maxp, J.root_p);
-  GemmBatch<double> xstep[2], mstep[2];
-  std::vector<GemmBatch<double>*> pw;  // power chain, step q: P_q = P_{q-1} T
-  std::vector<std::unique_ptr<GemmBatch<double>>> powers(std::max(0, maxp - 1));
-  for (auto& p : powers) p.reset(new GemmBatch<double>());
+  OzakiGemmBatch<double> xstep[2], mstep[2];
+  // power chain, step q: P_q = P_{q-1} T
+  std::vector<std::unique_ptr<OzakiGemmBatch<double>>> powers(std::max(0, maxp - 1));
+  for (auto& p : powers) p.reset(new OzakiGemmBatch<double>());
   for (int j = 0; j < nj; ++j) {
     const int n = host_[j].n, p = host_[j].root_p;
     const int64_t tot = (int64_t)n * n;

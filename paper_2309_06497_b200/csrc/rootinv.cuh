@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "tcgen05.cuh"
 
 namespace shampoo {
 
@@ -91,14 +92,14 @@ class RootInverseBatch {
   int32_t* d_warm_ = nullptr;
   std::vector<int32_t> vec_valid_;  // V holds eigenvectors of the last successful solve
   int64_t x_elems_ = 0, sweeps_total_ = 0;
-  GemmBatch<double> rr_, warm1_, warm2_;
+  OzakiGemmBatch<double> rr_, warm1_, warm2_;  // big n^3 GEMMs on tcgen05 (Ozaki, FP64-class)
   // mixed-precision eigensolver (FP32 Jacobi phase + FP64 Newton-Schulz re-orthonormalisation)
   bool mixed_ = false;  // SHAMPOO_EIG_MIXED=1
   float* ws32_ = nullptr;
   float* vs32_ = nullptr;
   float* us32_ = nullptr;
   int32_t* d_mix_ = nullptr;
-  GemmBatch<double> g_wv_, g_s1_, g_v1_, g_s2_, g_v2_;
+  OzakiGemmBatch<double> g_wv_, g_s1_, g_v1_, g_s2_, g_v2_;
   int32_t* d_pair_begin_ = nullptr;
   int32_t* d_item_begin_ = nullptr;
   int32_t* d_elem_begin_ = nullptr;
@@ -110,7 +111,7 @@ class RootInverseBatch {
   std::vector<int64_t> n2_off_;
   bool has_big_ = false;
   // reconstruction X = Y Y^T for all jobs (into xs_)
-  GemmBatch<double> recon_;
+  OzakiGemmBatch<double> recon_;
   bool recon_ready_ = false;
 };
 

@@ -459,12 +459,9 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
 template <typename T>
 int OzakiGemmBatch<T>::upload() {
   if (host.empty()) return SHAMPOO_OK;
-  static bool attr = false;
-  if (!attr) {
-    SH_CUDA_CHECK(cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)OzCfg<S>::SMEM));
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)OzCfg<S>::SMEM);  // once, thread-safe
+  SH_CUDA_CHECK(attr);
   std::vector<OzProb> tp(host.size());
   std::vector<int> a_set(host.size(), 0), b_set(host.size(), 0);
   std::vector<int64_t> begin(host.size()), rbegin, pbegin[2], ebegin[2];
