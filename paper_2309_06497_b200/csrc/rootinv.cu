@@ -31,6 +31,7 @@ constexpr int LDS_ = NS + 1;      // padded smem leading dim
 constexpr int SLOT = 2 * NS * NS + NS + 2;  // U (64x64) + S (64x64) + D (64) + flag
 constexpr int ECH = 4096;         // elements per chunk for elementwise job kernels
 constexpr int MAX_SWEEPS = 40;
+
 constexpr double U64 = 1.1102230246251565e-16;
 
 __device__ __forceinline__ int circle_pos(int r, int i, int m) {
@@ -223,7 +224,7 @@ __device__ __forceinline__ float eig_rsqrt(float x) { return rsqrtf(x); }
 // row phase: thread -> one pair, 8 columns; column phase: thread -> one row, 8 pairs; all
 // updates of a thread are independent and fully unrolled (loads batched ahead of stores).
 template <typename T>
-__device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null) {
+__device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_only = false) {
   constexpr T UR = EigU<T>::u;
   __shared__ T pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
   __shared__ int pa[NS / 2], pb[NS / 2];
@@ -231,11 +232,15 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null) {
   const int tid = threadIdx.x;
   for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? T(1) : T(0);
   if (tid == 0) rot_any = 0;
-  for (int r = 0; r < NS - 1; ++r) {
+  // full sweep: all 2016 pairs (circle method, 63 rounds); cross-only: the 1024 pairs between the
+  // two 32-row blocks (32 rounds, pair (i, 32 + (i + r) mod 32))
+  const int nrounds = cross_only ? HB : NS - 1;
+  for (int r = 0; r < nrounds; ++r) {
     if (tid == 0) rot_round = 0;
     __syncthreads();
     if (tid < NS / 2) {
-      const int a = circle_pos(r, tid, NS), b = circle_pos(r, NS - 1 - tid, NS);
+      const int a = cross_only ? tid : circle_pos(r, tid, NS);
+      const int b = cross_only ? HB + (tid + r) % HB : circle_pos(r, NS - 1 - tid, NS);
       const T apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
       T thr = fmax(T(4) * UR * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
       if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
@@ -327,7 +332,9 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null) {
 __global__ void __launch_bounds__(256, 3) k_subsolve(const RootJob* __restrict__ jobs, RootState* st,
                                                   const int32_t* __restrict__ pbegin, int njobs,
                                                   double* __restrict__ ws, double* __restrict__ vs,
-                                                  double* __restrict__ us) {
+                                                  double* __restrict__ us, int cross_only) {
+  // cross_only: sub-solves of outer rounds r > 0 rotate only the pairs between the two 32-row
+  // blocks; intra-block pairs are eliminated in round 0 of every sweep, where every block takes part
   extern __shared__ double smem[];
   double* S = smem;
   double* U = smem + NS * LDS_;
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(256, 3) k_subsolve(const RootJob* __restrict__
   }
   // blocked jobs: one inner sweep per outer round (outer sweeps barely change)
   const int any = small ? cta_jacobi(S, U, ns, tol_abs, tol_null, MAX_SWEEPS, &sweeps)
-                        : cta_jacobi64_sweep<double>(S, U, tol_abs, tol_null);
+                        : cta_jacobi64_sweep<double>(S, U, tol_abs, tol_null, cross_only && st[j].round != 0);
   if (small) {
     double* V = vs + J.v_off;
     for (int e = threadIdx.x; e < ns * ns; e += blockDim.x) {
@@ -1403,6 +1410,8 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   {
     const char* env = std::getenv("SHAMPOO_EIG_MIXED");
     mixed_ = env ? std::atoi(env) != 0 : false;  // measured: no net gain with SIMT FP32 rounds
+    const char* cr = std::getenv("SHAMPOO_EIG_CROSS");
+    cross_only_ = cr ? std::atoi(cr) != 0 : true;
   }
   if (mixed_ && has_big_) {
     SH_CUDA_CHECK(cudaMalloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
@@ -1540,7 +1549,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
   // Jacobi rounds until every job is inactive
   for (int R = 0;; ++R) {
     k_subsolve<<<total_pairs_, 256, 2 * NS * LDS_ * sizeof(double), s>>>(d_jobs_, d_state_, d_pair_begin_, nj,
-                                                                          ws_, vs_, us_);
+                                                                          ws_, vs_, us_, cross_only_ ? 1 : 0);
     SH_LAUNCH_CHECK();
     if (!has_big_) break;
     if (total_items_ > 0) {

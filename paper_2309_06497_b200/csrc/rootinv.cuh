@@ -95,6 +95,7 @@ class RootInverseBatch {
   OzakiGemmBatch<double> rr_, warm1_, warm2_;  // big n^3 GEMMs on tcgen05 (Ozaki, FP64-class)
   // mixed-precision eigensolver (FP32 Jacobi phase + FP64 Newton-Schulz re-orthonormalisation)
   bool mixed_ = false;  // SHAMPOO_EIG_MIXED=1
+  bool cross_only_ = true;  // SHAMPOO_EIG_CROSS=0: full inner sweeps in every outer round
   float* ws32_ = nullptr;
   float* vs32_ = nullptr;
   float* us32_ = nullptr;
