@@ -220,9 +220,11 @@ template <> struct EigU<float> { static constexpr float u = 5.9604645e-8f, big =
 __device__ __forceinline__ double eig_rsqrt(double x) { return rsqrt(x); }
 __device__ __forceinline__ float eig_rsqrt(float x) { return rsqrtf(x); }
 
-// One inner cyclic-Jacobi sweep on a 64x64 sub-problem with 256 threads, laid out for ILP:
-// row phase: thread -> one pair, 8 columns; column phase: thread -> one row, 8 pairs; all
-// updates of a thread are independent and fully unrolled (loads batched ahead of stores).
+// One inner cyclic-Jacobi sweep on a 64x64 sub-problem with 256 threads.  Per inner round:
+// 32 threads compute the round's disjoint rotations (one sqrt, one division), then one fused
+// phase applies S <- J^T S J as independent 2x2 blocks (rows of pair i x columns of pair j:
+// L_i M L_j^T, thread -> 4 blocks) and U <- U J (thread -> one row, 8 pairs): two barriers per
+// round.  The pair's own 2x2 block gets the exact values of Golub & Van Loan sym.schur2.
 template <typename T>
 __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_only = false) {
   constexpr T UR = EigU<T>::u;
@@ -246,10 +248,11 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
       if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
       T c = 1, sn = 0, t = 0;
       if (fabs(apq) > thr) {
-        const T tau = (aqq - app) / (T(2) * apq);
-        const T at = fabs(tau);
-        const T den = at < EigU<T>::big ? at + sqrt(fma(at, at, T(1))) : T(2) * at;
-        t = copysign(T(1), tau) / den;
+        // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / e, written as e sign(d) / (|d| + |(d, e)|)
+        const T d = aqq - app, e = T(2) * apq;
+        T h = sqrt(fma(d, d, e * e));
+        if (!(h <= EigU<T>::big)) h = hypot(d, e);  // overflow guard for huge entries
+        t = e * copysign(T(1), d) / (fabs(d) + h);
         c = eig_rsqrt(fma(t, t, T(1)));
         sn = t * c;
         rot_round = 1;
@@ -265,60 +268,57 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
     }
     __syncthreads();
     if (!rot_round) continue;  // uniform: every thread read it after the barrier
-    {  // rows: S <- J^T S
-      const int q = tid >> 3, c0 = tid & 7;
-      const T sn = ps[q];
-      if (sn != T(0)) {
-        const T c = pc[q];
-        const int a = pa[q], b = pb[q];
-        T xa[8], xb[8];
+    // S <- J^T S J by 2x2 blocks (pair i rows, pair j columns)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          xa[k] = S[a * LDS_ + c0 + 8 * k];
-          xb[k] = S[b * LDS_ + c0 + 8 * k];
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          S[a * LDS_ + c0 + 8 * k] = c * xa[k] - sn * xb[k];
-          S[b * LDS_ + c0 + 8 * k] = sn * xa[k] + c * xb[k];
-        }
+    for (int k = 0; k < 4; ++k) {
+      const int blk = tid + 256 * k;
+      const int i = blk >> 5, j = blk & 31;
+      const T si = ps[i], sj = ps[j];
+      if (si == T(0) && sj == T(0)) continue;
+      const int ai = pa[i], bi = pb[i];
+      if (i == j) {
+        S[ai * LDS_ + ai] = papp[i] - pt[i] * papq[i];
+        S[bi * LDS_ + bi] = paqq[i] + pt[i] * papq[i];
+        S[ai * LDS_ + bi] = T(0);
+        S[bi * LDS_ + ai] = T(0);
+        continue;
       }
+      const int aj = pa[j], bj = pb[j];
+      T m00 = S[ai * LDS_ + aj], m01 = S[ai * LDS_ + bj], m10 = S[bi * LDS_ + aj], m11 = S[bi * LDS_ + bj];
+      if (sj != T(0)) {  // columns: M <- M L_j^T
+        const T cj = pc[j];
+        const T n00 = cj * m00 - sj * m01, n01 = sj * m00 + cj * m01;
+        const T n10 = cj * m10 - sj * m11, n11 = sj * m10 + cj * m11;
+        m00 = n00; m01 = n01; m10 = n10; m11 = n11;
+      }
+      if (si != T(0)) {  // rows: M <- L_i M
+        const T ci = pc[i];
+        const T o00 = ci * m00 - si * m10, o10 = si * m00 + ci * m10;
+        const T o01 = ci * m01 - si * m11, o11 = si * m01 + ci * m11;
+        m00 = o00; m10 = o10; m01 = o01; m11 = o11;
+      }
+      S[ai * LDS_ + aj] = m00;
+      S[ai * LDS_ + bj] = m01;
+      S[bi * LDS_ + aj] = m10;
+      S[bi * LDS_ + bj] = m11;
     }
-    __syncthreads();
-    {  // columns: S <- S J, U <- U J; exact 2x2 pair block (sym.schur2); two halves of 4 pairs
+    {  // U <- U J: thread -> row tid/4, pairs (tid & 3) + 4k
       const int row = tid >> 2, q0 = tid & 3;
+      T ua[8], ub[8];
 #pragma unroll
-      for (int hlf = 0; hlf < 2; ++hlf) {
-        T sa[4], sb[4], ua[4], ub[4];
+      for (int k = 0; k < 8; ++k) {
+        const int q = q0 + 4 * k;
+        ua[k] = U[row * LDS_ + pa[q]];
+        ub[k] = U[row * LDS_ + pb[q]];
+      }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int q = q0 + 4 * (k + 4 * hlf);
-          const int a = pa[q], b = pb[q];
-          sa[k] = S[row * LDS_ + a];
-          sb[k] = S[row * LDS_ + b];
-          ua[k] = U[row * LDS_ + a];
-          ub[k] = U[row * LDS_ + b];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int q = q0 + 4 * (k + 4 * hlf);
-          const T sn = ps[q];
-          if (sn == T(0)) continue;
-          const T c = pc[q];
-          const int a = pa[q], b = pb[q];
-          U[row * LDS_ + a] = c * ua[k] - sn * ub[k];
-          U[row * LDS_ + b] = sn * ua[k] + c * ub[k];
-          if (row == a) {
-            S[a * LDS_ + a] = papp[q] - pt[q] * papq[q];
-            S[a * LDS_ + b] = T(0);
-          } else if (row == b) {
-            S[b * LDS_ + b] = paqq[q] + pt[q] * papq[q];
-            S[b * LDS_ + a] = T(0);
-          } else {
-            S[row * LDS_ + a] = c * sa[k] - sn * sb[k];
-            S[row * LDS_ + b] = sn * sa[k] + c * sb[k];
-          }
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int q = q0 + 4 * k;
+        const T sn = ps[q];
+        if (sn == T(0)) continue;
+        const T c = pc[q];
+        U[row * LDS_ + pa[q]] = c * ua[k] - sn * ub[k];
+        U[row * LDS_ + pb[q]] = sn * ua[k] + c * ub[k];
       }
     }
     if (tid == 0) rot_any = 1;
