@@ -9,7 +9,8 @@ namespace shampoo {
 
 namespace {
 
-constexpr int TM = 128, TN = 64, TKB = 32;    // CTA tile; 32 int8 (= one MMA K) per pipeline stage
+constexpr int TM = 128, TN = 32, TKB = 32;    // CTA tile; 32 int8 (= one MMA K) per pipeline stage
+constexpr int SL_PER_MMA = 256 / TN;          // B slices stacked along N in one MMA (N <= 256)
 constexpr int GEMM_THREADS = 192;             // warp 0 bulk copies, warp 1 MMA, warps 2-5 epilogue
 constexpr int64_t kOzSplitStages = 256;       // 8192 k per split: int32 sums stay exact (< 2^31)
 constexpr int PACK_UNITS = 256;               // pack threads per CTA (one unit = 16 k of one row)
@@ -21,9 +22,10 @@ struct OzCfg {
   static constexpr int A_BYTES = (TM / 8) * S * 256;     // one stage of a 128-row tile, all slices
   static constexpr int B_BYTES = (TN / 8) * S * 256;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE < 6 ? (200 * 1024) / STAGE : 6;
+  // two CTAs per SM (one's FP64 epilogue overlaps the other's MMAs): <= ~100 KB of stages each
+  static constexpr int STAGES = (100 * 1024) / STAGE < 6 ? (100 * 1024) / STAGE : 6;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
-  static constexpr uint32_t TMEM_COLS = 512;             // S * TN <= 512
+  static constexpr uint32_t TMEM_COLS = 256;             // S * TN <= 256: two CTAs share the 512 columns
   // kind::i8: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1), K-major, M = 128; N (bits 17-22)
   // is set per instruction
   static constexpr uint32_t IDESC_BASE = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TM >> 4) << 24);
@@ -111,17 +113,19 @@ __device__ __forceinline__ int find64(const int64_t* __restrict__ begin, int n, 
   return lo;
 }
 
-// SYM problems: 128 x 64 tiles that touch the lower triangle, tn <= 2 tm + 1, row-major order.
+// SYM problems: TM x TN tiles that touch the lower triangle, tn < (TM / TN)(tm + 1), row-major order.
 __host__ __device__ __forceinline__ int64_t sym_tiles_before(int tm, int nt) {
+  constexpr int R = TM / TN;
   int64_t c = 0;
-  for (int t = 0; t < tm; ++t) c += (2 * t + 2 < nt) ? 2 * t + 2 : nt;
+  for (int t = 0; t < tm; ++t) c += (R * (t + 1) < nt) ? R * (t + 1) : nt;
   return c;
 }
 __device__ __forceinline__ void sym_decode(int64_t l, int nt, int& tm, int& tn) {
+  constexpr int R = TM / TN;
   int t = 0;
   int64_t c = 0;
   for (;; ++t) {
-    const int w = (2 * t + 2 < nt) ? 2 * t + 2 : nt;
+    const int w = (R * (t + 1) < nt) ? R * (t + 1) : nt;
     if (l < c + w) break;
     c += w;
   }
@@ -223,7 +227,7 @@ __device__ __forceinline__ double pow2i(int e) {
 constexpr int LDE = TN + 1;  // staged epilogue tile leading dim (doubles)
 
 template <typename T, int S>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_oz_gemm(const GemmProblem* __restrict__ probs,
+__global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* __restrict__ probs,
                                                             const OzProb* __restrict__ tps,
                                                             const int64_t* __restrict__ begin, int nprob,
                                                             const int32_t* __restrict__ mask,
@@ -299,8 +303,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_oz_gemm(const GemmProblem* 
   } else if (warp == 1) {
     if (lane == 0) {
       // MMA issuer.  A slice sa times the B slices sb = 0 .. S-1-sa stacked along N (slice-major in
-      // smem): output column block sb lands at TMEM column (sa + sb) * 64 = accumulator of diagonal
-      // d = sa + sb.  N <= 256 per instruction.
+      // smem): output column block sb lands at TMEM column (sa + sb) * TN = accumulator of diagonal
+      // d = sa + sb.  N <= 256 per instruction (one MMA per A slice for TN = 32).
       for (int it = 0; it < nk; ++it) {
         const int st = it % Cfg::STAGES;
         mbar_wait(&full_bar[st], (uint32_t)(it / Cfg::STAGES) & 1u);
@@ -311,8 +315,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_oz_gemm(const GemmProblem* 
         for (int sa = 0; sa < S; ++sa) {
           const uint64_t ad = sdesc(sa_base + sa * (TM / 8) * 256, 128, 256);
 #pragma unroll
-          for (int sb0 = 0; sb0 < S - sa; sb0 += 4) {
-            const int nsl = min(4, S - sa - sb0);
+          for (int sb0 = 0; sb0 < S - sa; sb0 += SL_PER_MMA) {
+            const int nsl = min(SL_PER_MMA, S - sa - sb0);
             const uint64_t bd = sdesc(sb_base + sb0 * (TN / 8) * 256, 128, 256);
             const uint32_t idesc = Cfg::IDESC_BASE | ((uint32_t)(nsl * TN >> 3) << 17);
             tc_mma_i8(tmem + (uint32_t)((sa + sb0) * TN), ad, bd, idesc, (it > 0 || sa > 0) ? 1u : 0u);
@@ -342,22 +346,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_oz_gemm(const GemmProblem* 
     mbar_wait(&done_bar, 0);
     tc_fence_after();
     const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
+    // diagonals combined exactly in two int64 fixed-point halves (|acc_d| < 2^31, so each half
+    // stays below 2^53 and converts to double exactly): one rounding per output
+    constexpr int H = (S + 1) / 2;
     int32_t v[16];
     for (int c0 = 0; c0 < TN; c0 += 16) {
-      double acc[16];
+      long long hi[16], lo[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+      for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0;
       if (nk > 0) {
 #pragma unroll
-        for (int d = S - 1; d >= 0; --d) {  // smallest contributions first
+        for (int d = 0; d < S; ++d) {
           tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * TN + c0), v);
-          const double wd = pow2i(-7 * (d + 2));
 #pragma unroll
-          for (int q = 0; q < 16; ++q) acc[q] = fma((double)v[q], wd, acc[q]);
+          for (int q = 0; q < 16; ++q) {
+            if (d < H) hi[q] += (long long)v[q] << (7 * (H - 1 - d));
+            else lo[q] += (long long)v[q] << (7 * (S - 1 - d));
+          }
         }
       }
+      const double whi = pow2i(-7 * (H + 1)), wlo = pow2i(-7 * (S + 1));
 #pragma unroll
-      for (int q = 0; q < 16; ++q) tileS[rl * LDE + c0 + q] = acc[q] * rscale;
+      for (int q = 0; q < 16; ++q)
+        tileS[rl * LDE + c0 + q] = fma((double)hi[q], whi, (double)lo[q] * wlo) * rscale;
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
     const bool sym = (P.flags & kGemmSym) != 0;
