@@ -14,7 +14,8 @@ constexpr int SL_PER_MMA = 256 / TN;          // B slices stacked along N in one
 constexpr int GEMM_THREADS = 192;             // warp 0 bulk copies, warp 1 MMA, warps 2-5 epilogue
 constexpr int64_t kOzSplitStages = 256;       // 8192 k per split: int32 sums stay exact (< 2^31)
 constexpr int PACK_UNITS = 256;               // pack threads per CTA (one unit = 16 k of one row)
-constexpr int EXP_CHUNK = 64;                 // k per rowexp thread
+constexpr int EXP_CHUNK = 64;                 // k per rowexp thread (strided rows)
+constexpr int EXP_WARP_CHUNK = 2048;          // k per rowexp warp (contiguous rows)
 constexpr int kExpFloor = -1100;              // exponent of an all-zero row (ldexp -> 0)
 
 template <int S>
@@ -149,7 +150,11 @@ __device__ __forceinline__ void oz_store(const GemmProblem& P, int gi, int gj, d
   if (sym && gi != gj) C[evx(P.c_r, gj) + evx(P.c_c, gi)] = o;
 }
 
-// Row exponents: e_r = max_k frexp-exponent(x_rk) (|x_rk| < 2^e_r).
+// Row exponents: e_r = max_k frexp-exponent(x_rk) (|x_rk| < 2^e_r).  Rows contiguous along k:
+// a warp per (row, 2048-wide k chunk), lanes on consecutive k; otherwise a thread per
+// (k chunk, row) with consecutive threads on consecutive rows (coalesced for column access).
+__device__ __forceinline__ bool k_contig(const OzPackJob& J) { return J.k.div == 0x7fffffff && J.k.lo == 1; }
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__ jobs, const int64_t* __restrict__ ebegin,
                                                    int njobs, const int32_t* __restrict__ mask, int32_t* __restrict__ exps) {
@@ -157,14 +162,28 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
   const OzPackJob& J = jobs[j];
   if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
   const int64_t u = (int64_t)(blockIdx.x - ebegin[j]) * 256 + threadIdx.x;
-  if (u >= J.echunks) return;
-  const int nkc = (J.K + EXP_CHUNK - 1) / EXP_CHUNK;
-  const int row = (int)(u / nkc), k0 = (int)(u % nkc) * EXP_CHUNK;
   const T* __restrict__ src = static_cast<const T*>(J.src);
-  const int64_t rb = evx(J.r, row);
   double m = 0.0;
-  const int k1 = min(J.K, k0 + EXP_CHUNK);
-  for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)src[rb + evx(J.k, k)]));
+  int row;
+  if (k_contig(J)) {
+    const int64_t wu = u >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nkc = (J.K + EXP_WARP_CHUNK - 1) / EXP_WARP_CHUNK;
+    if (wu >= (int64_t)J.rows * nkc) return;  // whole warps exit together
+    row = (int)(wu / nkc);
+    const int k0 = (int)(wu % nkc) * EXP_WARP_CHUNK, k1 = min(J.K, k0 + EXP_WARP_CHUNK);
+    const T* rp = src + evx(J.r, row);
+    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs((double)rp[k]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane != 0) return;
+  } else {
+    if (u >= J.echunks) return;
+    row = (int)(u % J.rows);
+    const int k0 = (int)(u / J.rows) * EXP_CHUNK, k1 = min(J.K, k0 + EXP_CHUNK);
+    const int64_t rb = evx(J.r, row);
+    for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)src[rb + evx(J.k, k)]));
+  }
   if (m > 0.0) {
     int e;
     frexp(m, &e);
@@ -502,7 +521,9 @@ int OzakiGemmBatch<T>::upload() {
     J.dst = off;
     J.exp = exp;
     J.units = (int64_t)ks * rc * 16;
-    J.echunks = (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
+    J.echunks = (k.div == 0x7fffffff && k.lo == 1)
+                    ? (int64_t)rows * ((K + EXP_WARP_CHUNK - 1) / EXP_WARP_CHUNK) * 32  // threads (warps x 32)
+                    : (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
     PackSet& ps = sets_[set];
     pbegin[set].push_back(ps.pack_ctas);
     ps.pack_ctas += (J.units + PACK_UNITS - 1) / PACK_UNITS;

@@ -63,7 +63,7 @@ struct OzPackJob {
   int64_t dst;           // byte offset of the packed planes
   int64_t exp;           // row-exponent offset
   int64_t units;         // pack threads: rc * 8 * ks * 2 (row, stage, K core)
-  int64_t echunks;       // rowexp threads: rows * ceil(K / 64)
+  int64_t echunks;       // rowexp threads (contiguous rows: 32 per 2048-wide chunk; else 1 per 64)
 };
 
 template <typename T>

@@ -54,6 +54,21 @@ __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict
   const T* __restrict__ B = static_cast<const T*>(P.B);
   T* __restrict__ C = static_cast<T*>(P.C);
   const bool readc = (P.flags & kGemmReadC) != 0;
+  if (P.N >= 64) {  // wide rows: row loop outside, coalesced column loop inside (no divisions)
+    for (int i = r0; i < r0 + rows; ++i) {
+      const int64_t ai = ev(P.a_r, i), ci = ev(P.c_r, i);
+      for (int j = threadIdx.x; j < P.N; j += blockDim.x) {
+        const int64_t bj = ev(P.b_r, j);
+        double acc = 0.0;
+        for (int k = 0; k < P.K; ++k) acc = fma((double)A[ai + ev(P.a_k, k)], (double)B[bj + ev(P.b_k, k)], acc);
+        const int64_t at = ci + ev(P.c_c, j);
+        double v = P.alpha * acc;
+        if (readc) v = fma(P.beta, (double)C[at], v);
+        C[at] = (T)v;
+      }
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < rows * P.N; e += blockDim.x) {
     const int i = r0 + e / P.N, j = e % P.N;
     const int64_t ai = ev(P.a_r, i), bj = ev(P.b_r, j);
