@@ -220,29 +220,48 @@ template <> struct EigU<float> { static constexpr float u = 5.9604645e-8f, big =
 __device__ __forceinline__ double eig_rsqrt(double x) { return rsqrt(x); }
 __device__ __forceinline__ float eig_rsqrt(float x) { return rsqrtf(x); }
 
+// (c, s) of one rotation, loaded with one 16-byte (double) / 8-byte (float) shared access
+template <typename T> struct CS;
+template <> struct CS<double> { using type = double2; };
+template <> struct CS<float> { using type = float2; };
+
+// Pair q of inner round r: cross-only ordering (q, 32 + (q + r) mod 32), else the circle method.
+template <bool CROSS>
+__device__ __forceinline__ void pair_rows(int r, int q, int& a, int& b) {
+  if (CROSS) {
+    a = q;
+    b = HB + ((q + r) & (HB - 1));
+  } else {
+    a = circle_pos(r, q, NS);
+    b = circle_pos(r, NS - 1 - q, NS);
+  }
+}
+
 // One inner cyclic-Jacobi sweep on a 64x64 sub-problem with 256 threads.  Per inner round:
 // 32 threads compute the round's disjoint rotations (one sqrt, one division), then one fused
 // phase applies S <- J^T S J as independent 2x2 blocks (rows of pair i x columns of pair j:
 // L_i M L_j^T, thread -> 4 blocks) and U <- U J (thread -> one row, 8 pairs): two barriers per
-// round.  The pair's own 2x2 block gets the exact values of Golub & Van Loan sym.schur2.
-template <typename T>
-__device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_only = false) {
+// round.  Pair rows are recomputed in registers and (c, s) read as one vector, keeping the
+// shared-memory instruction count (the sub-solve's limiter: short-scoreboard / MIO stalls) low.
+// The pair's own 2x2 block gets the exact values of Golub & Van Loan sym.schur2.
+// CROSS: the 1024 pairs between the two 32-row blocks (32 rounds); else all 2016 pairs (63).
+template <typename T, bool CROSS>
+__device__ int cta_jacobi64_rounds(T* S, T* U, T tol_abs, T tol_null) {
+  using T2 = typename CS<T>::type;
   constexpr T UR = EigU<T>::u;
-  __shared__ T pc[NS / 2], ps[NS / 2], pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
-  __shared__ int pa[NS / 2], pb[NS / 2];
+  constexpr int NROUNDS = CROSS ? HB : NS - 1;
+  __shared__ T2 pcs[NS / 2];
+  __shared__ T pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
   __shared__ int rot_round, rot_any;
   const int tid = threadIdx.x;
   for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? T(1) : T(0);
   if (tid == 0) rot_any = 0;
-  // full sweep: all 2016 pairs (circle method, 63 rounds); cross-only: the 1024 pairs between the
-  // two 32-row blocks (32 rounds, pair (i, 32 + (i + r) mod 32))
-  const int nrounds = cross_only ? HB : NS - 1;
-  for (int r = 0; r < nrounds; ++r) {
+  for (int r = 0; r < NROUNDS; ++r) {
     if (tid == 0) rot_round = 0;
     __syncthreads();
     if (tid < NS / 2) {
-      const int a = cross_only ? tid : circle_pos(r, tid, NS);
-      const int b = cross_only ? HB + (tid + r) % HB : circle_pos(r, NS - 1 - tid, NS);
+      int a, b;
+      pair_rows<CROSS>(r, tid, a, b);
       const T apq = S[a * LDS_ + b], app = S[a * LDS_ + a], aqq = S[b * LDS_ + b];
       T thr = fmax(T(4) * UR * sqrt(fabs(app)) * sqrt(fabs(aqq)), tol_abs);
       if (fabs(app) <= tol_null && fabs(aqq) <= tol_null) thr = fmax(thr, tol_null);
@@ -257,10 +276,10 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
         sn = t * c;
         rot_round = 1;
       }
-      pa[tid] = a;
-      pb[tid] = b;
-      pc[tid] = c;
-      ps[tid] = sn;
+      T2 cs;
+      cs.x = c;
+      cs.y = sn;
+      pcs[tid] = cs;
       pt[tid] = t;
       papq[tid] = apq;
       papp[tid] = app;
@@ -273,9 +292,10 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
     for (int k = 0; k < 4; ++k) {
       const int blk = tid + 256 * k;
       const int i = blk >> 5, j = blk & 31;
-      const T si = ps[i], sj = ps[j];
-      if (si == T(0) && sj == T(0)) continue;
-      const int ai = pa[i], bi = pb[i];
+      const T2 csi = pcs[i], csj = pcs[j];
+      if (csi.y == T(0) && csj.y == T(0)) continue;
+      int ai, bi, aj, bj;
+      pair_rows<CROSS>(r, i, ai, bi);
       if (i == j) {
         S[ai * LDS_ + ai] = papp[i] - pt[i] * papq[i];
         S[bi * LDS_ + bi] = paqq[i] + pt[i] * papq[i];
@@ -283,16 +303,16 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
         S[bi * LDS_ + ai] = T(0);
         continue;
       }
-      const int aj = pa[j], bj = pb[j];
+      pair_rows<CROSS>(r, j, aj, bj);
       T m00 = S[ai * LDS_ + aj], m01 = S[ai * LDS_ + bj], m10 = S[bi * LDS_ + aj], m11 = S[bi * LDS_ + bj];
-      if (sj != T(0)) {  // columns: M <- M L_j^T
-        const T cj = pc[j];
+      if (csj.y != T(0)) {  // columns: M <- M L_j^T
+        const T cj = csj.x, sj = csj.y;
         const T n00 = cj * m00 - sj * m01, n01 = sj * m00 + cj * m01;
         const T n10 = cj * m10 - sj * m11, n11 = sj * m10 + cj * m11;
         m00 = n00; m01 = n01; m10 = n10; m11 = n11;
       }
-      if (si != T(0)) {  // rows: M <- L_i M
-        const T ci = pc[i];
+      if (csi.y != T(0)) {  // rows: M <- L_i M
+        const T ci = csi.x, si = csi.y;
         const T o00 = ci * m00 - si * m10, o10 = si * m00 + ci * m10;
         const T o01 = ci * m01 - si * m11, o11 = si * m01 + ci * m11;
         m00 = o00; m10 = o10; m01 = o01; m11 = o11;
@@ -305,20 +325,19 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
     {  // U <- U J: thread -> row tid/4, pairs (tid & 3) + 4k
       const int row = tid >> 2, q0 = tid & 3;
       T ua[8], ub[8];
+      int ca[8], cb[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int q = q0 + 4 * k;
-        ua[k] = U[row * LDS_ + pa[q]];
-        ub[k] = U[row * LDS_ + pb[q]];
+        pair_rows<CROSS>(r, q0 + 4 * k, ca[k], cb[k]);
+        ua[k] = U[row * LDS_ + ca[k]];
+        ub[k] = U[row * LDS_ + cb[k]];
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int q = q0 + 4 * k;
-        const T sn = ps[q];
-        if (sn == T(0)) continue;
-        const T c = pc[q];
-        U[row * LDS_ + pa[q]] = c * ua[k] - sn * ub[k];
-        U[row * LDS_ + pb[q]] = sn * ua[k] + c * ub[k];
+        const T2 cs = pcs[q0 + 4 * k];
+        if (cs.y == T(0)) continue;
+        U[row * LDS_ + ca[k]] = cs.x * ua[k] - cs.y * ub[k];
+        U[row * LDS_ + cb[k]] = cs.y * ua[k] + cs.x * ub[k];
       }
     }
     if (tid == 0) rot_any = 1;
@@ -326,6 +345,12 @@ __device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_
   }
   __syncthreads();
   return rot_any;
+}
+
+template <typename T>
+__device__ int cta_jacobi64_sweep(T* S, T* U, T tol_abs, T tol_null, bool cross_only = false) {
+  return cross_only ? cta_jacobi64_rounds<T, true>(S, U, tol_abs, tol_null)
+                    : cta_jacobi64_rounds<T, false>(S, U, tol_abs, tol_null);
 }
 
 // One CTA per (job, pair).  Small jobs are solved completely here.
