@@ -9,8 +9,8 @@ hand-written sm_100a kernels in ``libshampoo_b200.so`` (see include/shampoo_b200
 from .config import (BufferOverflowError, DivergedReplicasError, GraftKind, InvalidGroupSizeError,
                      LargeDimMethod, NativeError, NonFiniteGradientError, OutOfRangeError, ShampooConfig,
                      Solver, lr_at)
-from .planning import (AssignmentPlan, BlockPlan, BlockRegion, BlockSpec, GlobalBlock, NativePlan,
-                       block_partition, buffer_size, enumerate_blocks, greedy_assign, merge_dims,
+from .planning import (AssignmentPlan, BlockPlan, BlockRegion, BlockSpec, CommReport, GlobalBlock, NativePlan,
+                       block_partition, buffer_size, comm_meter, enumerate_blocks, greedy_assign, merge_dims,
                        plan_parameter, state_scalar_count)
 
 __version__ = "0.1.0"
@@ -28,10 +28,11 @@ def __getattr__(name):
 
 
 __all__ = [
-    "AssignmentPlan", "BlockPlan", "BlockRegion", "BlockSpec", "BufferOverflowError", "DistributedShampoo",
+    "AssignmentPlan", "BlockPlan", "BlockRegion", "BlockSpec", "BufferOverflowError", "CommReport",
+    "DistributedShampoo",
     "DivergedReplicasError", "GlobalBlock", "GraftKind", "GroupExchange", "GuardStats",
     "InvalidGroupSizeError", "LargeDimMethod", "NativeError", "NativePlan", "NonFiniteGradientError",
     "OutOfRangeError", "Shampoo", "ShampooConfig", "Solver", "batched_root_inverse", "tc_gemm", "block_partition",
-    "buffer_size", "enumerate_blocks", "greedy_assign", "launch_count", "lr_at", "merge_dims",
+    "buffer_size", "comm_meter", "enumerate_blocks", "greedy_assign", "launch_count", "lr_at", "merge_dims",
     "plan_parameter", "state_scalar_count",
 ]

@@ -25,7 +25,7 @@ from .config import LargeDimMethod, METHOD_CODES
 __all__ = [
     "SCALAR_BYTES", "merge_dims", "BlockSpec", "BlockPlan", "block_partition", "plan_parameter",
     "GlobalBlock", "BlockRegion", "AssignmentPlan", "NativePlan", "enumerate_blocks", "greedy_assign",
-    "buffer_size", "state_scalar_count",
+    "buffer_size", "state_scalar_count", "CommReport", "comm_meter",
 ]
 
 SCALAR_BYTES = 8  # reference wire scalar (dist.py:48-50)
@@ -241,3 +241,40 @@ def state_scalar_count(shape: tuple[int, ...], method: LargeDimMethod) -> int:
     if method is LargeDimMethod.ADAGRAD:
         return math.prod(shape)
     return sum(shape)
+
+
+@dataclass(frozen=True)
+class CommReport:
+    """Deterministic communication and memory accounting for a plan (dist.py:370-391)."""
+
+    steps: int
+    bytes_gathered_per_step: int  # one group's buffer, per step
+    world_bytes_per_step: int  # all replica groups together
+    total_bytes_gathered: int
+    per_worker_state_scalars: tuple
+    per_worker_state_bytes: tuple
+
+    def to_json_dict(self) -> dict:
+        return {
+            "steps": self.steps,
+            "bytes_gathered_per_step": self.bytes_gathered_per_step,
+            "world_bytes_per_step": self.world_bytes_per_step,
+            "total_bytes_gathered": self.total_bytes_gathered,
+            "per_worker_state_scalars": list(self.per_worker_state_scalars),
+            "per_worker_state_bytes": list(self.per_worker_state_bytes),
+        }
+
+
+def comm_meter(plan: AssignmentPlan, block_shapes: Sequence[Sequence[int]],
+               method: LargeDimMethod = LargeDimMethod.BLOCKING, steps: int = 1) -> CommReport:
+    """Gathered bytes per step and per-worker state footprint (dist.py:394-423), in the
+    reference's 8-byte wire scalars (the device buffer uses the context's element size)."""
+    if len(block_shapes) != len(plan.var_counts):
+        raise ValueError("one shape per planned block required")
+    per_group = buffer_size(plan)
+    world = per_group * plan.num_groups
+    state = tuple(sum(state_scalar_count(tuple(block_shapes[i]), method) for i in plan.assignments[r])
+                  for r in range(plan.world_size))
+    return CommReport(steps=steps, bytes_gathered_per_step=per_group, world_bytes_per_step=world,
+                      total_bytes_gathered=world * steps, per_worker_state_scalars=state,
+                      per_worker_state_bytes=tuple(x * SCALAR_BYTES for x in state))

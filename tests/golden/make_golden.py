@@ -27,7 +27,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, os.path.join(HERE, "..", ".."))
 
 from minishampoo import matfun  # noqa: E402
-from minishampoo.dist import enumerate_blocks, greedy_assign  # noqa: E402
+from minishampoo.dist import comm_meter, enumerate_blocks, greedy_assign  # noqa: E402
 from minishampoo.grafting import GraftKind  # noqa: E402
 from minishampoo.optim import Shampoo, ShampooConfig  # noqa: E402
 from minishampoo.precond import LargeDimMethod  # noqa: E402
@@ -64,6 +64,10 @@ def make_plans(out):
             out[f"{wk}/owner"] = owner
             out[f"{wk}/offset"] = offset
             out[f"{wk}/counters"] = np.array(plan.counters, np.int64)
+            rep = comm_meter(plan, [x.shape for x in blocks], steps=3)  # dist.py:394-423
+            out[f"{wk}/comm"] = np.array([rep.bytes_gathered_per_step, rep.world_bytes_per_step,
+                                          rep.total_bytes_gathered], np.int64)
+            out[f"{wk}/state_scalars"] = np.array(rep.per_worker_state_scalars, np.int64)
 
 
 TRAJ_SHAPES = [(6, 5), (7,), (3, 4, 5), (2, 3, 3, 1), (1, 1), (9, 4)]
@@ -173,9 +177,11 @@ def make_rootinv(out):
 def main():
     plans, traj, rinv, meta = {}, {}, {}, {}
     make_plans(plans)
+    np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans)
+    if "--plans-only" in sys.argv:
+        return
     make_trajectories(traj, meta)
     make_rootinv(rinv)
-    np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans)
     np.savez_compressed(os.path.join(HERE, "trajectories.npz"), **traj)
     np.savez_compressed(os.path.join(HERE, "rootinv.npz"), **rinv)
     with open(os.path.join(HERE, "trajectories.json"), "w") as fh:

@@ -128,6 +128,20 @@ def test_model_plans_bit_exact_with_reference(key):
             assert tuple(x.hi[k] - x.lo[k] for k in range(x.order)) == tuple(int(v) for v in row if v)
 
 
+@pytest.mark.parametrize("key", sorted({k.split("/")[0] for k in PLANS.files}))
+def test_comm_meter_matches_reference(key):
+    """comm_meter (dist.py:394-423) against the reference's own reports for every model plan."""
+    model, b = key.rsplit("_b", 1)
+    blocks = P.enumerate_blocks(MODEL_SHAPES[model], P.ShampooConfig(max_preconditioner_dim=int(b)))
+    for wk in sorted({k.split("/")[1] for k in PLANS.files if k.startswith(key + "/J")}):
+        world, group = (int(v) for v in wk[1:].split("G"))
+        plan = P.greedy_assign([x.var_count for x in blocks], world, group)
+        rep = P.comm_meter(plan, [x.shape for x in blocks], steps=3)
+        assert [rep.bytes_gathered_per_step, rep.world_bytes_per_step, rep.total_bytes_gathered] == \
+            PLANS[f"{key}/{wk}/comm"].tolist()
+        assert list(rep.per_worker_state_scalars) == PLANS[f"{key}/{wk}/state_scalars"].tolist()
+
+
 def test_resnet50_plan_summary():
     # SURVEY.md §0 fact 3: 161 blocks, orders 1/2/3 = 107/45/9; J=8 buffer 3,194,880 scalars/rank
     plan = P.NativePlan(MODEL_SHAPES["resnet50"], 2048, P.LargeDimMethod.BLOCKING, 8, 8)
@@ -156,3 +170,57 @@ def test_lr_schedule_table():
     with pytest.raises(P.OutOfRangeError):
         P.lr_at(cfg, 90)
     assert P.lr_at(P.ShampooConfig(lr=0.3), 10**6) == 0.3
+
+
+class TestCommMeter:
+    """dist.py:394-423, restating test_dist.py:234-274 (TestCommMeter)."""
+
+    def test_matrix_state_accounting(self):
+        cfg = P.ShampooConfig(max_preconditioner_dim=8)
+        blocks = P.enumerate_blocks([(8, 8)], cfg)
+        plan = P.greedy_assign([b.var_count for b in blocks], 1, 1)
+        report = P.comm_meter(plan, [b.shape for b in blocks])
+        assert report.per_worker_state_scalars == (4 * 64,)
+        assert report.per_worker_state_bytes == (4 * 64 * 8,)
+
+    def test_split_matrix_halves_state(self):
+        cfg = P.ShampooConfig(max_preconditioner_dim=8)
+        blocks = P.enumerate_blocks([(16, 8)], cfg)
+        assert len(blocks) == 2
+        plan = P.greedy_assign([b.var_count for b in blocks], 2, 2)
+        assert P.comm_meter(plan, [b.shape for b in blocks]).per_worker_state_scalars == (4 * 64, 4 * 64)
+
+    def test_cube_state_accounting(self):
+        b = 4
+        blocks = P.enumerate_blocks([(b, b, b)], P.ShampooConfig(max_preconditioner_dim=b))
+        plan = P.greedy_assign([blk.var_count for blk in blocks], 1, 1)
+        assert sum(P.comm_meter(plan, [blk.shape for blk in blocks]).per_worker_state_scalars) == 6 * b * b
+
+    def test_gather_volume_scales_with_groups(self):
+        plan_one = P.greedy_assign([6, 5, 4, 3], world_size=4, group_size=4)
+        plan_two = P.greedy_assign([6, 5, 4, 3], world_size=4, group_size=2)
+        shapes = [(6,), (5,), (4,), (3,)]
+        one = P.comm_meter(plan_one, shapes, steps=3)
+        two = P.comm_meter(plan_two, shapes, steps=3)
+        assert one.world_bytes_per_step == P.buffer_size(plan_one)
+        assert two.world_bytes_per_step == 2 * P.buffer_size(plan_two)
+        assert one.total_bytes_gathered == 3 * one.world_bytes_per_step
+        assert set(one.to_json_dict()) == {"steps", "bytes_gathered_per_step", "world_bytes_per_step",
+                                           "total_bytes_gathered", "per_worker_state_scalars",
+                                           "per_worker_state_bytes"}
+
+    def test_diagonal_fallback_accounting(self):
+        plan = P.greedy_assign([12], world_size=1, group_size=1)
+        assert P.comm_meter(plan, [(3, 4)], method=P.LargeDimMethod.DIAGONAL).per_worker_state_scalars == (7,)
+        assert P.comm_meter(plan, [(3, 4)], method=P.LargeDimMethod.ADAGRAD).per_worker_state_scalars == (12,)
+        with pytest.raises(ValueError):
+            P.comm_meter(plan, [(3, 4), (2,)])
+
+    def test_resnet50_world8_matches_reference_fixture(self):
+        # the J=8 ResNet-50 plan: per-group buffer 204,472,320 B (SURVEY.md §8a a7)
+        blocks = P.enumerate_blocks(MODEL_SHAPES["resnet50"], P.ShampooConfig(max_preconditioner_dim=2048))
+        plan = P.greedy_assign([b.var_count for b in blocks], 8, 8)
+        report = P.comm_meter(plan, [b.shape for b in blocks], steps=50)
+        assert report.bytes_gathered_per_step == 204_472_320
+        assert report.total_bytes_gathered == 50 * 204_472_320
+        assert sum(report.per_worker_state_scalars) == 2 * 128_111_874
