@@ -172,6 +172,17 @@ SHAMPOO_API int shampoo_stats_update(shampoo_ctx* ctx, const void* const* grads,
 /* Step t phase 2: if t >= start and t % frequency == 0, guarded root inverse of
  * every owned factor (eigh or coupled Newton).  Synchronises `stream` (one
  * small readback per solver sweep). Returns 1 in *refreshed if it ran. */
+/* ---- gradient reduction to block owners (replaces the DDP all-reduce the reference
+ * does not model, dist.py:332-356): every rank packs its LOCAL gradients into the gather-buffer layout
+ * (gbuf: group_size * max_payload scalars of the context dtype, block b at its gather offset), the
+ * caller reduce-scatters gbuf within the group (+ all-reduces the owned region across replica
+ * groups), checks non-finite entries of the owned blocks (device flag, to be max-reduced across
+ * ranks) and runs the stats phase from the reduced buffer, scaled by gscale (1/world for a mean). */
+SHAMPOO_API int shampoo_pack_gradients(shampoo_ctx* ctx, const void* const* grads, int32_t dtype, void* gbuf,
+                                       void* stream);
+SHAMPOO_API int shampoo_reduced_nonfinite(shampoo_ctx* ctx, const void* gbuf, int32_t* device_flag, void* stream);
+SHAMPOO_API int shampoo_stats_update_reduced(shampoo_ctx* ctx, const void* gbuf, double gscale,
+                                             const void* const* params, int32_t dtype, int64_t t, void* stream);
 SHAMPOO_API int shampoo_root_inverse(shampoo_ctx* ctx, int64_t t, int32_t* refreshed, void* stream);
 /* Step t phase 3: directions of owned blocks -> this rank's gather-buffer region. */
 SHAMPOO_API int shampoo_precondition_graft(shampoo_ctx* ctx, const void* const* params, int32_t dtype,

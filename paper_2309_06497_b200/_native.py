@@ -84,6 +84,9 @@ SIGNATURES = {
     "shampoo_check_finite": (C.c_int, [_P, C.POINTER(_P), _I32, _P]),
     "shampoo_stats_update": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I32, _I64, _P]),
     "shampoo_root_inverse": (C.c_int, [_P, _I64, _PI32, _P]),
+    "shampoo_pack_gradients": (C.c_int, [_P, C.POINTER(_P), _I32, _P, _P]),
+    "shampoo_reduced_nonfinite": (C.c_int, [_P, _P, _P, _P]),
+    "shampoo_stats_update_reduced": (C.c_int, [_P, _P, _D, C.POINTER(_P), _I32, _I64, _P]),
     "shampoo_precondition_graft": (C.c_int, [_P, C.POINTER(_P), _I32, _I64, _P]),
     "shampoo_apply": (C.c_int, [_P, C.POINTER(_P), _I32, _D, _P]),
     "shampoo_gather_buffer": (_P, [_P, _PI64, _PI32]),

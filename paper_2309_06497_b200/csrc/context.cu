@@ -591,14 +591,21 @@ int shampoo_check_finite(shampoo_ctx* c, const void* const* grads, int32_t dtype
   return SHAMPOO_OK;
 }
 
-int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* const* params, int32_t dtype,
-                         int64_t t, void* stream) {
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+namespace {
+// The stats phase; gradients from the caller's tensors (grads) or from a reduced gather-layout
+// buffer (gbuf, context dtype, scaled by gscale).
+int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf, double gscale,
+                      const void* const* params, int32_t dtype, int64_t t, cudaStream_t s) {
   int rc = upload_ptrs(c, grads, params, s);
   if (rc) return rc;
   const int64_t gstep = c->graft_step + 1;  // GraftState.update increments first (grafting.py:71)
-  const StepScalars sc = make_scalars(c, t, dtype, gstep);
+  StepScalars sc = make_scalars(c, t, dtype, gstep);
   ElemArenas ar = arenas(c);
+  if (gbuf) {
+    sc.gbuf = 1;
+    sc.gscale = gscale;
+    ar.GBUF = gbuf;
+  }
   const void* const* gp = (const void* const*)c->d_ptrs;
   const void* const* pp = (const void* const*)(c->d_ptrs + c->nparams);
   const int no = (int)c->owned.size();
@@ -630,6 +637,37 @@ int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* c
   for (size_t l = 0; l < c->owned.size(); ++l)
     if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_GRAFT_ONLY) ++c->step[l];
   return SHAMPOO_OK;
+}
+}  // namespace
+
+int shampoo_stats_update(shampoo_ctx* c, const void* const* grads, const void* const* params, int32_t dtype,
+                         int64_t t, void* stream) {
+  return stats_update_impl(c, grads, nullptr, 1.0, params, dtype, t, static_cast<cudaStream_t>(stream));
+}
+
+int shampoo_stats_update_reduced(shampoo_ctx* c, const void* gbuf, double gscale, const void* const* params,
+                                 int32_t dtype, int64_t t, void* stream) {
+  if (!gbuf) {
+    set_error("stats_update_reduced: null gradient buffer");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  return stats_update_impl(c, nullptr, gbuf, gscale, params, dtype, t, static_cast<cudaStream_t>(stream));
+}
+
+int shampoo_pack_gradients(shampoo_ctx* c, const void* const* grads, int32_t dtype, void* gbuf, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = upload_ptrs(c, grads, nullptr, s);
+  if (rc) return rc;
+  const void* const* gp = (const void* const*)c->d_ptrs;
+  return c->f32 ? launch_pack_grads<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, gp, dtype, gbuf, s)
+                : launch_pack_grads<double>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, gp, dtype, gbuf, s);
+}
+
+int shampoo_reduced_nonfinite(shampoo_ctx* c, const void* gbuf, int32_t* d_flag, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SH_CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), s));
+  return c->f32 ? launch_region_finite<float>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gbuf, d_flag, s)
+                : launch_region_finite<double>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gbuf, d_flag, s);
 }
 
 int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* stream) {

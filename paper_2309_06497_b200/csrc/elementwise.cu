@@ -67,9 +67,14 @@ __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restric
     const int64_t j = c.start + e;
     T g;
     if (pass == 0 || !normalized) {
-      const int64_t po = block_to_param_offset(B, j);
-      g = load_as<T>(gp, po, sc.pdtype);
-      if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
+      if (sc.gbuf) {  // reduced gradient: this block's slice of the gather-layout buffer
+        g = T(sc.gscale * (double)static_cast<const T*>(ar.GBUF)[B.gofs + j]);
+        if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
+      } else {
+        const int64_t po = block_to_param_offset(B, j);
+        g = load_as<T>(gp, po, sc.pdtype);
+        if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
+      }
       G[j] = g;
     } else {
       g = G[j];
@@ -362,6 +367,52 @@ int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void*
   return SHAMPOO_OK;
 }
 
+// Gradients (caller layout) -> gather-buffer layout: buf[gofs + j] for every block (all ranks pack
+// every block; a reduce-scatter then leaves each owner the summed gradient of its blocks).
+template <typename T>
+__global__ void __launch_bounds__(NT) k_pack_grads(const Chunk* __restrict__ chunks, const DevBlock* __restrict__ blocks,
+                                                   const void* const* __restrict__ grads, int32_t dtype,
+                                                   T* __restrict__ buf) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  const void* g = grads[B.param];
+  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
+    const int64_t j = c.start + e;
+    buf[B.gofs + j] = load_as<T>(g, block_to_param_offset(B, j), dtype);
+  }
+}
+
+// Non-finite entries among the owned blocks' reduced gradients (device flag, no host sync).
+template <typename T>
+__global__ void __launch_bounds__(NT) k_region_finite(const Chunk* __restrict__ chunks,
+                                                      const DevBlock* __restrict__ blocks,
+                                                      const T* __restrict__ buf, int32_t* flag) {
+  const Chunk c = chunks[blockIdx.x];
+  const DevBlock& B = blocks[c.block];
+  int bad = 0;
+  for (int64_t e = threadIdx.x; e < c.count; e += NT)
+    if (!isfinite((double)buf[B.gofs + c.start + e])) bad = 1;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+int launch_pack_grads(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* grads,
+                      int32_t dtype, void* buf, cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_pack_grads<T><<<nchunks, NT, 0, s>>>(chunks, blocks, grads, dtype, static_cast<T*>(buf));
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+template <typename T>
+int launch_region_finite(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* buf, int32_t* flag,
+                         cudaStream_t s) {
+  if (!nchunks) return SHAMPOO_OK;
+  k_region_finite<T><<<nchunks, NT, 0, s>>>(chunks, blocks, static_cast<const T*>(buf), flag);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
 #define SH_INST(T)                                                                                   \
   template int launch_finite<T>(const Chunk*, int, const DevBlock*, const void* const*, int32_t,    \
                                 int32_t*, cudaStream_t);                                             \
@@ -376,7 +427,10 @@ int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void*
   template int launch_fallback_update<T>(const Chunk*, int, const DevBlock*, const ElemArenas&,      \
                                          const FallbackArgs&, const int32_t*, int, cudaStream_t);    \
   template int launch_fallback_precondition<T>(const Chunk*, int, const DevBlock*, const ElemArenas&, \
-                                               const FallbackArgs&, const int32_t*, int, int, cudaStream_t);
+                                               const FallbackArgs&, const int32_t*, int, int, cudaStream_t); \
+  template int launch_pack_grads<T>(const Chunk*, int, const DevBlock*, const void* const*, int32_t, void*, \
+                                    cudaStream_t);                                                          \
+  template int launch_region_finite<T>(const Chunk*, int, const DevBlock*, const void*, int32_t*, cudaStream_t);
 SH_INST(double)
 SH_INST(float)
 

@@ -21,7 +21,8 @@ struct StepScalars {
   int32_t use_filter;  // beta1 > 0
   int32_t precond;     // t >= start_preconditioning_step
   int32_t pdtype;      // caller tensor dtype
-  int32_t pad;
+  int32_t gbuf;        // gradients come from the reduced gradient buffer (ElemArenas::GBUF), not grads[]
+  double gscale;       // multiplier on buffer gradients (1/world for a mean reduction)
 };
 
 struct ElemArenas {
@@ -37,6 +38,7 @@ struct ElemArenas {
   double* pg2;    // per owned block ||P_graft||^2
   double* ps2;    // per owned block ||P_shampoo||^2
   const int32_t* ready;  // per owned block: inverse present
+  const void* GBUF;       // reduced gradient buffer (gather-buffer layout, context dtype) or null
 };
 
 template <typename T>
@@ -73,5 +75,11 @@ int launch_fallback_precondition(const Chunk* chunks, int nchunks, const DevBloc
 template <typename T>
 int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
                  const void* buf, const StepScalars& sc, cudaStream_t s);
+template <typename T>
+int launch_pack_grads(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* grads,
+                      int32_t dtype, void* buf, cudaStream_t s);
+template <typename T>
+int launch_region_finite(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* buf, int32_t* flag,
+                         cudaStream_t s);
 
 }  // namespace shampoo

@@ -57,6 +57,34 @@ class GroupExchange:
                 if self.rank in ranks:
                     self.group = pg
         self.bytes_per_step = 0
+        # cross-group communicators: ranks with the same group rank in every replica group
+        self.cross = None
+        if self.world // group_size > 1:
+            for k in range(group_size):
+                ranks = list(range(k, self.world, group_size))
+                pg = dist.new_group(ranks)
+                if self.rank in ranks:
+                    self.cross = pg
+
+    def reduce_gradients(self, buf: torch.Tensor, group_rank: int, max_payload: int) -> None:
+        """Sum every rank's packed local gradients into the owner's region:
+        reduce-scatter inside the group, then all-reduce the region across the replica groups
+        (ranks holding the same blocks).  Half the bytes of a full gradient all-reduce."""
+        if max_payload == 0:
+            return
+        full = buf[: self.group_size * max_payload]
+        region = buf[group_rank * max_payload:(group_rank + 1) * max_payload]
+        if self.group_size > 1:
+            try:
+                dist.reduce_scatter_tensor(region, full, op=dist.ReduceOp.SUM, group=self.group)  # in place
+            except (RuntimeError, NotImplementedError, AttributeError, ValueError):
+                dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.group)  # backends without it (gloo)
+        if self.cross is not None:
+            dist.all_reduce(region, op=dist.ReduceOp.SUM, group=self.cross)
+
+    def max_flag(self, flag: torch.Tensor) -> None:
+        """Max over all ranks of a device flag (non-finite gradient anywhere aborts everywhere)."""
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
 
     def __call__(self, buf: torch.Tensor, group_rank: int, max_payload: int) -> None:
         if max_payload == 0 or self.group_size == 1:
@@ -85,7 +113,13 @@ class DistributedShampoo(torch.optim.Optimizer):
                  newton_tolerance: float = 1e-6, num_trainers_per_group: int = -1,
                  large_dim_method=LargeDimMethod.BLOCKING, precision: str = "double",
                  lr_schedule: str = "constant", warmup_steps: int = 0, total_steps: int = 0,
-                 process_group=None):
+                 process_group=None, reduce_gradients: Optional[str] = None):
+        """``reduce_gradients``: None (p.grad already holds the global gradient, e.g. after DDP) or
+        "mean" / "sum": p.grad holds this rank's LOCAL gradient and the optimizer reduce-scatters
+        it to the block owners itself (no separate DDP all-reduce needed)."""
+        if reduce_gradients not in (None, "mean", "sum"):
+            raise ValueError("reduce_gradients must be None, 'mean' or 'sum'")
+        self.reduce_gradients = reduce_gradients
         grafting = GraftKind(grafting) if not isinstance(grafting, GraftKind) else grafting
         solver = Solver(solver) if not isinstance(solver, Solver) else solver
         large_dim_method = (LargeDimMethod(large_dim_method)
@@ -127,7 +161,10 @@ class DistributedShampoo(torch.optim.Optimizer):
             with torch.enable_grad():
                 loss = closure()
         grads = [p.grad if p.grad is not None else torch.zeros_like(p) for p in self._plist]
-        self.engine.step(grads)
+        if self.reduce_gradients is None:
+            self.engine.step(grads)
+        else:
+            self.engine.step_local(grads, average=self.reduce_gradients == "mean")
         return loss
 
     def state_dict(self) -> dict:

@@ -229,6 +229,76 @@ class Shampoo:
         self.apply_gathered(t)
         self._t += 1
 
+    # -- gradient reduction to block owners
+
+    def reduced_gradient_buffer(self) -> torch.Tensor:
+        """Gather-layout gradient buffer (group_size * max_payload scalars, context dtype)."""
+        if getattr(self, "_gbuf", None) is None:
+            n = max(self.group_size * self.max_payload, 1)
+            self._gbuf = torch.zeros(n, dtype=torch.float32 if self._buf_f32 else torch.float64, device=self.device)
+            self._gflag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return self._gbuf
+
+    def pack_local_gradients(self, grads) -> torch.Tensor:
+        """This rank's LOCAL gradients -> the gather-layout buffer (every block at its offset)."""
+        grads = self._as_grads(grads)
+        buf = self.reduced_gradient_buffer()
+        gp = N.ptr_array([g.data_ptr() for g in grads])
+        N.check(N.lib().shampoo_pack_gradients(self._ctx, gp, _dtype_code(grads[0]), buf.data_ptr(), self._stream()),
+                "pack_gradients")
+        return buf
+
+    def step_reduced(self, scale: float = 1.0, flag: Optional[torch.Tensor] = None) -> None:
+        """One step whose gradients are the reduced buffer (``reduced_gradient_buffer()`` after the
+        reduce-scatter): only this rank's owned blocks are read, scaled by ``scale``.  Raises
+        NonFiniteGradientError before any mutation if an owned block holds a non-finite entry;
+        ``flag``: the ``nonfinite_flag()`` already max-reduced across ranks (distributed)."""
+        if flag is None:
+            flag = self.nonfinite_flag()
+        if self.check_finite and int(flag.item()):
+            raise NonFiniteGradientError("gradient contains non-finite entries; step aborted")
+        t = self._t
+        lr_at(self.config, t)  # OutOfRangeError before any mutation
+        self.compute_directions_from_buffer(scale, t)
+        if self.exchange is not None and self.group_size > 1:
+            self.exchange(self.gather_buffer, self.group_rank, self.max_payload)
+        self.apply_gathered(t)
+        self._t += 1
+
+    def compute_directions_from_buffer(self, scale: float = 1.0, t: Optional[int] = None) -> None:
+        """Phases 1-3 for the owned blocks with gradients from the reduced buffer (scaled)."""
+        t = self._t if t is None else t
+        lib = N.lib()
+        s = self._stream()
+        dtype = _dtype_code(self._params[0]) if self._params else N.DTYPE_F32
+        pp = N.ptr_array([p.data_ptr() for p in self._params])
+        N.check(lib.shampoo_stats_update_reduced(self._ctx, self.reduced_gradient_buffer().data_ptr(), float(scale),
+                                                 pp, dtype, t, s), "stats_update_reduced")
+        r = C.c_int32()
+        N.check(lib.shampoo_root_inverse(self._ctx, t, C.byref(r), s), "root_inverse")
+        N.check(lib.shampoo_precondition_graft(self._ctx, pp, dtype, t, s), "precondition_graft")
+
+    def nonfinite_flag(self) -> torch.Tensor:
+        """Device int32 flag: non-finite entries among this rank's owned reduced gradients."""
+        buf = self.reduced_gradient_buffer()
+        N.check(N.lib().shampoo_reduced_nonfinite(self._ctx, buf.data_ptr(), self._gflag.data_ptr(), self._stream()),
+                "reduced_nonfinite")
+        return self._gflag
+
+    def step_local(self, grads, average: bool = True) -> None:
+        """Step from this rank's LOCAL gradients: reduce-scatter them to the block owners (+ all-reduce
+        across replica groups) instead of a full DDP all-reduce, then the usual step.  ``average``
+        divides by the world size (DDP mean).  Single process: identical to ``step(grads)``."""
+        buf = self.pack_local_gradients(grads)
+        ex = self.exchange
+        distributed = ex is not None and self.world_size > 1
+        if distributed:
+            ex.reduce_gradients(buf, self.group_rank, self.max_payload)
+        flag = self.nonfinite_flag()
+        if distributed:
+            ex.max_flag(flag)
+        self.step_reduced(1.0 / self.world_size if average else 1.0, flag=flag)
+
     # -- parity helpers
 
     def direction(self, i: int, b: int) -> torch.Tensor:

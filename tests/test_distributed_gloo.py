@@ -104,3 +104,55 @@ def test_group_allgather_matches_single_process(world, group):
         p.join(timeout=240)
         assert p.exitcode == 0
     assert dict(out) == {r: 1 for r in range(world)}
+
+
+def _reduce_worker(rank, world, group, port, out):
+    """GroupExchange.reduce_gradients: after packing LOCAL gradients in the gather
+    layout and reducing, this rank's region holds the sum over ALL ranks of the gradients of the blocks
+    it owns (reduce-scatter in the group + all-reduce across replica groups); the non-finite flag is a
+    max over ranks."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2309_06497_b200 as P
+        from paper_2309_06497_b200.distributed import GroupExchange
+
+        plan = P.NativePlan(SHAPES, MAX_DIM, P.LargeDimMethod.BLOCKING, world, group)
+        ex = GroupExchange(group)
+        mp_ = plan.max_payload
+        info = plan.blocks_info
+
+        def packed(r):  # rank r's local gradients in the gather layout (the device pack, restated)
+            g = np.random.default_rng(100 + r)
+            buf = np.zeros(group * mp_)
+            for b in info:
+                buf[b.gather_offset: b.gather_offset + b.var_count] = g.standard_normal(b.var_count)
+            return buf
+
+        buf = torch.as_tensor(packed(rank))
+        ex.reduce_gradients(buf, rank % group, mp_)
+        total = sum(packed(r) for r in range(world))
+        gr = rank % group
+        mine = slice(gr * mp_, (gr + 1) * mp_)
+        ok = bool(np.allclose(buf.numpy()[mine], total[mine], rtol=1e-13, atol=1e-13))
+        flag = torch.tensor([1 if rank == world - 1 else 0], dtype=torch.int32)
+        ex.max_flag(flag)
+        ok &= int(flag.item()) == 1
+        out[rank] = int(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,group", [(2, 2), (4, 2), (4, 4)])
+def test_gradient_reduce_to_owners(world, group):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, group, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert dict(out) == {r: 1 for r in range(world)}

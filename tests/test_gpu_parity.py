@@ -319,3 +319,86 @@ def test_resnet_shapes_vs_oracle(cuda_device, precision, eps):
     print(f"{precision}: worst factor rel {worst['factor']:.2e}, worst direction rel {worst['dir']:.2e}")
     assert worst["factor"] <= 1e-4, worst
     assert worst["dir"] <= 1e-3, worst
+
+
+def test_step_local_single_process_equals_step(cuda_device):
+    """with one process the reduced-gradient path (pack -> buffer -> stats from the
+    buffer) is bit-identical to the plain step."""
+    name = "adam_beta1_l2"  # beta1 filter + L2 weight decay read through the buffer path
+    cfg = config_from_meta(name)
+    shapes = [tuple(s) for s in META["configs"][name]["shapes"]]
+
+    def run(local: bool):
+        params = [torch.as_tensor(TRAJ[f"{name}/init/{i}"].astype(np.float64), device=cuda_device)
+                  for i in range(len(shapes))]
+        opt = P.Shampoo(params, cfg)
+        for t in range(META["steps"]):
+            grads = [torch.as_tensor(TRAJ[f"{name}/grad/{t}/{i}"].astype(np.float64), device=cuda_device)
+                     for i in range(len(shapes))]
+            opt.step_local(grads) if local else opt.step(grads)
+        torch.cuda.synchronize()
+        return [p.cpu().numpy() for p in opt.params()]
+
+    for a, b in zip(run(True), run(False)):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("world,group", [(2, 2), (4, 2), (4, 4)])
+def test_reduced_gradients_match_mean_gradient_step(cuda_device, world, group):
+    """Ranks with DIFFERENT local gradients, reduced to the block owners (simulated on one GPU: the
+    packed buffers are summed as the reduce-scatter / cross-group all-reduce would), must follow the
+    single-process trajectory driven by the mean gradient (the DDP all-reduce the reduce-scatter
+    replaces), and stay bit-identical replicas."""
+    name = "adagrad_nesterov"
+    cfg = config_from_meta(name, precondition_frequency=1)
+    shapes = [tuple(s) for s in META["configs"][name]["shapes"]]
+    init = [TRAJ[f"{name}/init/{i}"].astype(np.float64) for i in range(len(shapes))]
+    rng = np.random.default_rng(7)
+    local = [[[rng.standard_normal(s) * 0.1 for s in shapes] for _ in range(world)] for _ in range(3)]
+
+    ref = P.Shampoo([torch.as_tensor(x, device=cuda_device) for x in init], cfg)
+    opts = [P.Shampoo([torch.as_tensor(x, device=cuda_device) for x in init], cfg, world_size=world,
+                      group_size=group, rank=r) for r in range(world)]
+    for t in range(3):
+        mean = [sum(torch.as_tensor(local[t][r][i], device=cuda_device) for r in range(world)) / world
+                for i in range(len(shapes))]
+        ref.step(mean)
+        bufs = [o.pack_local_gradients([torch.as_tensor(g, device=cuda_device) for g in local[t][r]])
+                for r, o in enumerate(opts)]
+        total = sum(b.clone() for b in bufs)
+        for o, b in zip(opts, bufs):
+            b.copy_(total)
+            o.compute_directions_from_buffer(1.0 / world)
+        for g0 in range(0, world, group):
+            grp = opts[g0:g0 + group]
+            mp = grp[0].max_payload
+            full = torch.cat([o.gather_buffer[o.group_rank * mp:(o.group_rank + 1) * mp] for o in grp])
+            for o in grp:
+                o.gather_buffer[: group * mp].copy_(full)
+        for o in opts:
+            o.apply_gathered()
+            o.advance_step()
+    torch.cuda.synchronize()
+    want = [p.cpu().numpy() for p in ref.params()]
+    for o in opts:
+        for a, b in zip(o.params(), want):
+            assert rel(a.cpu().numpy(), b) <= 1e-12
+    for o in opts[1:]:
+        for a, b in zip(o.params(), opts[0].params()):
+            assert torch.equal(a, b)
+
+
+def test_reduced_nonfinite_aborts_without_mutation(cuda_device):
+    shapes = [(6, 5), (7,)]
+    rng = np.random.default_rng(1)
+    opt = P.Shampoo([torch.as_tensor(rng.standard_normal(s), device=cuda_device) for s in shapes],
+                    P.ShampooConfig(precondition_frequency=1, max_preconditioner_dim=8))
+    before = opt.state_tree()
+    w0 = [p.clone() for p in opt.params()]
+    bad = [torch.as_tensor(rng.standard_normal(s), device=cuda_device) for s in shapes]
+    bad[1][3] = float("nan")
+    with pytest.raises(P.NonFiniteGradientError):
+        opt.step_local(bad)
+    assert all(torch.equal(a, b) for a, b in zip(opt.params(), w0))
+    after = opt.state_tree()
+    assert after["t"] == before["t"]
