@@ -81,6 +81,29 @@ __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict
   }
 }
 
+// Rank-1 symmetric update C = beta C + alpha x x^T of a contiguous row-major C (the factor EMA of
+// a vector block, precond.py:232-242): CTA per (problem, row), 16-byte vector accesses.  The
+// full square is computed (x_i x_j == x_j x_i exactly): C stays bitwise symmetric.
+template <typename T>
+__global__ void __launch_bounds__(256) k_thin_rank1(const GemmProblem* __restrict__ probs,
+                                                    const int64_t* __restrict__ begin, int nprob,
+                                                    const int32_t* __restrict__ mask) {
+  const int p = find64(begin, nprob, blockIdx.x);
+  const GemmProblem& P = probs[p];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  const int i = (int)(blockIdx.x - begin[p]);
+  const T* __restrict__ x = static_cast<const T*>(P.A);
+  T* __restrict__ row = static_cast<T*>(P.C) + (int64_t)i * P.N;
+  const double xi = (double)x[ev(P.a_r, i)];
+  const bool readc = (P.flags & kGemmReadC) != 0;
+  const int64_t step = P.a_r.lo;
+  for (int j = threadIdx.x; j < P.N; j += blockDim.x) {
+    double v = P.alpha * (xi * (double)x[j * step]);
+    if (readc) v = fma(P.beta, (double)row[j], v);
+    row[j] = (T)v;
+  }
+}
+
 // Small M and N (<= 8), any K: CTA per (problem, 4096-wide k chunk) -> FP64 partials.
 template <typename T>
 __global__ void __launch_bounds__(256) k_thin_kred(const GemmProblem* __restrict__ probs,
@@ -148,8 +171,16 @@ __global__ void k_thin_kred_final(const GemmProblem* __restrict__ probs, int npr
 
 bool ThinGemmBatch_accepts(const GemmProblem& p) { return p.K <= 32 || (p.M <= TMAX && p.N <= TMAX); }
 
+// x x^T with x contiguous (stride a_r.lo), C row-major contiguous: the vector-block factor update
+static bool is_rank1(const GemmProblem& p) {
+  return p.K == 1 && (p.flags & kGemmSym) && p.A == p.B && p.M == p.N && p.a_r.div == 0x7fffffff &&
+         p.c_r.div == 0x7fffffff && p.c_c.div == 0x7fffffff && p.c_r.lo == p.N && p.c_c.lo == 1;
+}
+
 template <typename T>
 ThinGemmBatch<T>::~ThinGemmBatch() {
+  cudaFree(d_r1_);
+  cudaFree(d_r1begin_);
   cudaFree(d_out_);
   cudaFree(d_obegin_);
   cudaFree(d_red_);
@@ -161,8 +192,21 @@ ThinGemmBatch<T>::~ThinGemmBatch() {
 
 template <typename T>
 int ThinGemmBatch<T>::upload() {
-  std::vector<GemmProblem> outp, redp;
-  for (const auto& p : host) (p.K <= 32 ? outp : redp).push_back(p);
+  std::vector<GemmProblem> outp, redp, r1p;
+  for (const auto& p : host) (is_rank1(p) ? r1p : p.K <= 32 ? outp : redp).push_back(p);
+  std::vector<int64_t> r1b;
+  n_r1_ctas_ = 0;
+  for (const auto& p : r1p) {
+    r1b.push_back(n_r1_ctas_);
+    n_r1_ctas_ += p.M;
+  }
+  n_r1_ = (int)r1p.size();
+  if (n_r1_) {
+    SH_CUDA_CHECK(cudaMalloc(&d_r1_, r1p.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(cudaMalloc(&d_r1begin_, r1b.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMemcpy(d_r1_, r1p.data(), r1p.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(d_r1begin_, r1b.data(), r1b.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
   std::vector<int64_t> ob, rb, wo;
   std::vector<int32_t> nch;
   n_out_items_ = 0;  // CTAs
@@ -205,6 +249,10 @@ int ThinGemmBatch<T>::upload() {
 
 template <typename T>
 int ThinGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
+  if (n_r1_) {
+    k_thin_rank1<T><<<(unsigned)n_r1_ctas_, 256, 0, s>>>(d_r1_, d_r1begin_, n_r1_, mask);
+    SH_LAUNCH_CHECK();
+  }
   if (n_out_) {
     k_thin_kout<T><<<(unsigned)n_out_items_, 256, 0, s>>>(d_out_, d_obegin_, n_out_, mask);
     SH_LAUNCH_CHECK();

@@ -1,6 +1,6 @@
 // Thin problems of the grouped GEMM phases: a dimension too small for a 128 x 64 tensor-core tile.
-//   K <= 32          (rank-1 factor updates of vector blocks, 3x3 / 7x7 kernel-mode products):
-//                    one thread per output element;
+//   rank-1 SYRK      (factor updates of vector blocks): CTA per row, contiguous vector accesses;
+//   K <= 32          (3x3 / 7x7 kernel-mode products): one thread per output element;
 //   M, N <= 8        (factors of 3x3 / 7x7 kernel modes, K up to 786k): CTA per 4096-wide k
 //                    chunk, FP64 partials reduced in chunk order.
 // Both are HBM-bound; products are exact and sums FP64 (deterministic), for float or double
@@ -29,6 +29,10 @@ class ThinGemmBatch {
   double flops() const;
 
  private:
+  GemmProblem* d_r1_ = nullptr;      // rank-1 symmetric updates (vector-block factors)
+  int64_t* d_r1begin_ = nullptr;
+  int64_t n_r1_ctas_ = 0;
+  int n_r1_ = 0;
   GemmProblem* d_out_ = nullptr;
   int64_t* d_obegin_ = nullptr;
   GemmProblem* d_red_ = nullptr;
