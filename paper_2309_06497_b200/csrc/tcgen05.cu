@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
                                                             const int32_t* __restrict__ exps, double* __restrict__ ws) {
   using Cfg = OzCfg<S>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
-  __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES], empty_bar[Cfg::STAGES], done_bar;
+  // per stage two "full" barriers: [0] all B slices + the first half of the A slices, [1] the rest of
+  // A, so the MMAs of the first A slices overlap the tail of the stage's copies
+  __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES][2], empty_bar[Cfg::STAGES], done_bar;
   __shared__ uint32_t tmem_slot;
   __shared__ double col_scale[TN];
   __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
@@ -281,7 +283,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&full_bar[i][0], 1);
+      mbar_init(&full_bar[i][1], 1);
       mbar_init(&empty_bar[i], 1);
     }
     mbar_init(&done_bar, 1);
@@ -309,14 +312,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
         const uint32_t use = (uint32_t)(it / Cfg::STAGES);
         if (it >= Cfg::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
         uint8_t* sb = sbase + (size_t)st * Cfg::STAGE;
-        mbar_expect_tx(&full_bar[st], (uint32_t)S * (a_bytes + b_bytes));
+        constexpr int SH = (S + 1) / 2;  // A slices in the first half
+        mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
+        mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
         const int8_t* as = a_src + (int64_t)it * S * a_plane;
         const int8_t* bs = b_src + (int64_t)it * S * b_plane;
 #pragma unroll
         for (int q = 0; q < S; ++q) {
-          bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st]);
-          bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st]);
+          bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st][0]);
+          if (q < SH) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][0]);
         }
+#pragma unroll
+        for (int q = SH; q < S; ++q) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][1]);
       }
     }
   } else if (warp == 1) {
@@ -326,12 +333,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
       // d = sa + sb.  N <= 256 per instruction (one MMA per A slice for TN = 32).
       for (int it = 0; it < nk; ++it) {
         const int st = it % Cfg::STAGES;
-        mbar_wait(&full_bar[st], (uint32_t)(it / Cfg::STAGES) & 1u);
+        const uint32_t par = (uint32_t)(it / Cfg::STAGES) & 1u;
+        mbar_wait(&full_bar[st][0], par);
         tc_fence_after();
         const uint32_t sa_base = smem_u32(sbase + (size_t)st * Cfg::STAGE);
         const uint32_t sb_base = sa_base + Cfg::A_BYTES;
 #pragma unroll
         for (int sa = 0; sa < S; ++sa) {
+          if (sa == (S + 1) / 2) {
+            mbar_wait(&full_bar[st][1], par);
+            tc_fence_after();
+          }
           const uint64_t ad = sdesc(sa_base + sa * (TM / 8) * 256, 128, 256);
 #pragma unroll
           for (int sb0 = 0; sb0 < S - sa; sb0 += SL_PER_MMA) {
