@@ -680,10 +680,19 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   if (njobs == 0) return SHAMPOO_OK;
   const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
   PhaseScope scope(&c->timer, 1, s);
-  std::vector<int32_t> has_prev[kRootGroups];
+  std::vector<int32_t> has_prev[kRootGroups], full_rank[kRootGroups];
   for (int g = 0; g < kRootGroups; ++g) {
     has_prev[g].resize(c->rinv[g].jobs());
-    for (size_t j = 0; j < has_prev[g].size(); ++j) has_prev[g][j] = c->ready_h[c->job_block[g][j]];
+    full_rank[g].resize(c->rinv[g].jobs());
+    for (size_t j = 0; j < has_prev[g].size(); ++j) {
+      const int l = c->job_block[g][j];
+      has_prev[g][j] = c->ready_h[l];
+      // structural rank of the factor: `step` accumulated Gram terms of rank numel/d each; only a
+      // possibly full-rank factor is worth the Newton pre-pass of the eigh path
+      const int64_t d = c->rinv[g].job_n((int)j);
+      const int64_t numel = c->plan.blocks[c->owned[l]].var_count;
+      full_rank[g][j] = (int64_t)c->step[l] * (numel / std::max<int64_t>(d, 1)) >= d ? 1 : 0;
+    }
   }
   // group g > 0 on side stream g (after everything already queued on s), group 0 on s
   SH_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
@@ -693,7 +702,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   auto solve = [&](int g, cudaStream_t st) {
     if (c->rinv[g].jobs() == 0) return;
     grc[g] = c->rinv[g].run(1.0 / corr, has_prev[g], k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance,
-                            st, gstats[g], nullptr, nullptr, /*allow_warm=*/true);
+                            st, gstats[g], nullptr, nullptr, /*allow_warm=*/true, &full_rank[g]);
     if (grc[g]) gerr[g] = shampoo_last_error();
   };
   std::vector<std::thread> threads;

@@ -31,6 +31,11 @@ constexpr int LDS_ = NS + 1;      // padded smem leading dim
 constexpr int SLOT = 2 * NS * NS + NS + 2;  // U (64x64) + S (64x64) + D (64) + flag
 constexpr int ECH = 4096;         // elements per chunk for elementwise job kernels
 constexpr int MAX_SWEEPS = 40;
+// eigh Newton pre-pass: well-conditioned factors reach ||M - I||_inf ~ 1e-15 in 8-12 iterations
+// (error vs eigh ~ 3e-15); the budget bounds the time spent on factors that need the Jacobi path
+constexpr double kHybridNewtonTol = 1e-12;
+constexpr double kHybridNewtonTolN = 4e-15;  // residual floor grows ~ n u (row sums of n rounded entries)
+constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi sweeps (Jacobi: 10-16 sweeps)
 
 constexpr double U64 = 1.1102230246251565e-16;
 
@@ -1002,7 +1007,7 @@ __global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ j
   __shared__ double red[32];
   const int j = blockIdx.x;
   const RootJob& J = jobs[j];
-  if (st[j].status != kEigOk) {
+  if (st[j].status != kEigOk || st[j].via_newton) {  // (Newton pre-pass jobs already hold X)
     if (threadIdx.x == 0) mask[j] = 0;
     return;
   }
@@ -1113,24 +1118,17 @@ __global__ void k_count(const RootJob* __restrict__ jobs, RootState* st, int njo
 
 // ---------------------------------------------------------------- coupled Newton
 
-// Per job scratch at nx + n2_off: X0, X1, M0, M1, T, Pa, Pb, Xbest (8 n^2).
-struct NewtonJob {
-  int32_t n, p;
-  int64_t off;
-  double best;
-  int32_t iters, converged;
-};
 
 __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__ jobs, RootState* st,
                                                      NewtonJob* nj, int32_t* mask,
                                                      const int32_t* __restrict__ ebegin, int njobs,
                                                      const double* __restrict__ ws, double* __restrict__ nx,
-                                                     double eps, int phase) {
-  // phase 0: after k_init (norm2 of A known) compute c; phase 1: fill X0, M0, Xbest
+                                                     double eps, const int32_t* __restrict__ cand) {
+  // after k_init (||A||, tr A known): c, X0 = I/c, M0 = (A + eps I)/c^p, Xbest; cand: jobs to run (null: all)
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   NewtonJob& N = nj[j];
-  if (st[j].status != kEigOk) {
+  if (st[j].status != kEigOk || (cand && !cand[j])) {
     if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) mask[j] = 0;
     return;
   }
@@ -1193,69 +1191,86 @@ __global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ 
   }
 }
 
-// residual = max row sum |M_next - I|; best tracking; convergence (one CTA per job)
-__global__ void __launch_bounds__(256) k_newton_res(NewtonJob* nj, int32_t* mask, int njobs,
-                                                    double* __restrict__ nx, int nxt, double tol,
-                                                    int32_t* count) {
-  __shared__ double red[32];
-  __shared__ int improved;
-  const int j = blockIdx.x;
+// Residual ||M_next - I||_inf, part 1: a warp per row over the job's element chunks, row sums
+// max-reduced into resbits[j] (non-negative doubles order like their bit patterns; NaN > inf).
+__global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restrict__ nj,
+                                                       const int32_t* __restrict__ mask,
+                                                       const int32_t* __restrict__ ebegin, int njobs, int echunks,
+                                                       const double* __restrict__ nx, int nxt,
+                                                       unsigned long long* resbits) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  NewtonJob& N = nj[j];
+  const NewtonJob& N = nj[j];
   const int n = N.n;
-  const int64_t tot = (int64_t)n * n;
-  const double* M = nx + N.off + (2 + nxt) * tot;
-  double rmax = 0.0;
-  int bad = 0;
-  for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
-    double s = 0;
-    for (int k = threadIdx.x & 31; k < n; k += 32) s += fabs(M[(int64_t)i * n + k] - (i == k ? 1.0 : 0.0));
-    s = warp_sum(s);
-    if (!isfinite(s)) bad = 1;
-    rmax = fmax(rmax, s);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rmax;
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
-    double r = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
-    N.iters += 1;
-    improved = 0;
-    if (bad || !isfinite(r)) {
-      mask[j] = 0;  // diverged: keep best iterate, not converged
-    } else {
-      if (r < N.best) {
-        N.best = r;
-        improved = 1;
-      }
-      if (r < tol) {
-        N.converged = 1;
-        mask[j] = 0;
-      } else if (N.iters >= 1000) {
-        mask[j] = 0;
-      }
+  const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
+  const int rows_per = (n + nch - 1) / nch;
+  const int r0 = (blockIdx.x - ebegin[j]) * rows_per;
+  const double* M = nx + N.off + (int64_t)(2 + nxt) * n * n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
+    double sum = 0.0;
+    for (int k = lane; k < n; k += 32) sum += fabs(M[(int64_t)i * n + k] - (i == k ? 1.0 : 0.0));
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      const unsigned long long b = isnan(sum) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(sum);
+      atomicMax(resbits + j, b);
     }
   }
-  __syncthreads();
-  if (improved) {
-    const double* X = nx + N.off + nxt * tot;
-    double* XB = nx + N.off + 7 * tot;
-    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) XB[e] = X[e];
+}
+
+// Residual part 2 (thread per job): best-iterate tracking and the stopping rule r < max(tol, tol_n n).
+__global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int njobs, unsigned long long* resbits, double tol,
+                               double tol_n, int32_t* improved, int32_t* count) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs) return;
+  improved[j] = 0;
+  if (!mask[j]) return;
+  NewtonJob& N = nj[j];
+  const double r = __longlong_as_double((long long)resbits[j]);
+  resbits[j] = 0ull;
+  N.iters += 1;
+  if (!isfinite(r)) {
+    mask[j] = 0;  // diverged: keep the best iterate, not converged
+    return;
   }
-  if (threadIdx.x == 0 && mask[j]) atomicAdd(count, 1);
+  if (r < N.best) {
+    N.best = r;
+    improved[j] = 1;
+  }
+  if (r < fmax(tol, tol_n * N.n)) {
+    N.converged = 1;
+    mask[j] = 0;
+  } else if (N.iters >= 1000) {
+    mask[j] = 0;
+  }
+  if (mask[j]) atomicAdd(count, 1);
+}
+
+// Xbest <- X_next for the jobs whose residual improved.
+__global__ void __launch_bounds__(256) k_newton_copybest(const NewtonJob* __restrict__ nj,
+                                                         const int32_t* __restrict__ improved,
+                                                         const int32_t* __restrict__ ebegin, int njobs,
+                                                         double* __restrict__ nx, int nxt) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!improved[j]) return;
+  const NewtonJob& N = nj[j];
+  const int64_t tot = (int64_t)N.n * N.n;
+  const double* X = nx + N.off + nxt * tot;
+  double* XB = nx + N.off + 7 * tot;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) XB[e] = X[e];
 }
 
 // X = sym(Xbest) into the V workspace (contiguous n x n); status from convergence.
 __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict__ jobs, RootState* st,
                                                        const NewtonJob* __restrict__ nj,
                                                        const int32_t* __restrict__ ebegin, int njobs,
-                                                       const double* __restrict__ nx, double* __restrict__ xs) {
+                                                       const double* __restrict__ nx, double* __restrict__ xs,
+                                                       const int32_t* __restrict__ cand, int only_converged) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   const NewtonJob& N = nj[j];
-  if (st[j].status != kEigOk) return;
+  if (st[j].status != kEigOk || (cand && !cand[j]) || (only_converged && !N.converged)) return;
   const int n = J.n;
   const int64_t tot = (int64_t)n * n;
   const double* XB = nx + N.off + 7 * tot;
@@ -1266,11 +1281,28 @@ __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict
   }
 }
 
-__global__ void k_newton_status(RootState* st, const NewtonJob* __restrict__ nj, int njobs) {
+// solver NEWTON: non-converged -> NoConvergence (guard).  Hybrid eigh pre-pass (cand != null):
+// converged candidates are finished (via_newton, inactive for the Jacobi rounds), the rest stay.
+__global__ void k_newton_status(RootState* st, const NewtonJob* __restrict__ nj, int njobs,
+                                const int32_t* __restrict__ cand) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= njobs) return;
+  if (cand) {
+    if (cand[j] && st[j].status == kEigOk && nj[j].converged) {
+      st[j].via_newton = 1;
+      st[j].active = 0;
+      st[j].sweep = nj[j].iters;
+    }
+    return;
+  }
   if (st[j].status == kEigOk && !nj[j].converged) st[j].status = kEigNoConvergence;
   st[j].sweep = nj[j].iters;
+}
+
+// eigen-path mask: status ok and not already solved by the Newton pre-pass
+__global__ void k_mask_eig(const RootState* __restrict__ st, int32_t* mask, int njobs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < njobs) mask[j] = st[j].status == kEigOk && !st[j].via_newton;
 }
 
 }  // namespace
@@ -1324,6 +1356,10 @@ RootInverseBatch::~RootInverseBatch() {
   cudaFree(xs_);
   cudaFree(ts_);
   cudaFree(d_warm_);
+  cudaFree(d_cand_);
+  cudaFree(d_newton_);
+  cudaFree(d_resbits_);
+  cudaFree(d_improved_);
   cudaFree(d_pair_begin_);
   cudaFree(d_item_begin_);
   cudaFree(d_elem_begin_);
@@ -1403,6 +1439,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   SH_CUDA_CHECK(cudaMalloc(&us_, std::max<int64_t>(u_elems_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMalloc(&wv_, std::max<int64_t>(w_elems_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMalloc(&d_warm_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMalloc(&d_cand_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_pair_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_item_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMalloc(&d_elem_begin_, nj * sizeof(int32_t)));
@@ -1437,6 +1474,8 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     mixed_ = env ? std::atoi(env) != 0 : false;  // measured: no net gain with SIMT FP32 rounds
     const char* cr = std::getenv("SHAMPOO_EIG_CROSS");
     cross_only_ = cr ? std::atoi(cr) != 0 : true;
+    const char* nw = std::getenv("SHAMPOO_EIG_NEWTON");
+    hybrid_ = nw ? std::atoi(nw) != 0 : true;
   }
   if (mixed_ && has_big_) {
     SH_CUDA_CHECK(cudaMalloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
@@ -1593,7 +1632,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
   }
   (void)iters;
   prof_mark("fp64_rounds");
-  k_mask_ok<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
+  k_mask_eig<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, nj);
   SH_LAUNCH_CHECK();
   int rc = rr_.launch(s, mask);  // T = A0 V
   if (rc) return rc;
@@ -1606,9 +1645,39 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
   return recon_.launch(s, mask);
 }
 
-int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters) {
+// T^p by binary powering over the scratch buffers T, Pa, Pb: (lhs, rhs, dst) steps and the result.
+namespace {
+enum NBuf { kNT = 4, kNPa = 5, kNPb = 6 };
+struct PowStep {
+  int lhs, rhs, dst;
+};
+std::vector<PowStep> power_plan(int p, int* final_buf) {
+  std::vector<PowStep> v;
+  switch (p) {
+    case 1: *final_buf = kNT; break;
+    case 2: v = {{kNT, kNT, kNPa}}; *final_buf = kNPa; break;
+    case 3: v = {{kNT, kNT, kNPa}, {kNPa, kNT, kNPb}}; *final_buf = kNPb; break;
+    case 4: v = {{kNT, kNT, kNPa}, {kNPa, kNPa, kNPb}}; *final_buf = kNPb; break;
+    case 5: v = {{kNT, kNT, kNPa}, {kNPa, kNPa, kNPb}, {kNPb, kNT, kNPa}}; *final_buf = kNPa; break;
+    case 6: v = {{kNT, kNT, kNPa}, {kNPa, kNT, kNPb}, {kNPb, kNPb, kNPa}}; *final_buf = kNPa; break;
+    case 8: v = {{kNT, kNT, kNPa}, {kNPa, kNPa, kNPb}, {kNPb, kNPb, kNPa}}; *final_buf = kNPa; break;
+    default: {  // plain chain P_q = P_{q-1} T
+      int prev = kNT;
+      for (int q = 2; q <= p; ++q) {
+        const int dst = (q & 1) ? kNPb : kNPa;
+        v.push_back({prev, kNT, dst});
+        prev = dst;
+      }
+      *final_buf = prev;
+    }
+  }
+  return v;
+}
+}  // namespace
+
+int RootInverseBatch::build_newton() {
+  if (newton_built_) return SHAMPOO_OK;
   const int nj = (int)host_.size();
-  int32_t* mask = d_count_ + 4;
   if (!nx_) SH_CUDA_CHECK(cudaMalloc(&nx_, std::max<int64_t>(n2_elems_, 1) * sizeof(double)));
   std::vector<NewtonJob> hn(nj);
   for (int j = 0; j < nj; ++j) {
@@ -1616,88 +1685,117 @@ int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::ve
     hn[j].p = host_[j].root_p;
     hn[j].off = n2_off_[j];
   }
-  NewtonJob* dn = nullptr;
-  SH_CUDA_CHECK(cudaMalloc(&dn, nj * sizeof(NewtonJob)));
-  SH_CUDA_CHECK(cudaMemcpyAsync(dn, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice, s));
-  k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, 0);
-  SH_LAUNCH_CHECK();
-  // GEMM sets for cur = 0/1: X_nxt = X_cur T ; powers ; M_nxt = T^p M_cur
-  int maxp = 1;
-  for (const auto& J : host_) maxp = std::max(maxp, J.root_p);
-  OzakiGemmBatch<double> xstep[2], mstep[2];
-  // power chain, step q: P_q = P_{q-1} T
-  std::vector<std::unique_ptr<OzakiGemmBatch<double>>> powers(std::max(0, maxp - 1));
-  for (auto& p : powers) p.reset(new OzakiGemmBatch<double>());
+  SH_CUDA_CHECK(cudaMalloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
+  SH_CUDA_CHECK(cudaMalloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
+  SH_CUDA_CHECK(cudaMemset(d_resbits_, 0, std::max(nj, 1) * sizeof(unsigned long long)));
+  SH_CUDA_CHECK(cudaMalloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(cudaMemcpy(d_newton_, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice));
+  // GEMM sets for cur = 0/1: X_nxt = X_cur T ; T^p ; M_nxt = T^p M_cur (tcgen05 Ozaki, FP64 class)
+  size_t nsteps = 0;
   for (int j = 0; j < nj; ++j) {
-    const int n = host_[j].n, p = host_[j].root_p;
+    int fb;
+    nsteps = std::max(nsteps, power_plan(host_[j].root_p, &fb).size());
+  }
+  newton_pow_.clear();
+  for (size_t q = 0; q < nsteps; ++q) newton_pow_.emplace_back(new OzakiGemmBatch<double>());
+  for (int j = 0; j < nj; ++j) {
+    const int n = host_[j].n;
     const int64_t tot = (int64_t)n * n;
     double* base = nx_ + n2_off_[j];
-    double *X[2] = {base, base + tot}, *M[2] = {base + 2 * tot, base + 3 * tot};
-    double *T = base + 4 * tot, *Pab[2] = {base + 5 * tot, base + 6 * tot};
-    // power chain result location: p==1 -> T ; else Pab[(p-2)&1]
-    double* Pfinal = (p == 1) ? T : Pab[(p - 2) & 1];
+    auto buf = [&](int k) { return base + k * tot; };
+    int fb;
+    const std::vector<PowStep> plan = power_plan(host_[j].root_p, &fb);
     for (int c = 0; c < 2; ++c) {
-      GemmProblem g = make_gemm(false, false, n, n, n, X[c], n, T, n, X[c ^ 1], n, 1.0, 0.0);
+      GemmProblem g = make_gemm(false, false, n, n, n, buf(c), n, buf(kNT), n, buf(c ^ 1), n, 1.0, 0.0);
       g.flags |= kGemmMasked;
       g.mask_index = j;
-      xstep[c].add(g);
-      g = make_gemm(false, false, n, n, n, Pfinal, n, M[c], n, M[c ^ 1], n, 1.0, 0.0);
+      newton_x_[c].add(g);
+      g = make_gemm(false, false, n, n, n, buf(fb), n, buf(2 + c), n, buf(2 + (c ^ 1)), n, 1.0, 0.0);
       g.flags |= kGemmMasked;
       g.mask_index = j;
-      mstep[c].add(g);
+      newton_m_[c].add(g);
     }
-    for (int q = 2; q <= p; ++q) {
-      const double* prev = (q == 2) ? T : Pab[(q - 3) & 1];
-      GemmProblem g = make_gemm(false, false, n, n, n, prev, n, T, n, Pab[(q - 2) & 1], n, 1.0, 0.0);
+    for (size_t q = 0; q < plan.size(); ++q) {
+      GemmProblem g = make_gemm(false, false, n, n, n, buf(plan[q].lhs), n, buf(plan[q].rhs), n, buf(plan[q].dst), n,
+                                1.0, 0.0);
       g.flags |= kGemmMasked;
       g.mask_index = j;
-      powers[q - 2]->add(g);
+      newton_pow_[q]->add(g);
     }
   }
   int rc;
   for (int c = 0; c < 2; ++c) {
-    if ((rc = xstep[c].upload())) return rc;
-    if ((rc = mstep[c].upload())) return rc;
+    if ((rc = newton_x_[c].upload())) return rc;
+    if ((rc = newton_m_[c].upload())) return rc;
   }
-  for (auto& p : powers)
+  for (auto& p : newton_pow_)
     if ((rc = p->upload())) return rc;
+  newton_built_ = true;
+  return SHAMPOO_OK;
+}
+
+// Coupled Newton iterations (matfun.py:164-222) for the jobs in `cand` (null: all), at most
+// `budget` iterations, stopping rule ||M - I||_inf < tol.  hybrid: converged candidates are
+// finished (X into xs, via_newton), the others untouched (left to the Jacobi rounds).
+int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int32_t* cand, bool hybrid,
+                                   cudaStream_t s) {
+  const int nj = (int)host_.size();
+  int32_t* mask = d_count_ + 4;
+  int rc = build_newton();
+  if (rc) return rc;
+  NewtonJob* dn = d_newton_;
+  k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, cand);
+  SH_LAUNCH_CHECK();
   int cur = 0;
-  for (int it = 1; it <= 1000; ++it) {
+  for (int it = 1; it <= budget; ++it) {
     k_newton_t<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, nx_, cur);
     SH_LAUNCH_CHECK();
-    if ((rc = xstep[cur].launch(s, mask))) return rc;
-    for (auto& p : powers)
+    if ((rc = newton_x_[cur].launch(s, mask))) return rc;
+    for (auto& p : newton_pow_)
       if ((rc = p->launch(s, mask))) return rc;
-    if ((rc = mstep[cur].launch(s, mask))) return rc;
+    if ((rc = newton_m_[cur].launch(s, mask))) return rc;
     SH_CUDA_CHECK(cudaMemsetAsync(d_count_, 0, sizeof(int32_t), s));
-    k_newton_res<<<nj, 256, 0, s>>>(dn, mask, nj, nx_, cur ^ 1, tol, d_count_);
+    k_newton_rowmax<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, total_elem_chunks_, nx_, cur ^ 1,
+                                                       d_resbits_);
+    SH_LAUNCH_CHECK();
+    k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, nj, d_resbits_, tol, hybrid ? kHybridNewtonTolN : 0.0,
+                                                    d_improved_, d_count_);
+    SH_LAUNCH_CHECK();
+    k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
     SH_LAUNCH_CHECK();
     cur ^= 1;
-    if ((it & 3) == 0 || it < 4) {
+    if ((it & 3) == 0 || it < 4 || (hybrid && it >= 6)) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SH_CUDA_CHECK(cudaStreamSynchronize(s));
       if (h_count_[0] == 0) break;
     }
   }
-  k_newton_finish<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, xs_);
+  k_newton_finish<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, xs_, cand,
+                                                     hybrid ? 1 : 0);
   SH_LAUNCH_CHECK();
-  k_newton_status<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, dn, nj);
+  k_newton_status<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, dn, nj, hybrid ? cand : nullptr);
   SH_LAUNCH_CHECK();
-  SH_CUDA_CHECK(cudaStreamSynchronize(s));
-  cudaFree(dn);
-  (void)iters;
   return SHAMPOO_OK;
+}
+
+int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters) {
+  (void)iters;
+  return newton_phase(eps, tol, 1000, nullptr, false, s);
 }
 
 int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
                           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
-                          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm) {
+                          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm,
+                          const std::vector<int32_t>* newton_hint) {
   const int nj = (int)host_.size();
   if (nj == 0) return SHAMPOO_OK;
-  bool any_warm = false;
-  std::vector<int32_t> warm(nj, 0);
+  bool any_warm = false, any_cand = false;
+  std::vector<int32_t> warm(nj, 0), cand(nj, 0);
+  const bool hybrid = solver == SHAMPOO_SOLVER_EIGH && eta == 1.0 && hybrid_;
   for (int j = 0; j < nj; ++j) {
-    warm[j] = (allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j]) ? 1 : 0;
+    cand[j] = (hybrid && host_[j].m > 0 && (!newton_hint || (*newton_hint)[j])) ? 1 : 0;
+    any_cand |= cand[j] != 0;
+    warm[j] = (allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j] && !cand[j]) ? 1 : 0;
     host_[j].warm = warm[j];
     any_warm |= warm[j] != 0;
     host_[j].in_scale = in_scale;
@@ -1724,6 +1822,12 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     if (rw) return rw;
   }
   prof_mark("init+warm");
+  if (any_cand) {
+    SH_CUDA_CHECK(cudaMemcpyAsync(d_cand_, cand.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    int rn = newton_phase(eps, kHybridNewtonTol, kHybridNewtonBudget, d_cand_, true, s);
+    if (rn) return rn;
+    prof_mark("newton");
+  }
   if (solver == SHAMPOO_SOLVER_EIGH && mixed_ && has_big_) {
     int rm = run_mixed_phase(s, any_warm);
     if (rm) return rm;
@@ -1749,7 +1853,7 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   SH_CUDA_CHECK(cudaStreamSynchronize(s));
   SH_CUDA_CHECK(cudaFreeAsync(d_stats, s));
   for (int j = 0; j < nj; ++j) {
-    if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = hs[j].status == kEigOk ? 1 : 0;
+    if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = (hs[j].status == kEigOk && !hs[j].via_newton) ? 1 : 0;
     else vec_valid_[j] = 0;
     sweeps_total_ += hs[j].sweep + hs[j].sweep32;
   }
@@ -1760,7 +1864,9 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   if (host_iters) {
     host_iters->resize(nj);
     // eigh: FP64 sweeps + 1000 x FP32-phase sweeps (mixed precision); Newton: iterations
-    for (int j = 0; j < nj; ++j) (*host_iters)[j] = hs[j].sweep + 1000 * hs[j].sweep32;
+    // (jobs finished by the Newton pre-pass: 100000 + iterations)
+    for (int j = 0; j < nj; ++j)
+      (*host_iters)[j] = hs[j].via_newton ? 100000 + hs[j].sweep : hs[j].sweep + 1000 * hs[j].sweep32;
   }
   return SHAMPOO_OK;
 }

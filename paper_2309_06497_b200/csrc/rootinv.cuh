@@ -7,6 +7,7 @@
 // Jacobi solver; the Newton path uses the grouped DGEMM.
 #pragma once
 
+#include <memory>
 #include <vector>
 
 #include "gemm.cuh"
@@ -51,7 +52,16 @@ struct RootState {
   double tol_null;
   double trace;            // tr(A)
   int32_t nonfinite, capped;  // capped: sweep cap reached (result still used)
-  int32_t sweep32, pad;       // FP32-phase sweeps (mixed-precision eigensolver)
+  int32_t sweep32;            // FP32-phase sweeps (mixed-precision eigensolver)
+  int32_t via_newton;         // eigh job solved by the coupled-Newton pre-pass (no eigenvectors kept)
+};
+
+// Coupled-Newton job; per job scratch at nx + off: X0, X1, M0, M1, T, Pa, Pb, Xbest (8 n^2).
+struct NewtonJob {
+  int32_t n, p;
+  int64_t off;
+  double best;
+  int32_t iters, converged;
 };
 
 class RootInverseBatch {
@@ -64,18 +74,26 @@ class RootInverseBatch {
   int setup(const std::vector<int32_t>& n, const std::vector<int32_t>& root_p);
   void set_io(int j, const void* in, bool in_f32, void* out, bool out_f32);
   // Run on all jobs. scale: input multiplier; has_prev per job (host).
+  // eigh with eta = 1: jobs with n > 64 (and newton_hint[j] != 0 if given: the factor can be full
+  // rank) first try the coupled-Newton iteration to an FP64-level residual within a fixed budget --
+  // the same matrix function (lambda + eps)^(-1/p) when lambda_min >= 0 -- and only the
+  // non-converged ones run the Jacobi rounds.
   // stats[4] accumulates GuardStats branches; host_status receives per-job status.
   // allow_warm: start from eigenvectors of the previous successful run of the same job.
   int run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
-          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm = false);
+          std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm = false,
+          const std::vector<int32_t>* newton_hint = nullptr);
   int64_t sweeps_total() const { return sweeps_total_; }
   size_t jobs() const { return host_.size(); }
+  int32_t job_n(int j) const { return host_[j].n; }
   double work_n3() const;  // sum n^3
 
  private:
   int run_eigh(double eta, double eps, cudaStream_t s, std::vector<int32_t>* iters);
   int run_newton(double eps, double tol, cudaStream_t s, std::vector<int32_t>* iters);
+  int build_newton();
+  int newton_phase(double eps, double tol, int budget, const int32_t* cand, bool hybrid, cudaStream_t s);
   int prepare_warm(cudaStream_t s);
   int build_warm_gemms();
   int run_mixed_phase(cudaStream_t s, bool any_warm);
@@ -111,6 +129,16 @@ class RootInverseBatch {
   int64_t ws_elems_ = 0, u_elems_ = 0, w_elems_ = 0, n2_elems_ = 0;
   std::vector<int64_t> n2_off_;
   bool has_big_ = false;
+  // coupled Newton (solver NEWTON, and the eigh pre-pass for well-conditioned factors): persistent
+  // tcgen05 Ozaki GEMM sets X_nxt = X T, T^p (binary powering), M_nxt = T^p M
+  NewtonJob* d_newton_ = nullptr;
+  unsigned long long* d_resbits_ = nullptr;  // per job max row sum of |M - I| (bit pattern)
+  int32_t* d_improved_ = nullptr;
+  bool newton_built_ = false;
+  OzakiGemmBatch<double> newton_x_[2], newton_m_[2];
+  std::vector<std::unique_ptr<OzakiGemmBatch<double>>> newton_pow_;
+  int32_t* d_cand_ = nullptr;  // eigh jobs tried with the Newton pre-pass
+  bool hybrid_ = true;          // SHAMPOO_EIG_NEWTON=0 disables the pre-pass
   // reconstruction X = Y Y^T for all jobs (into xs_)
   OzakiGemmBatch<double> recon_;
   bool recon_ready_ = false;

@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const double t = y * 128.0;
-        const double q = trunc(t);   // |q| <= 127
+        // truncate, except the last slice rounds to nearest: the dropped remainder is then
+        // unbiased (+-2^-7S / 2 of the row maximum) instead of always shrinking |x|
+        const double q = (s + 1 < S) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
         y = t - q;                   // exact
         w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)q) << (8 * (i & 3));
       }

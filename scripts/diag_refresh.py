@@ -17,7 +17,7 @@ shapes = [tuple(s) for s in MODEL_SHAPES["resnet50"]]
 g = torch.Generator(device=dev); g.manual_seed(0)
 params = [torch.randn(s, generator=g, device=dev) * 0.05 for s in shapes]
 g.manual_seed(1)
-pool = [[torch.randn(s, generator=g, device=dev) * 1e-2 for s in shapes] for _ in range(4)]
+pool = [[torch.randn(s, generator=g, device=dev) * 1e-2 for s in shapes] for _ in range(T + 1)]  # fresh per step
 cfg = P.ShampooConfig(grafting=P.GraftKind.ADAGRAD, max_preconditioner_dim=2048, precondition_frequency=50,
                       betas=(0.0, 0.999), epsilon=1e-12, momentum=0.9, use_nesterov=True, weight_decay=1e-4,
                       use_decoupled_weight_decay=True)
@@ -27,7 +27,7 @@ lib.shampoo_timing_enable(opt._ctx, 1)
 ms = (C.c_double * 5)(); cnt = (C.c_int64 * 5)()
 for t in range(T + 1):
     lib.shampoo_timing_get(opt._ctx, None, None)
-    opt.step(pool[t % 4])
+    opt.step(pool[t])
     torch.cuda.synchronize()
     lib.shampoo_timing_get(opt._ctx, ms, cnt)
     if cnt[1]:
@@ -53,8 +53,14 @@ for p, mats in sorted(by_p.items()):
     hist = {}
     for m, s in zip(mats, sweeps):
         hist.setdefault(m.shape[0], []).append(s)
-    fmt = lambda v: f"{min(x // 1000 for x in v)}-{max(x // 1000 for x in v)}/{min(x % 1000 for x in v)}-{max(x % 1000 for x in v)}"
-    print(f"p={p}: {len(mats)} factors cold {dt*1e3:.1f} ms; sweeps fp32/fp64 by n: "
+    def fmt(v):
+        nw = [x - 100000 for x in v if x >= 100000]
+        jb = [x for x in v if x < 100000]
+        out = f"newton {len(nw)}" + (f" ({min(nw)}-{max(nw)} it)" if nw else "")
+        if jb:
+            out += f", jacobi {len(jb)} ({min(x % 1000 for x in jb)}-{max(x % 1000 for x in jb)} sw)"
+        return out
+    print(f"p={p}: {len(mats)} factors cold {dt*1e3:.1f} ms; solver by n: "
           + ", ".join(f"{n}:{fmt(v)}" for n, v in sorted(hist.items(), reverse=True)), flush=True)
 print(f"cold total {tot*1e3:.1f} ms")
 # per-size timing, one size at a time (cold)

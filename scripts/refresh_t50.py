@@ -9,17 +9,17 @@ shapes = [tuple(s) for s in MODEL_SHAPES["resnet50"]]
 g = torch.Generator(device=dev); g.manual_seed(0)
 params = [torch.randn(s, generator=g, device=dev) * 0.05 for s in shapes]
 g.manual_seed(1)
-pool = [[torch.randn(s, generator=g, device=dev) * 1e-2 for s in shapes] for _ in range(4)]
+T = int(sys.argv[1]) if len(sys.argv) > 1 else 51
+pool = [[torch.randn(s, generator=g, device=dev) * 1e-2 for s in shapes] for _ in range(T)]  # fresh per step
 cfg = P.ShampooConfig(grafting=P.GraftKind.ADAGRAD, max_preconditioner_dim=2048, precondition_frequency=50,
                       betas=(0.0, 0.999), epsilon=1e-12, momentum=0.9, use_nesterov=True, weight_decay=1e-4,
                       use_decoupled_weight_decay=True)
 opt = P.Shampoo(params, cfg)
-T = int(sys.argv[1]) if len(sys.argv) > 1 else 51
 for t in range(T):
     if t == T - 1:
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
-    opt.step(pool[t % 4])
+    opt.step(pool[t])
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 print("done", opt.guard_stats)
