@@ -10,6 +10,7 @@
 // chunk tables, independent of the number of blocks.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -19,6 +20,7 @@
 #include "gemm.cuh"
 #include "tcgen05.cuh"
 #include "thin.cuh"
+#include "lowrank.cuh"
 #include "rootinv.cuh"
 
 namespace shampoo {
@@ -29,6 +31,7 @@ namespace {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+constexpr int kLowRankMax = 128;  // factors of structural rank <= 128 (and <= d/2) take the low-rank path
 constexpr int kRootGroups = 2;  // measured: 2 -> 1234 ms, 4 -> 1221 ms per t=50 refresh (ResNet-50)
 
 struct EngineBase {
@@ -108,6 +111,7 @@ struct shampoo_ctx {
   shampoo_config cfg{};
   int32_t rank = 0, grank = 0, device = 0;
   bool f32 = false;
+  bool low_rank = true;  // low-rank root-inverse path (SHAMPOO_EIG_LOWRANK=0 disables)
   size_t esz = 8;
   int32_t nparams = 0;
   // owned blocks
@@ -561,6 +565,10 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     }
   }
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  {
+    const char* lr = std::getenv("SHAMPOO_EIG_LOWRANK");
+    c->low_rank = lr ? std::atoi(lr) != 0 : true;
+  }
   for (int g = 1; g < kRootGroups; ++g) {
     SH_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side[g], cudaStreamNonBlocking));
     SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join[g], cudaEventDisableTiming));
@@ -680,19 +688,41 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   if (njobs == 0) return SHAMPOO_OK;
   const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
   PhaseScope scope(&c->timer, 1, s);
-  std::vector<int32_t> has_prev[kRootGroups], full_rank[kRootGroups];
+  std::vector<int32_t> has_prev[kRootGroups], full_rank[kRootGroups], low_rank[kRootGroups];
+  std::vector<LowRankJob> lr_jobs;
   for (int g = 0; g < kRootGroups; ++g) {
     has_prev[g].resize(c->rinv[g].jobs());
     full_rank[g].resize(c->rinv[g].jobs());
+    low_rank[g].assign(c->rinv[g].jobs(), 0);
     for (size_t j = 0; j < has_prev[g].size(); ++j) {
       const int l = c->job_block[g][j];
       has_prev[g][j] = c->ready_h[l];
       // structural rank of the factor: `step` accumulated Gram terms of rank numel/d each; only a
-      // possibly full-rank factor is worth the Newton pre-pass of the eigh path
+      // possibly full-rank factor is worth the Newton pre-pass of the eigh path, and a factor of
+      // small rank r is solved through its r x r compression (lowrank.cuh)
       const int64_t d = c->rinv[g].job_n((int)j);
       const int64_t numel = c->plan.blocks[c->owned[l]].var_count;
-      full_rank[g][j] = (int64_t)c->step[l] * (numel / std::max<int64_t>(d, 1)) >= d ? 1 : 0;
+      const int64_t rank = (int64_t)c->step[l] * (numel / std::max<int64_t>(d, 1));
+      full_rank[g][j] = rank >= d ? 1 : 0;
+      if (k.solver == SHAMPOO_SOLVER_EIGH && k.epsilon > 0.0 && !c->f32 && d > 64 && rank <= kLowRankMax &&
+          2 * rank <= d && c->low_rank) {
+        low_rank[g][j] = 1;
+        LowRankJob L{};
+        L.d = (int32_t)d;
+        L.r = (int32_t)std::max<int64_t>(rank, 1);
+        L.root_p = c->rinv[g].job_p((int)j);
+        L.has_prev = c->ready_h[l];
+        L.in = static_cast<const double*>(c->rinv[g].job_in((int)j));
+        L.out = static_cast<double*>(c->rinv[g].job_out((int)j));
+        lr_jobs.push_back(L);
+      }
     }
+  }
+  if (!lr_jobs.empty()) {
+    int64_t lstats[4] = {0, 0, 0, 0};
+    int rl = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, s, lstats);
+    if (rl) return rl;
+    for (int q = 0; q < 4; ++q) c->guard[q] += lstats[q];
   }
   // group g > 0 on side stream g (after everything already queued on s), group 0 on s
   SH_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
@@ -702,7 +732,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   auto solve = [&](int g, cudaStream_t st) {
     if (c->rinv[g].jobs() == 0) return;
     grc[g] = c->rinv[g].run(1.0 / corr, has_prev[g], k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance,
-                            st, gstats[g], nullptr, nullptr, /*allow_warm=*/true, &full_rank[g]);
+                            st, gstats[g], nullptr, nullptr, /*allow_warm=*/true, &full_rank[g], &low_rank[g]);
     if (grc[g]) gerr[g] = shampoo_last_error();
   };
   std::vector<std::thread> threads;

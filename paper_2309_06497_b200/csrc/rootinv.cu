@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
   const bool ok = st[j].status == kEigOk;
-  if (!ok && J.has_prev) return;
+  if ((!ok && J.has_prev) || st[j].status == kEigSkipped) return;
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   const int64_t tot = (int64_t)J.n * J.n;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
@@ -1095,6 +1095,15 @@ __global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs
   }
 }
 
+// jobs handled by another path: status kEigSkipped, inactive, masked off
+__global__ void k_skip(RootState* st, int32_t* mask, const int32_t* __restrict__ skip, int njobs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= njobs || !skip[j]) return;
+  st[j].status = kEigSkipped;
+  st[j].active = 0;
+  mask[j] = 0;
+}
+
 __global__ void k_mask_ok(const RootState* __restrict__ st, int32_t* mask, int njobs) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < njobs) mask[j] = st[j].status == kEigOk;
@@ -1103,6 +1112,7 @@ __global__ void k_mask_ok(const RootState* __restrict__ st, int32_t* mask, int n
 __global__ void k_count(const RootJob* __restrict__ jobs, RootState* st, int njobs, int64_t* stats) {
   if (threadIdx.x != 0) return;
   for (int j = 0; j < njobs; ++j) {
+    if (st[j].status == kEigSkipped) continue;
     if (st[j].status == kEigOk) {
       st[j].result = 0;
       ++stats[0];
@@ -1786,16 +1796,19 @@ int RootInverseBatch::run_newton(double eps, double tol, cudaStream_t s, std::ve
 int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
                           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
                           std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm,
-                          const std::vector<int32_t>* newton_hint) {
+                          const std::vector<int32_t>* newton_hint, const std::vector<int32_t>* skip) {
   const int nj = (int)host_.size();
   if (nj == 0) return SHAMPOO_OK;
-  bool any_warm = false, any_cand = false;
+  bool any_warm = false, any_cand = false, any_skip = false;
   std::vector<int32_t> warm(nj, 0), cand(nj, 0);
   const bool hybrid = solver == SHAMPOO_SOLVER_EIGH && eta == 1.0 && hybrid_;
   for (int j = 0; j < nj; ++j) {
-    cand[j] = (hybrid && host_[j].m > 0 && (!newton_hint || (*newton_hint)[j])) ? 1 : 0;
+    const bool sk = skip && (*skip)[j];
+    any_skip |= sk;
+    cand[j] = (!sk && hybrid && host_[j].m > 0 && (!newton_hint || (*newton_hint)[j])) ? 1 : 0;
     any_cand |= cand[j] != 0;
-    warm[j] = (allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j] && !cand[j]) ? 1 : 0;
+    warm[j] = (!sk && allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j] && !cand[j]) ? 1
+                                                                                                              : 0;
     host_[j].warm = warm[j];
     any_warm |= warm[j] != 0;
     host_[j].in_scale = in_scale;
@@ -1816,6 +1829,11 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   int32_t* mask = d_count_ + 4;
   k_init_finish<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, mask, nj, eps);
   SH_LAUNCH_CHECK();
+  if (any_skip) {
+    SH_CUDA_CHECK(cudaMemcpyAsync(d_cand_, skip->data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    k_skip<<<(nj + 127) / 128, 128, 0, s>>>(d_state_, mask, d_cand_, nj);
+    SH_LAUNCH_CHECK();
+  }
   SH_CUDA_CHECK(cudaMemcpyAsync(d_warm_, warm.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   if (any_warm) {
     int rw = prepare_warm(s);

@@ -21,6 +21,7 @@ enum EigStatus : int32_t {
   kEigNoConvergence = 2,
   kEigEpsZeroSingular = 3,
   kEigNonFiniteResult = 4,
+  kEigSkipped = 5,  // solved elsewhere (low-rank path): untouched by this batch
 };
 
 // One matrix of a batch.
@@ -83,10 +84,13 @@ class RootInverseBatch {
   int run(double in_scale, const std::vector<int32_t>& has_prev, double eta, double eps,
           int32_t solver, double newton_tol, cudaStream_t s, int64_t* stats,
           std::vector<int32_t>* host_status, std::vector<int32_t>* host_iters, bool allow_warm = false,
-          const std::vector<int32_t>* newton_hint = nullptr);
+          const std::vector<int32_t>* newton_hint = nullptr, const std::vector<int32_t>* skip = nullptr);
   int64_t sweeps_total() const { return sweeps_total_; }
   size_t jobs() const { return host_.size(); }
   int32_t job_n(int j) const { return host_[j].n; }
+  int32_t job_p(int j) const { return host_[j].root_p; }
+  const void* job_in(int j) const { return host_[j].in; }
+  void* job_out(int j) const { return host_[j].out; }
   double work_n3() const;  // sum n^3
 
  private:
