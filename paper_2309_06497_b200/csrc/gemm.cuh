@@ -20,7 +20,7 @@
 namespace shampoo {
 
 enum GemmFlags : int32_t {
-  kGemmSym = 1,    // C symmetric and A==B: compute tiles tm >= tn, mirror-write the rest
+  kGemmSym = 1,    // C symmetric: compute tiles tm >= tn, mirror-write the rest (A==B except on the Ozaki path)
   kGemmReadC = 2,  // C = alpha*AB + beta*C (else beta ignored)
   kGemmMasked = 4, // skip unless mask[mask_index] != 0
   kGemmConstA = 8,  // operand A changes rarely (an inverse factor): tensor-core packs are cached

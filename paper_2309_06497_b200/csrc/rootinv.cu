@@ -17,7 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <string>
 
 #include "rootinv.cuh"
 
@@ -36,6 +38,13 @@ constexpr int MAX_SWEEPS = 40;
 constexpr double kHybridNewtonTol = 1e-12;
 constexpr double kHybridNewtonTolN = 4e-15;  // residual floor grows ~ n u (row sums of n rounded entries)
 constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi sweeps (Jacobi: 10-16 sweeps)
+// Conditioning gate of the pre-pass: the coupled iteration's forward error grows like C kappa u
+// (C ~ 10 measured on the golden rank-deficient cases), eigh's like kappa u / p.  The number of
+// iterations bounds kappa(A + eps I) from above: the smallest scaled eigenvalue grows by
+// ((p+1)/p)^p per linear-phase iteration, then ~5 quadratic ones.  Jobs that need more than
+// 5 + log(kappa_max) / (p log((p+1)/p)) iterations are left to the Jacobi path.
+constexpr double kHybridNewtonKappa = 5e6;
+constexpr int kPowerIters = 12;  // power-iteration steps for the pre-pass scaling (k_pow_*)
 
 constexpr double U64 = 1.1102230246251565e-16;
 
@@ -1129,11 +1138,80 @@ __global__ void k_count(const RootJob* __restrict__ jobs, RootState* st, int njo
 // ---------------------------------------------------------------- coupled Newton
 
 
+// Power iteration for lambda_max(A) of the hybrid pre-pass candidates (x, y in the free Pa slot).
+// The coupled iteration converges for a scaled spectrum inside (0, p + 1); the reference's
+// c^p = 2 ||A + eps I||_F / (p + 1) (matfun.py:190-198) guarantees that but overestimates
+// lambda_max by up to sqrt(n), which costs log(ratio) / (p log((p+1)/p)) extra iterations.  The
+// Rayleigh quotient after kPowerIters steps from a random start is within a few % below
+// lambda_max (its top-eigenvector weight grows like (lambda_1 / lambda_i)^(2k)); a divergent run
+// (scaled spectrum beyond p + 1) is caught by the residual check and handed to the Jacobi path.
+__global__ void __launch_bounds__(256) k_pow_start(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                   const NewtonJob* __restrict__ nj, const int32_t* __restrict__ ebegin,
+                                                   int njobs, double* __restrict__ nx, const int32_t* __restrict__ cand) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (st[j].status != kEigOk || (cand && !cand[j])) return;
+  const int n = jobs[j].n;
+  double* x = nx + nj[j].off + 5 * (int64_t)n * n;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < n; e += blockDim.x) {
+    uint64_t h = (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(j + 1) * 0xBF58476D1CE4E5B9ull;
+    h = (h ^ (h >> 31)) * 0x94D049BB133111EBull;
+    h ^= h >> 29;
+    x[e] = (double)(h >> 11) * 0x1.0p-52 - 1.0;  // uniform in [-1, 1)
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pow_mv(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                const NewtonJob* __restrict__ nj, const int32_t* __restrict__ ebegin,
+                                                int njobs, int echunks, const double* __restrict__ ws,
+                                                double* __restrict__ nx, const int32_t* __restrict__ cand) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (st[j].status != kEigOk || (cand && !cand[j])) return;
+  const RootJob& J = jobs[j];
+  const int n = J.n;
+  const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
+  const int rows_per = (n + nch - 1) / nch;
+  const int r0 = (blockIdx.x - ebegin[j]) * rows_per;
+  const double* A = ws + J.ws_off;
+  const double* x = nx + nj[j].off + 5 * (int64_t)n * n;
+  double* y = const_cast<double*>(x) + n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
+    double sum = 0.0;
+    for (int k = lane; k < n; k += 32) sum = fma(A[(int64_t)i * J.np + k], x[k], sum);
+    sum = warp_sum(sum);
+    if (lane == 0) y[i] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pow_norm(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                  NewtonJob* nj, double* __restrict__ nx,
+                                                  const int32_t* __restrict__ cand) {
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  if (st[j].status != kEigOk || (cand && !cand[j])) return;
+  const int n = jobs[j].n;
+  double* x = nx + nj[j].off + 5 * (int64_t)n * n;
+  const double* y = x + n;
+  double xx = 0.0, xy = 0.0, yy = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    xx = fma(x[i], x[i], xx);
+    xy = fma(x[i], y[i], xy);
+    yy = fma(y[i], y[i], yy);
+  }
+  xx = block_sum<double, 256>(xx, red);
+  xy = block_sum<double, 256>(xy, red);
+  yy = block_sum<double, 256>(yy, red);
+  if (threadIdx.x == 0) nj[j].lam = xx > 0.0 ? xy / xx : 0.0;
+  const double inv = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = y[i] * inv;
+}
+
 __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__ jobs, RootState* st,
                                                      NewtonJob* nj, int32_t* mask,
                                                      const int32_t* __restrict__ ebegin, int njobs,
                                                      const double* __restrict__ ws, double* __restrict__ nx,
-                                                     double eps, const int32_t* __restrict__ cand) {
+                                                     double eps, const int32_t* __restrict__ cand, int lam_scale) {
   // after k_init (||A||, tr A known): c, X0 = I/c, M0 = (A + eps I)/c^p, Xbest; cand: jobs to run (null: all)
   const int j = find_job(ebegin, njobs, blockIdx.x);
   const RootJob& J = jobs[j];
@@ -1167,7 +1245,10 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
   const double tr = st[j].trace;
   const double fro2 = st[j].norm2 + (eps > 0.0 ? 2.0 * eps * tr + n * eps * eps : 0.0);
   const int p = J.root_p;
-  const double c = pow(2.0 * sqrt(fro2) / (p + 1), 1.0 / p);
+  // reference scaling, or (hybrid) 1.05 x the power-iteration lambda_max(A + eps I) when usable
+  double cpow = 2.0 * sqrt(fro2) / (p + 1);
+  if (lam_scale && N.lam > 0.0 && isfinite(N.lam)) cpow = fmin(cpow * (p + 1) / 2.0, 1.05 * N.lam + eps);
+  const double c = pow(cpow, 1.0 / p);
   const double cp = pow(c, (double)p);
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     const int64_t i = e / n, k = e % n;
@@ -1250,7 +1331,7 @@ __global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int njobs, unsigned
   if (r < fmax(tol, tol_n * N.n)) {
     N.converged = 1;
     mask[j] = 0;
-  } else if (N.iters >= 1000) {
+  } else if (N.iters >= 1000 || (tol_n > 0.0 && N.iters >= N.cap)) {
     mask[j] = 0;
   }
   if (mask[j]) atomicAdd(count, 1);
@@ -1340,11 +1421,17 @@ struct EigProfile {
     if (!on || marks.empty()) return;
     cudaEventSynchronize(marks.back().second);
     std::fprintf(stderr, "[eig]");
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;  // repeated marks summed
     for (size_t i = 1; i < marks.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-      std::fprintf(stderr, " %s %.2f", marks[i].first, ms);
+      auto it = std::find_if(agg.begin(), agg.end(), [&](const auto& a) { return a.first == marks[i].first; });
+      if (it == agg.end()) agg.push_back({marks[i].first, {ms, 1}});
+      else it->second.first += ms, it->second.second += 1;
     }
+    for (const auto& a : agg)
+      if (a.second.second > 1) std::fprintf(stderr, " %s %.2f(x%d)", a.first.c_str(), a.second.first, a.second.second);
+      else std::fprintf(stderr, " %s %.2f", a.first.c_str(), a.second.first);
     std::fprintf(stderr, " ms\n");
     for (auto& m : marks) cudaEventDestroy(m.second);
   }
@@ -1694,6 +1781,10 @@ int RootInverseBatch::build_newton() {
     hn[j].n = host_[j].n;
     hn[j].p = host_[j].root_p;
     hn[j].off = n2_off_[j];
+    {
+      const double p = host_[j].root_p;
+      hn[j].cap = 5 + (int)std::ceil(std::log(kHybridNewtonKappa) / (p * std::log((p + 1.0) / p)));
+    }
   }
   SH_CUDA_CHECK(cudaMalloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
   SH_CUDA_CHECK(cudaMalloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
@@ -1715,23 +1806,21 @@ int RootInverseBatch::build_newton() {
     auto buf = [&](int k) { return base + k * tot; };
     int fb;
     const std::vector<PowStep> plan = power_plan(host_[j].root_p, &fb);
+    // every iterate is a polynomial in A (symmetric, mutually commuting), so each product is
+    // symmetric: B = B^T is read row-contiguous and only the lower tiles are computed, mirrored
+    // (the mirror also keeps the iterates exactly symmetric)
+    auto sym_gemm = [&](double* a, double* b, double* c) {
+      GemmProblem g = make_gemm(false, true, n, n, n, a, n, b, n, c, n, 1.0, 0.0);
+      g.flags |= kGemmMasked | kGemmSym;
+      g.mask_index = j;
+      return g;
+    };
     for (int c = 0; c < 2; ++c) {
-      GemmProblem g = make_gemm(false, false, n, n, n, buf(c), n, buf(kNT), n, buf(c ^ 1), n, 1.0, 0.0);
-      g.flags |= kGemmMasked;
-      g.mask_index = j;
-      newton_x_[c].add(g);
-      g = make_gemm(false, false, n, n, n, buf(fb), n, buf(2 + c), n, buf(2 + (c ^ 1)), n, 1.0, 0.0);
-      g.flags |= kGemmMasked;
-      g.mask_index = j;
-      newton_m_[c].add(g);
+      newton_x_[c].add(sym_gemm(buf(c), buf(kNT), buf(c ^ 1)));
+      newton_m_[c].add(sym_gemm(buf(fb), buf(2 + c), buf(2 + (c ^ 1))));
     }
-    for (size_t q = 0; q < plan.size(); ++q) {
-      GemmProblem g = make_gemm(false, false, n, n, n, buf(plan[q].lhs), n, buf(plan[q].rhs), n, buf(plan[q].dst), n,
-                                1.0, 0.0);
-      g.flags |= kGemmMasked;
-      g.mask_index = j;
-      newton_pow_[q]->add(g);
-    }
+    for (size_t q = 0; q < plan.size(); ++q)
+      newton_pow_[q]->add(sym_gemm(buf(plan[q].lhs), buf(plan[q].rhs), buf(plan[q].dst)));
   }
   int rc;
   for (int c = 0; c < 2; ++c) {
@@ -1754,16 +1843,34 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
   int rc = build_newton();
   if (rc) return rc;
   NewtonJob* dn = d_newton_;
-  k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, cand);
+  if (hybrid) {
+    k_pow_start<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, cand);
+    SH_LAUNCH_CHECK();
+    for (int k = 0; k < kPowerIters; ++k) {
+      k_pow_mv<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, total_elem_chunks_, ws_,
+                                                  nx_, cand);
+      SH_LAUNCH_CHECK();
+      k_pow_norm<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, nx_, cand);
+      SH_LAUNCH_CHECK();
+    }
+    prof_mark("nw_power");
+  }
+  k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, cand,
+                                                   hybrid ? 1 : 0);
   SH_LAUNCH_CHECK();
+  prof_mark("nw_init");
   int cur = 0;
   for (int it = 1; it <= budget; ++it) {
     k_newton_t<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, nx_, cur);
     SH_LAUNCH_CHECK();
+    prof_mark("nw_misc");
     if ((rc = newton_x_[cur].launch(s, mask))) return rc;
+    prof_mark("nw_gemm_x");
     for (auto& p : newton_pow_)
       if ((rc = p->launch(s, mask))) return rc;
+    prof_mark("nw_gemm_pow");
     if ((rc = newton_m_[cur].launch(s, mask))) return rc;
+    prof_mark("nw_gemm_m");
     SH_CUDA_CHECK(cudaMemsetAsync(d_count_, 0, sizeof(int32_t), s));
     k_newton_rowmax<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, total_elem_chunks_, nx_, cur ^ 1,
                                                        d_resbits_);
@@ -1774,9 +1881,11 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
     SH_LAUNCH_CHECK();
     cur ^= 1;
+    prof_mark("nw_misc");
     if ((it & 3) == 0 || it < 4 || (hybrid && it >= 6)) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      prof_mark("nw_sync");
       if (h_count_[0] == 0) break;
     }
   }
@@ -1874,6 +1983,17 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = (hs[j].status == kEigOk && !hs[j].via_newton) ? 1 : 0;
     else vec_valid_[j] = 0;
     sweeps_total_ += hs[j].sweep + hs[j].sweep32;
+  }
+  if (prof.on) {  // per-size solver histogram: n:{newton its | jacobi sweeps (w = warm started)}
+    std::map<int, std::string> by_n;
+    for (int j = 0; j < nj; ++j) {
+      if (host_[j].m == 0 || (skip && (*skip)[j])) continue;
+      char b[32];
+      std::snprintf(b, sizeof b, " %s%d", hs[j].via_newton ? "N" : (warm[j] ? "w" : "j"), hs[j].sweep);
+      by_n[host_[j].n] += b;
+    }
+    for (auto it = by_n.rbegin(); it != by_n.rend(); ++it)
+      std::fprintf(stderr, "[eig]   n=%d:%s\n", it->first, it->second.c_str());
   }
   if (host_status) {
     host_status->resize(nj);

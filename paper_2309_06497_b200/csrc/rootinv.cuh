@@ -63,6 +63,9 @@ struct NewtonJob {
   int64_t off;
   double best;
   int32_t iters, converged;
+  int32_t cap;  // hybrid pre-pass: iteration cap (conditioning gate, kHybridNewtonKappa)
+  int32_t pad;
+  double lam;   // hybrid pre-pass: power-iteration estimate of lambda_max(A) (scales X0, M0)
 };
 
 class RootInverseBatch {

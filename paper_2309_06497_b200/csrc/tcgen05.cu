@@ -483,6 +483,13 @@ __global__ void __launch_bounds__(256) k_oz_reduce(const GemmProblem* __restrict
 
 }  // namespace
 
+namespace {
+bool same_idx(const Idx2& a, const Idx2& b) { return a.div == b.div && a.hi == b.hi && a.lo == b.lo; }
+bool same_operand(const GemmProblem& p) {
+  return p.A == p.B && p.M == p.N && same_idx(p.a_r, p.b_r) && same_idx(p.a_k, p.b_k);
+}
+}  // namespace
+
 template <typename T>
 OzakiGemmBatch<T>::~OzakiGemmBatch() {
   cudaFree(d_prob_);
@@ -555,13 +562,16 @@ int OzakiGemmBatch<T>::upload() {
     t.kst = (t.ks + t.ksplit - 1) / t.ksplit;
     t.ksplit = (t.ks + t.kst - 1) / t.kst;
     const bool sym = (p.flags & kGemmSym) != 0;
+    // SYM output with A == B (a SYRK) shares one pack; SYM output of two distinct operands (products
+    // of commuting symmetric matrices, e.g. the coupled-Newton iterates) packs both
+    const bool share = sym && same_operand(p);
     if (p.M == 0 || p.N == 0) t.tiles = 0;
     else t.tiles = sym ? sym_tiles_before(t.mt, t.nt) : (int64_t)t.mt * t.nt;
     const int mi = (p.flags & kGemmMasked) ? p.mask_index : -1;
     const int aset = (p.flags & kGemmConstA) ? 1 : 0;
     add_pack(aset, p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp);
     a_set[i] = aset;
-    if (sym) {
+    if (share) {
       t.b_pack = t.a_pack;
       t.b_rc = t.a_rc;
       t.b_exp = t.a_exp;
@@ -589,7 +599,7 @@ int OzakiGemmBatch<T>::upload() {
   sets_[1].exp_elems = exp_count[1];
   for (size_t i = 0; i < host.size(); ++i) {
     if (a_set[i] == 1) tp[i].a_exp += exp_count[0];
-    if (host[i].flags & kGemmSym) tp[i].b_exp = tp[i].a_exp;
+    if ((host[i].flags & kGemmSym) && same_operand(host[i])) tp[i].b_exp = tp[i].a_exp;
     else if (b_set[i] == 1) tp[i].b_exp += exp_count[0];
   }
   for (int q = 0; q < 2; ++q)
