@@ -29,6 +29,17 @@ extern int64_t g_launches;  // kernel launches issued by this library (bench evi
     }                                                                                \
   } while (0)
 
+// Device workspace cache for the solver objects (Ozaki GEMM batches, root-inverse batches, the
+// low-rank path), which are built per refresh: blocks are reused instead of cudaMalloc/cudaFree
+// (cudaFree synchronises the device and stalls the other streams).  dev_free requires the block
+// to be idle: every kernel that used it has completed (its owner synchronised its stream).
+cudaError_t dev_malloc_bytes(void** p, size_t bytes);
+void dev_free(void* p);
+template <typename T>
+inline cudaError_t dev_malloc(T** p, size_t bytes) {
+  return dev_malloc_bytes(reinterpret_cast<void**>(p), bytes);
+}
+
 constexpr int kMaxOrder = SHAMPOO_MAX_ORDER;
 constexpr int kNumSMs = 148;
 

@@ -31,7 +31,9 @@ namespace {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-constexpr int kLowRankMax = 128;  // factors of structural rank <= 128 (and <= d/2) take the low-rank path
+// factors of structural rank r <= d - kLowRankGap take the low-rank path (range compression, lowrank.cuh):
+// their null space makes the full-size Newton pre-pass inapplicable, the compressed r x r factor is full rank
+constexpr int kLowRankGap = 8;
 constexpr int kRootGroups = 2;  // measured: 2 -> 1234 ms, 4 -> 1221 ms per t=50 refresh (ResNet-50)
 
 struct EngineBase {
@@ -578,7 +580,10 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   return SHAMPOO_OK;
 }
 
-void shampoo_ctx_destroy(shampoo_ctx* ctx) { delete ctx; }
+void shampoo_ctx_destroy(shampoo_ctx* ctx) {
+  cudaDeviceSynchronize();  // the solver workspaces return to the device cache idle (dev_free)
+  delete ctx;
+}
 
 int64_t shampoo_ctx_device_bytes(const shampoo_ctx* ctx) { return (int64_t)ctx->arena_bytes; }
 
@@ -704,8 +709,8 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
       const int64_t numel = c->plan.blocks[c->owned[l]].var_count;
       const int64_t rank = (int64_t)c->step[l] * (numel / std::max<int64_t>(d, 1));
       full_rank[g][j] = rank >= d ? 1 : 0;
-      if (k.solver == SHAMPOO_SOLVER_EIGH && k.epsilon > 0.0 && !c->f32 && d > 64 && rank <= kLowRankMax &&
-          2 * rank <= d && c->low_rank) {
+      if (k.solver == SHAMPOO_SOLVER_EIGH && k.epsilon > 0.0 && !c->f32 && d > 64 &&
+          rank + kLowRankGap <= d && c->low_rank) {
         low_rank[g][j] = 1;
         LowRankJob L{};
         L.d = (int32_t)d;

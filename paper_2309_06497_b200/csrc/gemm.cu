@@ -465,20 +465,20 @@ __global__ void __launch_bounds__(256) grouped_gemv_kernel(const GemvProblem* __
 
 template <typename T>
 GemmBatch<T>::~GemmBatch() {
-  cudaFree(d_prob_);
-  cudaFree(d_begin_);
-  cudaFree(d_rbegin_);
-  cudaFree(d_rprob_);
-  cudaFree(ws_);
+  dev_free(d_prob_);
+  dev_free(d_begin_);
+  dev_free(d_rbegin_);
+  dev_free(d_rprob_);
+  dev_free(ws_);
 }
 
 template <typename T>
 int GemmBatch<T>::upload() {
-  cudaFree(d_prob_);
-  cudaFree(d_begin_);
-  cudaFree(d_rbegin_);
-  cudaFree(d_rprob_);
-  cudaFree(ws_);
+  dev_free(d_prob_);
+  dev_free(d_begin_);
+  dev_free(d_rbegin_);
+  dev_free(d_rprob_);
+  dev_free(ws_);
   d_prob_ = nullptr;
   d_begin_ = d_rbegin_ = nullptr;
   d_rprob_ = nullptr;
@@ -516,14 +516,14 @@ int GemmBatch<T>::upload() {
     begin[i] = total_items_;
     total_items_ += p.tiles * p.ksplit;
   }
-  SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemmProblem)));
-  SH_CUDA_CHECK(cudaMalloc(&d_begin_, host.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemmProblem)));
+  SH_CUDA_CHECK(dev_malloc(&d_begin_, host.size() * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   if (!rbegin.empty()) {
-    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
-    SH_CUDA_CHECK(cudaMalloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
-    SH_CUDA_CHECK(cudaMalloc(&ws_, ws_elems * sizeof(double)));
+    SH_CUDA_CHECK(dev_malloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(dev_malloc(&ws_, ws_elems * sizeof(double)));
     SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rbegin.data(), rbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_rprob_, rprob.data(), rprob.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     nred_ = (int)rbegin.size();
@@ -556,14 +556,14 @@ double GemmBatch<T>::flops() const {
 
 template <typename T>
 GemvBatch<T>::~GemvBatch() {
-  cudaFree(d_prob_);
-  cudaFree(d_begin_);
+  dev_free(d_prob_);
+  dev_free(d_begin_);
 }
 
 template <typename T>
 int GemvBatch<T>::upload() {
-  cudaFree(d_prob_);
-  cudaFree(d_begin_);
+  dev_free(d_prob_);
+  dev_free(d_begin_);
   d_prob_ = nullptr;
   d_begin_ = nullptr;
   total_groups_ = 0;
@@ -573,8 +573,8 @@ int GemvBatch<T>::upload() {
     begin[i] = total_groups_;
     total_groups_ += (host[i].n + 7) / 8;
   }
-  SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemvProblem)));
-  SH_CUDA_CHECK(cudaMalloc(&d_begin_, host.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemvProblem)));
+  SH_CUDA_CHECK(dev_malloc(&d_begin_, host.size() * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemvProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   return SHAMPOO_OK;

@@ -13,6 +13,7 @@
 // tol_abs = max(0.1 u ||A||_F, 1e-9 eps); ignoring smaller couplings changes
 // X = f(A) by < 1e-9 relative (the f'(lambda) bound near the eps floor).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1437,36 +1438,45 @@ struct EigProfile {
   }
 };
 thread_local EigProfile* g_prof = nullptr;
+// host-side accounting of the profiled run: time blocked in stream syncs, time in build_newton
+thread_local double g_sync_ms = 0.0, g_build_ms = 0.0;
+cudaError_t timed_sync(cudaStream_t s) {
+  if (!g_prof || !g_prof->on) return cudaStreamSynchronize(s);
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaStreamSynchronize(s);
+  g_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return e;
+}
 void prof_mark(const char* n) {
   if (g_prof) g_prof->mark(n);
 }
 }  // namespace
 
 RootInverseBatch::~RootInverseBatch() {
-  cudaFree(d_jobs_);
-  cudaFree(d_state_);
-  cudaFree(ws_);
-  cudaFree(vs_);
-  cudaFree(us_);
-  cudaFree(wv_);
-  cudaFree(nx_);
-  cudaFree(xs_);
-  cudaFree(ts_);
-  cudaFree(d_warm_);
-  cudaFree(d_cand_);
-  cudaFree(d_newton_);
-  cudaFree(d_resbits_);
-  cudaFree(d_improved_);
-  cudaFree(d_pair_begin_);
-  cudaFree(d_item_begin_);
-  cudaFree(d_elem_begin_);
-  cudaFree(d_col_begin_);
-  cudaFree(d_count_);
-  cudaFreeHost(h_count_);
-  cudaFree(ws32_);
-  cudaFree(vs32_);
-  cudaFree(us32_);
-  cudaFree(d_mix_);
+  dev_free(d_jobs_);
+  dev_free(d_state_);
+  dev_free(ws_);
+  dev_free(vs_);
+  dev_free(us_);
+  dev_free(wv_);
+  dev_free(nx_);
+  dev_free(xs_);
+  dev_free(ts_);
+  dev_free(d_warm_);
+  dev_free(d_cand_);
+  dev_free(d_newton_);
+  dev_free(d_resbits_);
+  dev_free(d_improved_);
+  dev_free(d_pair_begin_);
+  dev_free(d_item_begin_);
+  dev_free(d_elem_begin_);
+  dev_free(d_col_begin_);
+  dev_free(d_count_);
+  dev_free(d_stats_);
+  dev_free(ws32_);
+  dev_free(vs32_);
+  dev_free(us32_);
+  dev_free(d_mix_);
 }
 
 double RootInverseBatch::work_n3() const {
@@ -1528,21 +1538,21 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   const size_t nj = host_.size();
   vec_valid_.assign(nj, 0);
   if (nj == 0) return SHAMPOO_OK;
-  SH_CUDA_CHECK(cudaMalloc(&d_jobs_, nj * sizeof(RootJob)));
-  SH_CUDA_CHECK(cudaMalloc(&d_state_, nj * sizeof(RootState)));
-  SH_CUDA_CHECK(cudaMalloc(&ws_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
-  SH_CUDA_CHECK(cudaMalloc(&vs_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
-  SH_CUDA_CHECK(cudaMalloc(&xs_, std::max<int64_t>(x_elems_, 1) * sizeof(double)));
-  SH_CUDA_CHECK(cudaMalloc(&us_, std::max<int64_t>(u_elems_, 1) * sizeof(double)));
-  SH_CUDA_CHECK(cudaMalloc(&wv_, std::max<int64_t>(w_elems_, 1) * sizeof(double)));
-  SH_CUDA_CHECK(cudaMalloc(&d_warm_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_cand_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_pair_begin_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_item_begin_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_elem_begin_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_col_begin_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMalloc(&d_count_, 4 * sizeof(int32_t) + nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(cudaMallocHost(&h_count_, 4 * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_jobs_, nj * sizeof(RootJob)));
+  SH_CUDA_CHECK(dev_malloc(&d_state_, nj * sizeof(RootState)));
+  SH_CUDA_CHECK(dev_malloc(&ws_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(dev_malloc(&vs_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(dev_malloc(&xs_, std::max<int64_t>(x_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(dev_malloc(&us_, std::max<int64_t>(u_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(dev_malloc(&wv_, std::max<int64_t>(w_elems_, 1) * sizeof(double)));
+  SH_CUDA_CHECK(dev_malloc(&d_warm_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_cand_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_pair_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_item_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_elem_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_col_begin_, nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_count_, 4 * sizeof(int32_t) + nj * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_stats_, 4 * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_pair_begin_, pbeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_item_begin_, ibeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_elem_begin_, ebeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1575,11 +1585,11 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     hybrid_ = nw ? std::atoi(nw) != 0 : true;
   }
   if (mixed_ && has_big_) {
-    SH_CUDA_CHECK(cudaMalloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
-    SH_CUDA_CHECK(cudaMalloc(&vs32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
-    SH_CUDA_CHECK(cudaMalloc(&us32_, std::max<int64_t>(u_elems_ / SLOT * SLOT32, 1) * sizeof(float)));
-    SH_CUDA_CHECK(cudaMalloc(&d_mix_, nj * sizeof(int32_t)));
-    if (!ts_) SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+    SH_CUDA_CHECK(dev_malloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
+    SH_CUDA_CHECK(dev_malloc(&vs32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
+    SH_CUDA_CHECK(dev_malloc(&us32_, std::max<int64_t>(u_elems_ / SLOT * SLOT32, 1) * sizeof(float)));
+    SH_CUDA_CHECK(dev_malloc(&d_mix_, nj * sizeof(int32_t)));
+    if (!ts_) SH_CUDA_CHECK(dev_malloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
     if ((rc = build_warm_gemms())) return rc;
     for (size_t j = 0; j < nj; ++j) {
       const RootJob& J = host_[j];
@@ -1623,7 +1633,7 @@ void RootInverseBatch::set_io(int j, const void* in, bool in_f32, void* out, boo
 int RootInverseBatch::build_warm_gemms() {
   // B = V^T A0 V for big jobs: T = A0 V -> ts ; B = V^T T -> ws (launched with a job mask)
   if (!warm1_.empty()) return SHAMPOO_OK;
-  if (!ts_) SH_CUDA_CHECK(cudaMalloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
+  if (!ts_) SH_CUDA_CHECK(dev_malloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
   for (size_t j = 0; j < host_.size(); ++j) {
     const RootJob& J = host_[j];
     if (J.m == 0) continue;
@@ -1673,7 +1683,7 @@ int RootInverseBatch::run_mixed_phase(cudaStream_t s, bool any_warm) {
     SH_LAUNCH_CHECK();
     if ((R & 7) == 7) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      SH_CUDA_CHECK(timed_sync(s));
       if (h_count_[0] == 0) break;
     }
     if (R > 256 * (MAX_SWEEPS32 + 1)) break;
@@ -1722,7 +1732,7 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     SH_LAUNCH_CHECK();
     if ((R & 7) == 7) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      SH_CUDA_CHECK(timed_sync(s));
       if (h_count_[0] == 0) break;
     }
     if (R > 256 * (MAX_SWEEPS + 1)) break;  // safety net (k_book caps sweeps per job)
@@ -1775,7 +1785,7 @@ std::vector<PowStep> power_plan(int p, int* final_buf) {
 int RootInverseBatch::build_newton() {
   if (newton_built_) return SHAMPOO_OK;
   const int nj = (int)host_.size();
-  if (!nx_) SH_CUDA_CHECK(cudaMalloc(&nx_, std::max<int64_t>(n2_elems_, 1) * sizeof(double)));
+  if (!nx_) SH_CUDA_CHECK(dev_malloc(&nx_, std::max<int64_t>(n2_elems_, 1) * sizeof(double)));
   std::vector<NewtonJob> hn(nj);
   for (int j = 0; j < nj; ++j) {
     hn[j].n = host_[j].n;
@@ -1786,10 +1796,10 @@ int RootInverseBatch::build_newton() {
       hn[j].cap = 5 + (int)std::ceil(std::log(kHybridNewtonKappa) / (p * std::log((p + 1.0) / p)));
     }
   }
-  SH_CUDA_CHECK(cudaMalloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
-  SH_CUDA_CHECK(cudaMalloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
+  SH_CUDA_CHECK(dev_malloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
+  SH_CUDA_CHECK(dev_malloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(cudaMemset(d_resbits_, 0, std::max(nj, 1) * sizeof(unsigned long long)));
-  SH_CUDA_CHECK(cudaMalloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_newton_, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice));
   // GEMM sets for cur = 0/1: X_nxt = X_cur T ; T^p ; M_nxt = T^p M_cur (tcgen05 Ozaki, FP64 class)
   size_t nsteps = 0;
@@ -1840,8 +1850,10 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
                                    cudaStream_t s) {
   const int nj = (int)host_.size();
   int32_t* mask = d_count_ + 4;
+  const auto tb0 = std::chrono::steady_clock::now();
   int rc = build_newton();
   if (rc) return rc;
+  g_build_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count();
   NewtonJob* dn = d_newton_;
   if (hybrid) {
     k_pow_start<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, d_elem_begin_, nj, nx_, cand);
@@ -1884,7 +1896,7 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     prof_mark("nw_misc");
     if ((it & 3) == 0 || it < 4 || (hybrid && it >= 6)) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      SH_CUDA_CHECK(cudaStreamSynchronize(s));
+      SH_CUDA_CHECK(timed_sync(s));
       prof_mark("nw_sync");
       if (h_count_[0] == 0) break;
     }
@@ -1926,6 +1938,8 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   }
   EigProfile prof(s);
   g_prof = &prof;
+  const auto t_run0 = std::chrono::steady_clock::now();
+  g_sync_ms = g_build_ms = 0.0;
   struct ProfReset {
     ~ProfReset() { g_prof = nullptr; }
   } prof_reset;
@@ -1969,8 +1983,7 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   SH_LAUNCH_CHECK();
   k_select<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, d_elem_begin_, nj, xs_);
   SH_LAUNCH_CHECK();
-  int64_t* d_stats = nullptr;
-  SH_CUDA_CHECK(cudaMallocAsync(&d_stats, 4 * sizeof(int64_t), s));
+  int64_t* d_stats = d_stats_;
   SH_CUDA_CHECK(cudaMemcpyAsync(d_stats, stats, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
   k_count<<<1, 32, 0, s>>>(d_jobs_, d_state_, nj, d_stats);
   SH_LAUNCH_CHECK();
@@ -1978,12 +1991,15 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   std::vector<RootState> hs(nj);
   SH_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_state_, nj * sizeof(RootState), cudaMemcpyDeviceToHost, s));
   SH_CUDA_CHECK(cudaStreamSynchronize(s));
-  SH_CUDA_CHECK(cudaFreeAsync(d_stats, s));
   for (int j = 0; j < nj; ++j) {
     if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = (hs[j].status == kEigOk && !hs[j].via_newton) ? 1 : 0;
     else vec_valid_[j] = 0;
     sweeps_total_ += hs[j].sweep + hs[j].sweep32;
   }
+  if (prof.on)
+    std::fprintf(stderr, "[eig] host: run %.2f ms, blocked in syncs %.2f ms, build_newton %.2f ms (jobs %d)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run0).count(),
+                 g_sync_ms, g_build_ms, nj);
   if (prof.on) {  // per-size solver histogram: n:{newton its | jacobi sweeps (w = warm started)}
     std::map<int, std::string> by_n;
     for (int j = 0; j < nj; ++j) {

@@ -131,7 +131,9 @@ class RootInverseBatch {
   int32_t* d_elem_begin_ = nullptr;
   int32_t* d_col_begin_ = nullptr;
   int32_t* d_count_ = nullptr;
-  int32_t* h_count_ = nullptr;  // pinned
+  int32_t h_count_[4] = {0, 0, 0, 0};  // pageable: the D2H read is a sync point anyway (no pinned
+                                       // alloc per batch: cudaMallocHost/cudaFreeHost stall the device)
+  int64_t* d_stats_ = nullptr;
   int32_t total_pairs_ = 0, total_items_ = 0, total_elem_chunks_ = 0, total_col_chunks_ = 0;
   int64_t ws_elems_ = 0, u_elems_ = 0, w_elems_ = 0, n2_elems_ = 0;
   std::vector<int64_t> n2_off_;

@@ -492,19 +492,19 @@ bool same_operand(const GemmProblem& p) {
 
 template <typename T>
 OzakiGemmBatch<T>::~OzakiGemmBatch() {
-  cudaFree(d_prob_);
-  cudaFree(d_tp_);
-  cudaFree(d_begin_);
+  dev_free(d_prob_);
+  dev_free(d_tp_);
+  dev_free(d_begin_);
   for (auto& ps : sets_) {
-    cudaFree(ps.d_jobs);
-    cudaFree(ps.d_pbegin);
-    cudaFree(ps.d_ebegin);
+    dev_free(ps.d_jobs);
+    dev_free(ps.d_pbegin);
+    dev_free(ps.d_ebegin);
   }
-  cudaFree(d_rbegin_);
-  cudaFree(d_rprob_);
-  cudaFree(arena_);
-  cudaFree(exps_);
-  cudaFree(ws_);
+  dev_free(d_rbegin_);
+  dev_free(d_rprob_);
+  dev_free(arena_);
+  dev_free(exps_);
+  dev_free(ws_);
 }
 
 template <typename T>
@@ -605,11 +605,11 @@ int OzakiGemmBatch<T>::upload() {
   for (int q = 0; q < 2; ++q)
     for (auto& J : jobs[q]) J.exp += sets_[q].exp_begin;
   nred_ = (int)rbegin.size();
-  SH_CUDA_CHECK(cudaMalloc(&d_prob_, host.size() * sizeof(GemmProblem)));
-  SH_CUDA_CHECK(cudaMalloc(&d_tp_, tp.size() * sizeof(OzProb)));
-  SH_CUDA_CHECK(cudaMalloc(&d_begin_, begin.size() * sizeof(int64_t)));
-  SH_CUDA_CHECK(cudaMalloc(&arena_, std::max<int64_t>(arena, 256)));
-  SH_CUDA_CHECK(cudaMalloc(&exps_, std::max<int64_t>(exp_count[0] + exp_count[1], 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemmProblem)));
+  SH_CUDA_CHECK(dev_malloc(&d_tp_, tp.size() * sizeof(OzProb)));
+  SH_CUDA_CHECK(dev_malloc(&d_begin_, begin.size() * sizeof(int64_t)));
+  SH_CUDA_CHECK(dev_malloc(&arena_, std::max<int64_t>(arena, 256)));
+  SH_CUDA_CHECK(dev_malloc(&exps_, std::max<int64_t>(exp_count[0] + exp_count[1], 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_tp_, tp.data(), tp.size() * sizeof(OzProb), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_begin_, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
@@ -617,18 +617,18 @@ int OzakiGemmBatch<T>::upload() {
     PackSet& ps = sets_[q];
     ps.njobs = (int)jobs[q].size();
     if (!ps.njobs) continue;
-    SH_CUDA_CHECK(cudaMalloc(&ps.d_jobs, jobs[q].size() * sizeof(OzPackJob)));
-    SH_CUDA_CHECK(cudaMalloc(&ps.d_pbegin, pbegin[q].size() * sizeof(int64_t)));
-    SH_CUDA_CHECK(cudaMalloc(&ps.d_ebegin, ebegin[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&ps.d_jobs, jobs[q].size() * sizeof(OzPackJob)));
+    SH_CUDA_CHECK(dev_malloc(&ps.d_pbegin, pbegin[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&ps.d_ebegin, ebegin[q].size() * sizeof(int64_t)));
     SH_CUDA_CHECK(cudaMemcpy(ps.d_jobs, jobs[q].data(), jobs[q].size() * sizeof(OzPackJob), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(ps.d_pbegin, pbegin[q].data(), pbegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(ps.d_ebegin, ebegin[q].data(), ebegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   cached_valid_ = false;
   if (nred_ > 0) {
-    SH_CUDA_CHECK(cudaMalloc(&ws_, wsz * sizeof(double)));
-    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
-    SH_CUDA_CHECK(cudaMalloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(dev_malloc(&ws_, wsz * sizeof(double)));
+    SH_CUDA_CHECK(dev_malloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_rprob_, rprob.size() * sizeof(int32_t)));
     SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rbegin.data(), rbegin.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_rprob_, rprob.data(), rprob.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }

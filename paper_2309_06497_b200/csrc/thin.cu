@@ -179,15 +179,15 @@ static bool is_rank1(const GemmProblem& p) {
 
 template <typename T>
 ThinGemmBatch<T>::~ThinGemmBatch() {
-  cudaFree(d_r1_);
-  cudaFree(d_r1begin_);
-  cudaFree(d_out_);
-  cudaFree(d_obegin_);
-  cudaFree(d_red_);
-  cudaFree(d_rbegin_);
-  cudaFree(d_woff_);
-  cudaFree(d_nch_);
-  cudaFree(ws_);
+  dev_free(d_r1_);
+  dev_free(d_r1begin_);
+  dev_free(d_out_);
+  dev_free(d_obegin_);
+  dev_free(d_red_);
+  dev_free(d_rbegin_);
+  dev_free(d_woff_);
+  dev_free(d_nch_);
+  dev_free(ws_);
 }
 
 template <typename T>
@@ -202,8 +202,8 @@ int ThinGemmBatch<T>::upload() {
   }
   n_r1_ = (int)r1p.size();
   if (n_r1_) {
-    SH_CUDA_CHECK(cudaMalloc(&d_r1_, r1p.size() * sizeof(GemmProblem)));
-    SH_CUDA_CHECK(cudaMalloc(&d_r1begin_, r1b.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_r1_, r1p.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(dev_malloc(&d_r1begin_, r1b.size() * sizeof(int64_t)));
     SH_CUDA_CHECK(cudaMemcpy(d_r1_, r1p.data(), r1p.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_r1begin_, r1b.data(), r1b.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
@@ -228,17 +228,17 @@ int ThinGemmBatch<T>::upload() {
   n_out_ = (int)outp.size();
   n_red_ = (int)redp.size();
   if (n_out_) {
-    SH_CUDA_CHECK(cudaMalloc(&d_out_, outp.size() * sizeof(GemmProblem)));
-    SH_CUDA_CHECK(cudaMalloc(&d_obegin_, ob.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_out_, outp.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(dev_malloc(&d_obegin_, ob.size() * sizeof(int64_t)));
     SH_CUDA_CHECK(cudaMemcpy(d_out_, outp.data(), outp.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_obegin_, ob.data(), ob.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   if (n_red_) {
-    SH_CUDA_CHECK(cudaMalloc(&d_red_, redp.size() * sizeof(GemmProblem)));
-    SH_CUDA_CHECK(cudaMalloc(&d_rbegin_, rb.size() * sizeof(int64_t)));
-    SH_CUDA_CHECK(cudaMalloc(&d_woff_, wo.size() * sizeof(int64_t)));
-    SH_CUDA_CHECK(cudaMalloc(&d_nch_, nch.size() * sizeof(int32_t)));
-    SH_CUDA_CHECK(cudaMalloc(&ws_, wsz * sizeof(double)));
+    SH_CUDA_CHECK(dev_malloc(&d_red_, redp.size() * sizeof(GemmProblem)));
+    SH_CUDA_CHECK(dev_malloc(&d_rbegin_, rb.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_woff_, wo.size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&d_nch_, nch.size() * sizeof(int32_t)));
+    SH_CUDA_CHECK(dev_malloc(&ws_, wsz * sizeof(double)));
     SH_CUDA_CHECK(cudaMemcpy(d_red_, redp.data(), redp.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rb.data(), rb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_woff_, wo.data(), wo.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
