@@ -56,6 +56,7 @@ struct DevBlock {
   int64_t dims[kMaxOrder];
   int64_t lo[kMaxOrder];
   int64_t mstride[kMaxOrder];
+  int64_t cbase;       // >= 0: the block is one contiguous run of its parameter starting there
 };
 
 // A contiguous run of elements of one block processed by one CTA.
@@ -68,6 +69,12 @@ struct Chunk {
 
 // Flat element index inside a block -> element offset inside the parameter.
 __device__ __forceinline__ int64_t block_to_param_offset(const DevBlock& b, int64_t e) {
+  if (b.cbase >= 0) return b.cbase + e;  // row partitions and whole parameters: no index arithmetic
+  if (e < 0x7fffffff && b.order == 2 && b.dims[1] < 0x7fffffff) {  // 32-bit division
+    const uint32_t d1 = (uint32_t)b.dims[1], ue = (uint32_t)e;
+    const uint32_t i0 = ue / d1, i1 = ue - i0 * d1;
+    return (b.lo[0] + i0) * b.mstride[0] + (b.lo[1] + i1) * b.mstride[1];
+  }
   int64_t off = 0;
 #pragma unroll 1
   for (int k = b.order - 1; k >= 0; --k) {

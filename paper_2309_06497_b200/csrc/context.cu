@@ -448,10 +448,19 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
       d.lo[k] = b.lo[k];
       d.mstride[k] = pp.mstride[k];
     }
+    bool contig = b.order > 0 && d.mstride[b.order - 1] == 1;
+    for (int k = 0; k + 1 < b.order && contig; ++k) contig = d.mstride[k] == d.dims[k + 1] * d.mstride[k + 1];
+    for (int k = 1; k < b.order && contig; ++k) contig = d.lo[k] == 0;
+    d.cbase = -1;
+    if (contig) {
+      d.cbase = 0;
+      for (int k = 0; k < b.order; ++k) d.cbase += d.lo[k] * d.mstride[k];
+    }
   }
   for (int p = 0; p < c->nparams; ++p) {
     std::memset(&dp[p], 0, sizeof(DevBlock));
     dp[p].param = p;
+    dp[p].cbase = -1;
     const int64_t n = plan->params[p].numel;
     for (int64_t s = 0; s < n; s += kChunk) pc.push_back(Chunk{p, 0, s, std::min<int64_t>(kChunk, n - s)});
   }

@@ -57,6 +57,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Long waits (the epilogue warps wait out the whole mainloop): back off between polls so the
+// spinning warps do not take issue slots (and the sync unit) from the producer / MMA lanes.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0, ns = 32;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -376,7 +391,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
       row_off[et] = evx(P.c_r, gi);
       mcol_off[et] = evx(P.c_c, gi);
     }
-    mbar_wait(&done_bar, 0);
+    mbar_wait_sleep(&done_bar, 0);
     tc_fence_after();
     const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
     // diagonals combined exactly in two int64 fixed-point halves (|acc_d| < 2^31, so each half
