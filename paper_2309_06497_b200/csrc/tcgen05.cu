@@ -206,6 +206,46 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
   }
 }
 
+// The S signed 7-bit slices of y = x 2^-e (|y| < 1) -- the digits of the fixed-point |y| in base
+// 128 with the sign of x, the last one rounded half-to-even on the remaining bits and clamped to
+// +-127; i.e. exactly  t = 128 y, q = trunc(t), y = t - q  for the first S - 1 slices and
+// q = rint(t) for the last (unbiased truncation of the dropped remainder), computed on the
+// integer mantissa (no FP64 / conversion-pipe work).
+template <int S>
+__device__ __forceinline__ void ozaki_slices(double x, int e, int8_t (&q)[S]) {
+  constexpr int G = 7;  // guard bits below the last slice
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int bexp = (int)((bits >> 52) & 0x7ff);
+  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
+  if (bexp) m |= 1ull << 52;
+  // |x| = m 2^(max(bexp,1) - 1075);  Yg = |y| 2^(7S + G) = m 2^sh
+  const int sh = (bexp ? bexp : 1) - 1075 - e + 7 * S + G;
+  unsigned long long yg;
+  bool sticky;
+  if (sh >= 0) {
+    yg = m << sh;  // |y| < 1 keeps yg < 2^(7S+G) <= 2^63
+    sticky = false;
+  } else if (sh > -64) {
+    yg = m >> (-sh);
+    sticky = (m & ((1ull << (-sh)) - 1ull)) != 0ull;
+  } else {
+    yg = 0ull;
+    sticky = m != 0ull;
+  }
+  const unsigned long long top = yg >> G;
+  const unsigned frac = (unsigned)(yg & ((1u << G) - 1u)), half = 1u << (G - 1);
+  const int neg = (int)(bits >> 63);
+#pragma unroll
+  for (int s = 0; s + 1 < S; ++s) {
+    const int d = (int)((top >> (7 * (S - 1 - s))) & 127ull);
+    q[s] = (int8_t)(neg ? -d : d);
+  }
+  int last = (int)(top & 127ull);
+  if (frac > half || (frac == half && (sticky || (last & 1)))) ++last;
+  last = last > 127 ? 127 : last;
+  q[S - 1] = (int8_t)(neg ? -last : last);
+}
+
 // Operands -> int8 slice planes, slice-major per stage: byte offset
 // ((stage * S + s) * rc + core) * 256 + kc * 128 + r8 * 16 holds row 8 core + r8,
 // k = 32 stage + 16 kc .. +15 of slice s.  Unit u = ((stage * rc + core) * 2 + kc) * 8 + r8.
@@ -233,19 +273,15 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
     const T* __restrict__ src = static_cast<const T*>(J.src);
     const int64_t rb = evx(J.r, row);
     const int e = max(exps[J.exp + row], kExpFloor);
+    double xv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(J.k, k0 + i)] : 0.0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int k = k0 + i;
-      double y = (k < J.K) ? ldexp((double)src[rb + evx(J.k, k)], -e) : 0.0;  // |y| < 1, exact
+      int8_t q[S];
+      ozaki_slices<S>(xv[i], e, q);
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const double t = y * 128.0;
-        // truncate, except the last slice rounds to nearest: the dropped remainder is then
-        // unbiased (+-2^-7S / 2 of the row maximum) instead of always shrinking |x|
-        const double q = (s + 1 < S) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
-        y = t - q;                   // exact
-        w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)q) << (8 * (i & 3));
-      }
+      for (int s = 0; s < S; ++s) w[s][i >> 2] |= ((uint32_t)(uint8_t)q[s]) << (8 * (i & 3));
     }
   }
   int8_t* dst = arena + J.dst + ((int64_t)stage * S * J.rc + core) * 256 + kc * 128 + r8 * 16;
