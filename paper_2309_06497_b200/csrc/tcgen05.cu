@@ -1,7 +1,11 @@
 // Grouped Ozaki-split int8 GEMM on tcgen05 tensor cores (see tcgen05.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "tcgen05.cuh"
 
@@ -12,6 +16,7 @@ namespace {
 constexpr int TM = 128, TN = 32, TKB = 32;    // CTA tile; 32 int8 (= one MMA K) per pipeline stage
 constexpr int SL_PER_MMA = 256 / TN;          // B slices stacked along N in one MMA (N <= 256)
 constexpr int GEMM_THREADS = 192;             // warp 0 bulk copies, warp 1 MMA, warps 2-5 epilogue
+constexpr int GEMM_THREADS_P = 320;           // persistent variant: 8 epilogue warps
 constexpr int64_t kOzSplitStages = 256;       // 8192 k per split: int32 sums stay exact (< 2^31)
 constexpr int PACK_UNITS = 256;               // pack threads per CTA (one unit = 16 k of one row)
 constexpr int EXP_CHUNK = 64;                 // k per rowexp thread (strided rows)
@@ -77,6 +82,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// TMA tile load of a 3-D box (tensor map in global memory) into shared memory.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // ---- tcgen05 ----
@@ -304,7 +318,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
                                                             const int64_t* __restrict__ begin, int nprob,
                                                             const int32_t* __restrict__ mask,
                                                             const int8_t* __restrict__ arena,
-                                                            const int32_t* __restrict__ exps, double* __restrict__ ws) {
+                                                            const int32_t* __restrict__ exps, double* __restrict__ ws,
+                                                            const CUtensorMap* __restrict__ tmaps) {
   using Cfg = OzCfg<S>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   // per stage two "full" barriers: [0] all B slices + the first half of the A slices, [1] the rest of
@@ -366,10 +381,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
         if (it >= Cfg::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
         uint8_t* sb = sbase + (size_t)st * Cfg::STAGE;
         constexpr int SH = (S + 1) / 2;  // A slices in the first half
-        mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
-        mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
         const int8_t* as = a_src + (int64_t)it * S * a_plane;
         const int8_t* bs = b_src + (int64_t)it * S * b_plane;
+        if (tmaps) {
+          // three TMA boxes per stage: B (4 cores x S slices), A slices [0, SH) and [SH, S) (16 cores
+          // each); cores past the operand's end arrive zero-filled, so the byte counts are fixed
+          const CUtensorMap* tm3 = tmaps + 3 * pi;
+          const int z = (s0 + it) * S;
+          mbar_expect_tx(&full_bar[st][0], (uint32_t)(S * (TN / 8) * 256 + SH * (TM / 8) * 256));
+          mbar_expect_tx(&full_bar[st][1], (uint32_t)((S - SH) * (TM / 8) * 256));
+          tma_load_3d(sb + Cfg::A_BYTES, tm3 + 2, 0, tn * (TN / 8), z, &full_bar[st][0]);
+          tma_load_3d(sb, tm3 + 0, 0, tm * (TM / 8), z, &full_bar[st][0]);
+          tma_load_3d(sb + SH * (TM / 8) * 256, tm3 + 1, 0, tm * (TM / 8), z + SH, &full_bar[st][1]);
+          continue;
+        }
+        mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
+        mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
 #pragma unroll
         for (int q = 0; q < S; ++q) {
           bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st][0]);
@@ -504,6 +531,262 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
   }
 }
 
+// Persistent variant: one CTA per SM walks the tile list with a static stride; the stage ring runs
+// across tiles (the producer prefetches the next tile's k-steps while the current one computes) and
+// the TMEM accumulators are double-buffered (2 x 256 columns), so the FP64 epilogue of tile i
+// overlaps the MMAs of tile i + 1.  Same math, layout and epilogue semantics as k_oz_gemm.
+template <int S>
+struct OzPCfg {
+  static constexpr int STAGE = OzCfg<S>::STAGE;
+  static constexpr size_t TILE_BYTES = (size_t)TM * LDE * sizeof(double);
+  static constexpr int STAGES_RAW = (int)((226 * 1024 - TILE_BYTES - 1024) / STAGE);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + TILE_BYTES + 1024;
+};
+
+struct OzItem {
+  int pi, tm, tn, split, s0, nk;
+  int64_t tile;
+};
+
+__device__ __forceinline__ bool oz_decode(const GemmProblem* __restrict__ probs, const OzProb* __restrict__ tps,
+                                          const int64_t* __restrict__ begin, int nprob,
+                                          const int32_t* __restrict__ mask, int64_t item, OzItem& it) {
+  it.pi = find64<GemmProblem>(begin, nprob, item);
+  const GemmProblem& P = probs[it.pi];
+  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return false;
+  const OzProb& T_ = tps[it.pi];
+  const int64_t l = item - begin[it.pi];
+  it.split = (int)(l % T_.ksplit);
+  it.tile = l / T_.ksplit;
+  if (P.flags & kGemmSym) sym_decode(it.tile, T_.nt, it.tm, it.tn);
+  else {
+    it.tm = (int)(it.tile / T_.nt);
+    it.tn = (int)(it.tile % T_.nt);
+  }
+  it.s0 = it.split * T_.kst;
+  it.nk = min(T_.ks, it.s0 + T_.kst) - it.s0;
+  return true;
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProblem* __restrict__ probs,
+                                                               const OzProb* __restrict__ tps,
+                                                               const int64_t* __restrict__ begin, int nprob,
+                                                               int64_t total_items, const int32_t* __restrict__ mask,
+                                                               const int8_t* __restrict__ arena,
+                                                               const int32_t* __restrict__ exps, double* __restrict__ ws) {
+  using Cfg = OzCfg<S>;
+  using PC = OzPCfg<S>;
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  __shared__ __align__(8) uint64_t full_bar[PC::STAGES][2], empty_bar[PC::STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ double col_scale[TN];
+  __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
+  double* tileS = reinterpret_cast<double*>(sbase + (size_t)PC::STAGES * PC::STAGE);
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < PC::STAGES; ++i) {
+      mbar_init(&full_bar[i][0], 1);
+      mbar_init(&full_bar[i][1], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "n"(2 * Cfg::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      uint32_t g = 0;
+      OzItem it;
+      for (int64_t item = blockIdx.x; item < total_items; item += gridDim.x) {
+        if (!oz_decode(probs, tps, begin, nprob, mask, item, it)) continue;
+        const OzProb& T_ = tps[it.pi];
+        const int a_cores = min(TM / 8, T_.a_rc - it.tm * (TM / 8));
+        const int b_cores = min(TN / 8, T_.b_rc - it.tn * (TN / 8));
+        const int64_t a_plane = (int64_t)T_.a_rc * 256, b_plane = (int64_t)T_.b_rc * 256;
+        const int8_t* a_src = arena + T_.a_pack + (int64_t)it.s0 * S * a_plane + (int64_t)it.tm * (TM / 8) * 256;
+        const int8_t* b_src = arena + T_.b_pack + (int64_t)it.s0 * S * b_plane + (int64_t)it.tn * (TN / 8) * 256;
+        const uint32_t a_bytes = (uint32_t)a_cores * 256, b_bytes = (uint32_t)b_cores * 256;
+        for (int k = 0; k < it.nk; ++k, ++g) {
+          const int st = (int)(g % PC::STAGES);
+          const uint32_t use = g / PC::STAGES;
+          if (g >= (uint32_t)PC::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
+          uint8_t* sb = sbase + (size_t)st * PC::STAGE;
+          constexpr int SH = (S + 1) / 2;
+          mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
+          mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
+          const int8_t* as = a_src + (int64_t)k * S * a_plane;
+          const int8_t* bs = b_src + (int64_t)k * S * b_plane;
+#pragma unroll
+          for (int q = 0; q < S; ++q) {
+            bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st][0]);
+            if (q < SH) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][0]);
+          }
+#pragma unroll
+          for (int q = SH; q < S; ++q) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][1]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      uint32_t g = 0, tcount = 0;
+      OzItem it;
+      for (int64_t item = blockIdx.x; item < total_items; item += gridDim.x) {
+        if (!oz_decode(probs, tps, begin, nprob, mask, item, it)) continue;
+        const uint32_t b = tcount & 1u;
+        mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);  // the epilogue drained this buffer
+        tc_fence_after();
+        const uint32_t acc = tmem + b * Cfg::TMEM_COLS;
+        for (int k = 0; k < it.nk; ++k, ++g) {
+          const int st = (int)(g % PC::STAGES);
+          const uint32_t par = (g / PC::STAGES) & 1u;
+          mbar_wait(&full_bar[st][0], par);
+          tc_fence_after();
+          const uint32_t sa_base = smem_u32(sbase + (size_t)st * PC::STAGE);
+          const uint32_t sb_base = sa_base + Cfg::A_BYTES;
+#pragma unroll
+          for (int sa = 0; sa < S; ++sa) {
+            if (sa == (S + 1) / 2) {
+              mbar_wait(&full_bar[st][1], par);
+              tc_fence_after();
+            }
+            const uint64_t ad = sdesc(sa_base + sa * (TM / 8) * 256, 128, 256);
+#pragma unroll
+            for (int sb0 = 0; sb0 < S - sa; sb0 += SL_PER_MMA) {
+              const int nsl = min(SL_PER_MMA, S - sa - sb0);
+              const uint64_t bd = sdesc(sb_base + sb0 * (TN / 8) * 256, 128, 256);
+              const uint32_t idesc = Cfg::IDESC_BASE | ((uint32_t)(nsl * TN >> 3) << 17);
+              tc_mma_i8(acc + (uint32_t)((sa + sb0) * TN), ad, bd, idesc, (k > 0 || sa > 0) ? 1u : 0u);
+            }
+          }
+          tc_commit(&empty_bar[st]);
+        }
+        tc_commit(&tfull[b]);  // accumulators of this tile complete
+        ++tcount;
+      }
+    }
+  } else {
+    // 8 epilogue warps: warp w drains TMEM lanes 32 (w % 4) .. +31, the two warpgroups split the columns
+    const int et = threadIdx.x - 64;
+    const int lg = warp & 3;
+    const int rl = lg * 32 + lane;
+    const int cbeg = (et >= 128) ? TN / 2 : 0;
+    uint32_t tcount = 0;
+    OzItem it;
+    for (int64_t item = blockIdx.x; item < total_items; item += gridDim.x) {
+      if (!oz_decode(probs, tps, begin, nprob, mask, item, it)) continue;
+      const GemmProblem& P = probs[it.pi];
+      const OzProb& T_ = tps[it.pi];
+      const int tm = it.tm, tn = it.tn;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's readers of the smem arrays done
+      if (et < TN) {
+        const int gj = tn * TN + et;
+        col_scale[et] = pow2i(exps[T_.b_exp + min(gj, T_.b_rc * 8 - 1)]);
+        col_off[et] = evx(P.c_c, gj);
+        mrow_off[et] = evx(P.c_r, gj);
+      }
+      if (et < TM) {
+        const int gi = tm * TM + et;
+        row_off[et] = evx(P.c_r, gi);
+        mcol_off[et] = evx(P.c_c, gi);
+      }
+      const uint32_t b = tcount & 1u;
+      mbar_wait_sleep(&tfull[b], (tcount >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t acc = tmem + b * Cfg::TMEM_COLS;
+      const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
+      constexpr int H = (S + 1) / 2;
+      int32_t v[16];
+      for (int c0 = cbeg; c0 < cbeg + TN / 2; c0 += 16) {
+        long long hi[16], lo[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0;
+        if (it.nk > 0) {
+#pragma unroll
+          for (int d = 0; d < S; ++d) {
+            tmem_ld16(acc + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * TN + c0), v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              if (d < H) hi[q] += (long long)v[q] << (7 * (H - 1 - d));
+              else lo[q] += (long long)v[q] << (7 * (S - 1 - d));
+            }
+          }
+        }
+        const double whi = pow2i(-7 * (H + 1)), wlo = pow2i(-7 * (S + 1));
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          tileS[rl * LDE + c0 + q] = fma((double)hi[q], whi, (double)lo[q] * wlo) * rscale;
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // all TMEM reads of buffer b done, tileS complete
+      if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+      ++tcount;
+      const bool sym = (P.flags & kGemmSym) != 0;
+      if (T_.ksplit == 1) {
+        T* __restrict__ C = static_cast<T*>(P.C);
+        const bool readc = (P.flags & kGemmReadC) != 0;
+        for (int e0 = et; e0 < TM * TN; e0 += 8 * 256) {
+          double cv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 256, r = e / TN, c = e % TN;
+            const int gi = tm * TM + r, gj = tn * TN + c;
+            const bool live = gi < P.M && gj < P.N && !(sym && gi < gj);
+            cv[u] = (readc && live) ? (double)C[row_off[r] + col_off[c]] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 256, r = e / TN, c = e % TN;
+            const int gi = tm * TM + r, gj = tn * TN + c;
+            if (gi >= P.M || gj >= P.N || (sym && gi < gj)) continue;
+            double val = P.alpha * (tileS[r * LDE + c] * col_scale[c]);
+            if (readc) val = fma(P.beta, cv[u], val);
+            tileS[r * LDE + c] = val;
+            C[row_off[r] + col_off[c]] = (T)val;
+          }
+        }
+        if (sym) {
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          for (int e = et; e < TM * TN; e += 256) {
+            const int c = e / TM, r = e % TM;
+            const int gi = tm * TM + r, gj = tn * TN + c;
+            if (gi >= P.M || gj >= P.N || gi <= gj) continue;
+            C[mrow_off[c] + mcol_off[r]] = (T)tileS[r * LDE + c];
+          }
+        }
+      } else {
+        double* dst = ws + T_.ws_off + (it.tile * T_.ksplit + it.split) * (int64_t)(TM * TN);
+        for (int e = et; e < TM * TN; e += 256) {
+          const int r = e / TN, c = e % TN;
+          dst[e] = tileS[r * LDE + c] * col_scale[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * Cfg::TMEM_COLS) : "memory");
+  }
+}
+
 // Split-K: scaled partial tiles summed in split order in FP64, then the epilogue.
 template <typename T>
 __global__ void __launch_bounds__(256) k_oz_reduce(const GemmProblem* __restrict__ probs, const OzProb* __restrict__ tps,
@@ -556,6 +839,7 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
   dev_free(arena_);
   dev_free(exps_);
   dev_free(ws_);
+  dev_free(d_tmaps_);
 }
 
 template <typename T>
@@ -564,6 +848,9 @@ int OzakiGemmBatch<T>::upload() {
   static const cudaError_t attr = cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)OzCfg<S>::SMEM);  // once, thread-safe
   SH_CUDA_CHECK(attr);
+  static const cudaError_t attr_p = cudaFuncSetAttribute(
+      k_oz_gemm_p<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OzPCfg<S>::SMEM);
+  SH_CUDA_CHECK(attr_p);
   std::vector<OzProb> tp(host.size());
   std::vector<int> a_set(host.size(), 0), b_set(host.size(), 0);
   std::vector<int64_t> begin(host.size()), rbegin, pbegin[2], ebegin[2];
@@ -676,6 +963,41 @@ int OzakiGemmBatch<T>::upload() {
     SH_CUDA_CHECK(cudaMemcpy(ps.d_ebegin, ebegin[q].data(), ebegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   cached_valid_ = false;
+  // TMA tensor maps of the packed operands: [S * ks slices-by-stage][rc cores][256 B core block]
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      cudaGetLastError();
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    std::vector<CUtensorMap> maps(3 * host.size());
+    bool ok = encode != nullptr && std::getenv("SHAMPOO_OZ_NO_TMA") == nullptr;
+    constexpr int SH = (S + 1) / 2;
+    auto make = [&](CUtensorMap* m, int64_t off, int rc, int ks, int cores, int slices) {
+      const cuuint64_t dims[3] = {256, (cuuint64_t)rc, (cuuint64_t)S * ks};
+      const cuuint64_t strides[2] = {256, (cuuint64_t)rc * 256};
+      const cuuint32_t box[3] = {256, (cuuint32_t)cores, (cuuint32_t)slices};
+      const cuuint32_t es[3] = {1, 1, 1};
+      return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, arena_ + off, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    for (size_t i = 0; i < host.size() && ok; ++i) {
+      const OzProb& t = tp[i];
+      if (t.tiles == 0) continue;
+      ok = make(&maps[3 * i + 0], t.a_pack, t.a_rc, t.ks, TM / 8, SH) &&
+           make(&maps[3 * i + 1], t.a_pack, t.a_rc, t.ks, TM / 8, S - SH) &&
+           make(&maps[3 * i + 2], t.b_pack, t.b_rc, t.ks, TN / 8, S);
+    }
+    if (ok) {
+      SH_CUDA_CHECK(dev_malloc(&d_tmaps_, maps.size() * sizeof(CUtensorMap)));
+      SH_CUDA_CHECK(cudaMemcpy(d_tmaps_, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    }
+  }
   if (nred_ > 0) {
     SH_CUDA_CHECK(dev_malloc(&ws_, wsz * sizeof(double)));
     SH_CUDA_CHECK(dev_malloc(&d_rbegin_, rbegin.size() * sizeof(int64_t)));
@@ -706,8 +1028,19 @@ int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
     cached_valid_ = true;
   }
   if ((rc = launch_pack(sets_[0], s, mask))) return rc;
-  k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_,
-                                                                              (int)host.size(), mask, arena_, exps_, ws_);
+  static const bool persist = [] {
+    const char* e = std::getenv("SHAMPOO_OZ_PERSIST");
+    return e ? std::atoi(e) != 0 : false;  // measured slower (one producer per SM): kept for experiments
+  }();
+  if (persist) {
+    const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
+    k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_, (int)host.size(),
+                                                                 total_items_, mask, arena_, exps_, ws_);
+  } else {
+    k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(
+        d_prob_, d_tp_, d_begin_, (int)host.size(), mask, arena_, exps_, ws_,
+        static_cast<const CUtensorMap*>(d_tmaps_));
+  }
   SH_LAUNCH_CHECK();
   if (total_red_ > 0) {
     k_oz_reduce<T><<<(unsigned)total_red_, 256, 0, s>>>(d_prob_, d_tp_, d_rbegin_, d_rprob_, nred_, mask, ws_);

@@ -104,6 +104,7 @@ class OzakiGemmBatch {
   int8_t* arena_ = nullptr;        // packed slice planes
   int32_t* exps_ = nullptr;        // row exponents
   double* ws_ = nullptr;           // split-K partial tiles
+  void* d_tmaps_ = nullptr;        // per problem 3 TMA tensor maps (A first/second slice half, B)
   int64_t total_items_ = 0, total_red_ = 0;
   int nred_ = 0;
   double mma_count_ = 0;
