@@ -575,7 +575,8 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
                                                                const int64_t* __restrict__ begin, int nprob,
                                                                int64_t total_items, const int32_t* __restrict__ mask,
                                                                const int8_t* __restrict__ arena,
-                                                               const int32_t* __restrict__ exps, double* __restrict__ ws) {
+                                                               const int32_t* __restrict__ exps, double* __restrict__ ws,
+                                                               const CUtensorMap* __restrict__ tmaps) {
   using Cfg = OzCfg<S>;
   using PC = OzPCfg<S>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
@@ -629,6 +630,16 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
           if (g >= (uint32_t)PC::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
           uint8_t* sb = sbase + (size_t)st * PC::STAGE;
           constexpr int SH = (S + 1) / 2;
+          if (tmaps) {
+            const CUtensorMap* tm3 = tmaps + 3 * it.pi;
+            const int z = (it.s0 + k) * S;
+            mbar_expect_tx(&full_bar[st][0], (uint32_t)(S * (TN / 8) * 256 + SH * (TM / 8) * 256));
+            mbar_expect_tx(&full_bar[st][1], (uint32_t)((S - SH) * (TM / 8) * 256));
+            tma_load_3d(sb + Cfg::A_BYTES, tm3 + 2, 0, it.tn * (TN / 8), z, &full_bar[st][0]);
+            tma_load_3d(sb, tm3 + 0, 0, it.tm * (TM / 8), z, &full_bar[st][0]);
+            tma_load_3d(sb + SH * (TM / 8) * 256, tm3 + 1, 0, it.tm * (TM / 8), z + SH, &full_bar[st][1]);
+            continue;
+          }
           mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
           mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
           const int8_t* as = a_src + (int64_t)k * S * a_plane;
@@ -1035,7 +1046,8 @@ int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   if (persist) {
     const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
     k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_, (int)host.size(),
-                                                                 total_items_, mask, arena_, exps_, ws_);
+                                                                 total_items_, mask, arena_, exps_, ws_,
+                                                                 static_cast<const CUtensorMap*>(d_tmaps_));
   } else {
     k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(
         d_prob_, d_tp_, d_begin_, (int)host.size(), mask, arena_, exps_, ws_,
