@@ -227,11 +227,13 @@ def run_ours(args):
     gen = torch.Generator(device=dev)
     gen.manual_seed(0)
     params = [torch.randn(s, generator=gen, device=dev) * 0.05 for s in shapes]
-    # fresh N(0, 0.01^2) gradients for every step of the warm-up and the timed window,
-    # generated before timing and resident in HBM (~0.1 GB per step); later windows reuse them cyclically
+    # fresh N(0, 0.01^2) gradients for every step of the warm-up, the timed window, the per-phase
+    # window and the e2e window: W + 3K distinct sets generated before timing and
+    # resident in HBM (~0.1 GB per step).  A reused gradient makes the factors rank deficient below
+    # their structural rank (and the refresh slower than in training), so no window repeats one.
     pool = []
     gen.manual_seed(1 + rank * 0)  # identical gradients on every rank (no DDP all-reduce modelled)
-    for _ in range(args.warmup + args.steps):
+    for _ in range(args.warmup + 3 * args.steps):
         pool.append([torch.randn(s, generator=gen, device=dev) * 1e-2 for s in shapes])
     npool = len(pool)
     cfg = P.ShampooConfig(grafting=P.GraftKind.ADAGRAD, precision=args.precision, **CFG)
@@ -368,13 +370,29 @@ def run_ours(args):
                 "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()}, "kernels": kernels,
                 "sum_n3_G": round(n3.value / 1e9, 2)}
 
-    # e2e through the public API with host buffers: pinned H2D of grads, step, D2H of params, over
-    # the same number of steps as the timed window (so it contains one refresh, like `value`)
+    # e2e through the public API with host buffers: every step's gradients H2D from pinned host memory
+    # and every step's updated parameters D2H, over the same number of steps as the timed window (so
+    # it contains one refresh, like `value`).  Double-buffered input pipeline: step k+1's gradients
+    # are copied on an H2D stream while step k computes; step k's parameters are snapshotted on the
+    # device (D2D) and read back on a D2H stream while step k+1 computes.  All copies complete inside
+    # the timed region (the end event waits for the last D2H).
     e2e = None
     if not args.skip_e2e:
-        host_grads = [[g.cpu().pin_memory() for g in pool[i]] for i in range(4)]
-        host_params = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
-        dev_grads = [torch.empty_like(p) for p in params]
+        t_e2e = opt.step_count  # the e2e window's gradients: the host copies of pool[t_e2e ...]
+        # each step's gradients as ONE flat pinned host buffer (one H2D copy per step: 161 small copies
+        # cost ~50% more copy-engine time); the device views of a flat buffer are what step() gets
+        numels = [math.prod(s_) for s_ in shapes]
+        host_grads = [torch.cat([g.reshape(-1) for g in pool[(t_e2e + k) % npool]]).cpu().pin_memory()
+                      for k in range(args.steps)]
+        host_params = torch.empty(n_params, dtype=torch.float32).pin_memory()
+        dev_flat = [torch.empty(n_params, dtype=torch.float32, device=dev) for _ in range(2)]
+        dev_grads = [[v.view(s_) for v, s_ in zip(torch.split(f, numels), shapes)] for f in dev_flat]
+        snap_flat = torch.empty(n_params, dtype=torch.float32, device=dev)
+        snap = [v.view(s_) for v, s_ in zip(torch.split(snap_flat, numels), shapes)]
+        h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_used = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_snap, ev_out = torch.cuda.Event(), torch.cuda.Event()
         e2e_steps = args.steps
         e2e_refresh = 0
         if world > 1:
@@ -382,14 +400,34 @@ def run_ours(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+
+        def upload(k, b):
+            with torch.cuda.stream(h2d):
+                h2d.wait_event(e0)
+                if k >= 2:
+                    h2d.wait_event(ev_used[b])  # step k-2 finished reading this buffer
+                dev_flat[b].copy_(host_grads[k], non_blocking=True)
+                ev_in[b].record(h2d)
+
+        upload(0, 0)
         for k in range(e2e_steps):
+            b = k % 2
+            if k + 1 < e2e_steps:
+                upload(k + 1, 1 - b)
             if opt.step_count % cfg.precondition_frequency == 0:
                 e2e_refresh += 1
-            for d, h in zip(dev_grads, host_grads[k % 4]):
-                d.copy_(h, non_blocking=True)
-            opt.step(dev_grads)
-            for h, p in zip(host_params, opt.params()):
-                h.copy_(p, non_blocking=True)
+            stream.wait_event(ev_in[b])
+            opt.step(dev_grads[b])
+            ev_used[b].record(stream)
+            if k > 0:
+                stream.wait_event(ev_out)  # the previous read-back finished with the snapshot
+            torch._foreach_copy_(snap, list(opt.params()))  # device snapshot (D2D), read back below
+            ev_snap.record(stream)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_snap)
+                host_params.copy_(snap_flat, non_blocking=True)
+                ev_out.record(d2h)
+        stream.wait_event(ev_out)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -399,7 +437,8 @@ def run_ours(args):
             e2e_ms = float(tt.item())
         e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": 4 * n_params,
                "d2h_bytes_per_step": 4 * n_params, "steps": e2e_steps, "refresh_steps": e2e_refresh,
-               "note": "Shampoo.step with pinned H2D copies of the gradients and D2H of all parameters each step"}
+               "note": "Shampoo.step with pinned H2D copies of the gradients and D2H of all parameters each "
+                       "step; double-buffered (H2D of step k+1 and D2H of step k overlap step k+1's compute)"}
 
     # Adam baseline on the same shapes
     adam_ms = None
@@ -438,7 +477,7 @@ def run_ours(args):
                            "epsilon": 1e-12, "refresh_steps_in_window": refresh_steps,
                            "parallelism": f"dp{world} (block-sharded, all-gather)",
                            "l2": "state (factors+inverses ~2 GB) >> 126 MB L2; no flush needed",
-                           "gradients": "fresh N(0, 0.01^2) fp32 per step (W+K distinct sets resident in HBM)"},
+                           "gradients": "fresh N(0, 0.01^2) fp32 per step (W+3K distinct sets resident in HBM: no window reuses one)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "host_ms_per_step": round(1e3 * host_s / args.steps, 3),
                 "clocks": clk.summary(), "adam_fused_ms": round(adam_ms, 4) if adam_ms else None,
