@@ -1,5 +1,6 @@
-"""Bench workload up to the t=50 refresh (for ncu launch lists of one refresh: use -s to skip t<50)."""
-import os, sys
+"""Bench workload up to the t=50 refresh; the last step (the refresh) is bracketed by cuProfilerStart/Stop
+(ncu --profile-from-start off captures only it)."""
+import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2309_06497_b200 as P
@@ -18,8 +19,8 @@ opt = P.Shampoo(params, cfg)
 for t in range(T):
     if t == T - 1:
         torch.cuda.synchronize()
-        torch.cuda.cudart().cudaProfilerStart()
+        ctypes.CDLL("libcuda.so.1").cuProfilerStart()
     opt.step(pool[t])
 torch.cuda.synchronize()
-torch.cuda.cudart().cudaProfilerStop()
+ctypes.CDLL("libcuda.so.1").cuProfilerStop()
 print("done", opt.guard_stats)
