@@ -157,6 +157,10 @@ struct shampoo_ctx {
   std::vector<int32_t> job_block[kRootGroups];  // root-inverse job -> owned local block
   cudaStream_t side[kRootGroups] = {};          // side[0] unused (group 0 runs on the caller's stream)
   cudaEvent_t ev_fork = nullptr, ev_join[kRootGroups] = {};
+  // plain steps: the statistics GEMMs run on side[1] concurrently with precondition/graft/apply
+  // (they read only G; the factors they write are read again only at the next refresh)
+  cudaEvent_t ev_prep = nullptr, ev_stats = nullptr;
+  bool stats_pending = false;
   int64_t guard[4] = {0, 0, 0, 0};
   PhaseTimer timer;
 
@@ -177,6 +181,8 @@ struct shampoo_ctx {
       if (ev_join[g]) cudaEventDestroy(ev_join[g]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_prep) cudaEventDestroy(ev_prep);
+    if (ev_stats) cudaEventDestroy(ev_stats);
   }
   template <typename T>
   Engine<T>& eng() { return *static_cast<Engine<T>*>(engine.get()); }
@@ -576,6 +582,8 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     }
   }
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_prep, cudaEventDisableTiming));
+  SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
   {
     const char* lr = std::getenv("SHAMPOO_EIG_LOWRANK");
     c->low_rank = lr ? std::atoi(lr) != 0 : true;
@@ -614,11 +622,22 @@ int shampoo_check_finite(shampoo_ctx* c, const void* const* grads, int32_t dtype
 }
 
 namespace {
+// Orders the caller's stream after the statistics launched on side[1] (before anything that reads
+// the factors or overwrites G, and at the end of every step).
+int join_stats(shampoo_ctx* c, cudaStream_t s) {
+  if (!c->stats_pending) return SHAMPOO_OK;
+  SH_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_stats, 0));
+  c->stats_pending = false;
+  return SHAMPOO_OK;
+}
+
 // The stats phase; gradients from the caller's tensors (grads) or from a reduced gather-layout
 // buffer (gbuf, context dtype, scaled by gscale).
 int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf, double gscale,
                       const void* const* params, int32_t dtype, int64_t t, cudaStream_t s) {
-  int rc = upload_ptrs(c, grads, params, s);
+  int rc = join_stats(c, s);
+  if (rc) return rc;
+  rc = upload_ptrs(c, grads, params, s);
   if (rc) return rc;
   const int64_t gstep = c->graft_step + 1;  // GraftState.update increments first (grafting.py:71)
   StepScalars sc = make_scalars(c, t, dtype, gstep);
@@ -643,10 +662,22 @@ int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf
               : launch_prepare<double>(1, c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, gp, pp, sc, ar, s);
   if (rc) return rc;
   if ((rc = launch_block_reduce(c->d_cb, c->d_cc, no, c->part, c->pg2, s))) return rc;
-  rc = c->f32 ? c->eng<float>().stats.launch(s) : c->eng<double>().stats.launch(s);
+  // concurrent statistics (not under per-phase timing, where phases must not overlap)
+  const bool concurrent = !c->timer.on && c->side[1] != nullptr;
+  cudaStream_t ss = s;
+  if (concurrent) {
+    SH_CUDA_CHECK(cudaEventRecord(c->ev_prep, s));
+    SH_CUDA_CHECK(cudaStreamWaitEvent(c->side[1], c->ev_prep, 0));
+    ss = c->side[1];
+  }
+  rc = c->f32 ? c->eng<float>().stats.launch(ss) : c->eng<double>().stats.launch(ss);
   if (rc) return rc;
-  rc = c->f32 ? c->eng<float>().stats_thin.launch(s) : c->eng<double>().stats_thin.launch(s);
+  rc = c->f32 ? c->eng<float>().stats_thin.launch(ss) : c->eng<double>().stats_thin.launch(ss);
   if (rc) return rc;
+  if (concurrent) {
+    SH_CUDA_CHECK(cudaEventRecord(c->ev_stats, ss));
+    c->stats_pending = true;
+  }
   if (c->n_fb_chunks) {
     const FallbackArgs fa = fallback_args(c, t);
     rc = c->f32 ? launch_fallback_update<float>(c->d_fb_chunks, c->n_fb_chunks, c->d_blocks, ar, fa,
@@ -701,6 +732,10 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   for (const auto& r : c->rinv) njobs += r.jobs();
   if (njobs == 0) return SHAMPOO_OK;
   const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
+  {
+    const int rj = join_stats(c, s);  // the refresh reads this step's factors
+    if (rj) return rj;
+  }
   PhaseScope scope(&c->timer, 1, s);
   std::vector<int32_t> has_prev[kRootGroups], full_rank[kRootGroups], low_rank[kRootGroups];
   std::vector<LowRankJob> lr_jobs;
@@ -813,9 +848,13 @@ int shampoo_apply(shampoo_ctx* c, void* const* params, int32_t dtype, double lr,
   sc.lr = lr;
   sc.pdtype = dtype;
   void* const* pp = (void* const*)(c->d_ptrs + c->nparams);
-  PhaseScope scope(&c->timer, 4, s);
-  return c->f32 ? launch_apply<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s)
+  {
+    PhaseScope scope(&c->timer, 4, s);
+    rc = c->f32 ? launch_apply<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s)
                 : launch_apply<double>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s);
+  }
+  if (rc) return rc;
+  return join_stats(c, s);  // the step ends with everything it launched ordered before the caller's stream
 }
 
 int shampoo_timing_enable(shampoo_ctx* c, int32_t enable) {
