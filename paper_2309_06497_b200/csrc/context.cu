@@ -161,6 +161,8 @@ struct shampoo_ctx {
   // (they read only G; the factors they write are read again only at the next refresh)
   cudaEvent_t ev_prep = nullptr, ev_stats = nullptr;
   bool stats_pending = false;
+  cudaStream_t lr_stream = nullptr;  // the low-rank path, concurrent with the two root-inverse groups
+  cudaEvent_t ev_lr = nullptr;
   int64_t guard[4] = {0, 0, 0, 0};
   PhaseTimer timer;
 
@@ -182,6 +184,8 @@ struct shampoo_ctx {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_prep) cudaEventDestroy(ev_prep);
+    if (ev_lr) cudaEventDestroy(ev_lr);
+    if (lr_stream) cudaStreamDestroy(lr_stream);
     if (ev_stats) cudaEventDestroy(ev_stats);
   }
   template <typename T>
@@ -583,6 +587,8 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   }
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_prep, cudaEventDisableTiming));
+  SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_lr, cudaEventDisableTiming));
+  SH_CUDA_CHECK(cudaStreamCreateWithFlags(&c->lr_stream, cudaStreamNonBlocking));
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
   {
     const char* lr = std::getenv("SHAMPOO_EIG_LOWRANK");
@@ -767,14 +773,20 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
       }
     }
   }
-  if (!lr_jobs.empty()) {
-    int64_t lstats[4] = {0, 0, 0, 0};
-    int rl = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, s, lstats);
-    if (rl) return rl;
-    for (int q = 0; q < 4; ++q) c->guard[q] += lstats[q];
-  }
-  // group g > 0 on side stream g (after everything already queued on s), group 0 on s
+  // group g > 0 on side stream g, the low-rank jobs on lr_stream (each after everything already
+  // queued on s, each driven by its own host thread), group 0 on s; the groups skip the low-rank jobs
   SH_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
+  int64_t lstats[4] = {0, 0, 0, 0};
+  int lrc = SHAMPOO_OK;
+  std::string lerr;
+  std::thread lr_thread;
+  if (!lr_jobs.empty()) {
+    SH_CUDA_CHECK(cudaStreamWaitEvent(c->lr_stream, c->ev_fork, 0));
+    lr_thread = std::thread([&] {
+      lrc = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, c->lr_stream, lstats);
+      if (lrc) lerr = shampoo_last_error();
+    });
+  }
   int64_t gstats[kRootGroups][4] = {};
   int grc[kRootGroups] = {};
   std::string gerr[kRootGroups];
@@ -791,6 +803,16 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   }
   solve(0, s);
   for (auto& th : threads) th.join();
+  if (lr_thread.joinable()) {
+    lr_thread.join();
+    SH_CUDA_CHECK(cudaEventRecord(c->ev_lr, c->lr_stream));
+    SH_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_lr, 0));
+    if (lrc) {
+      set_error(lerr);
+      return lrc;
+    }
+    for (int q = 0; q < 4; ++q) c->guard[q] += lstats[q];
+  }
   for (int g = 1; g < kRootGroups; ++g) {
     SH_CUDA_CHECK(cudaEventRecord(c->ev_join[g], c->side[g]));
     SH_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_join[g], 0));

@@ -25,7 +25,8 @@ constexpr int64_t kSplitChunk = 2048;
 
 __device__ __forceinline__ int64_t ev(const Idx2& x, int32_t v) {
   if (x.div == 0x7fffffff) return (int64_t)v * x.lo;
-  return (int64_t)(v / x.div) * x.hi + (int64_t)(v % x.div) * x.lo;
+  const uint32_t q = (uint32_t)v / (uint32_t)x.div;
+  return (int64_t)q * x.hi + (int64_t)((uint32_t)v - q * (uint32_t)x.div) * x.lo;
 }
 
 __device__ __forceinline__ void tri_index(int64_t l, int& tm, int& tn) {

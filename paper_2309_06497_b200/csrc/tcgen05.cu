@@ -39,7 +39,8 @@ struct OzCfg {
 
 __device__ __forceinline__ int64_t evx(const Idx2& x, int64_t v) {
   if (x.div == 0x7fffffff) return v * x.lo;
-  return (v / x.div) * x.hi + (v % x.div) * x.lo;
+  const uint32_t q = (uint32_t)v / (uint32_t)x.div;  // indices are < 2^31: 32-bit division
+  return (int64_t)q * x.hi + (int64_t)((uint32_t)v - q * (uint32_t)x.div) * x.lo;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

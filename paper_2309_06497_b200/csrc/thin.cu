@@ -14,7 +14,8 @@ constexpr int KOUT_ITEMS = 2048;  // outputs per CTA of the small-K kernel
 
 __device__ __forceinline__ int64_t ev(const Idx2& x, int64_t v) {
   if (x.div == 0x7fffffff) return v * x.lo;
-  return (v / x.div) * x.hi + (v % x.div) * x.lo;
+  const uint32_t q = (uint32_t)v / (uint32_t)x.div;  // indices are < 2^31: 32-bit division
+  return (int64_t)q * x.hi + (int64_t)((uint32_t)v - q * (uint32_t)x.div) * x.lo;
 }
 
 __device__ __forceinline__ int find64(const int64_t* __restrict__ begin, int n, int64_t x) {
