@@ -46,6 +46,7 @@ constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi swe
 // 5 + log(kappa_max) / (p log((p+1)/p)) iterations are left to the Jacobi path.
 constexpr double kHybridNewtonKappa = 5e6;
 constexpr int kPowerIters = 12;  // power-iteration steps for the pre-pass scaling (k_pow_*)
+constexpr double kNewtonFinalRes = 3e-7;  // residual after which one X <- X T finishes (hybrid pre-pass)
 
 constexpr double U64 = 1.1102230246251565e-16;
 
@@ -1263,6 +1264,7 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
     N.best = INFINITY;
     N.iters = 0;
     N.converged = 0;
+    N.fin = 0;
   }
 }
 
@@ -1311,13 +1313,21 @@ __global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restri
 }
 
 // Residual part 2 (thread per job): best-iterate tracking and the stopping rule r < max(tol, tol_n n).
-__global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int njobs, unsigned long long* resbits, double tol,
-                               double tol_n, int32_t* improved, int32_t* count) {
+__global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int32_t* mask2, int njobs, unsigned long long* resbits,
+                               double tol, double tol_n, int32_t* improved, int32_t* count) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= njobs) return;
   improved[j] = 0;
   if (!mask[j]) return;
   NewtonJob& N = nj[j];
+  if (N.fin) {  // the final X <- X T of a converging job (no T^p / M this iteration)
+    N.iters += 1;
+    N.converged = 1;
+    improved[j] = 1;
+    mask[j] = 0;
+    mask2[j] = 0;
+    return;
+  }
   const double r = __longlong_as_double((long long)resbits[j]);
   resbits[j] = 0ull;
   N.iters += 1;
@@ -1334,7 +1344,13 @@ __global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int njobs, unsigned
     mask[j] = 0;
   } else if (N.iters >= 1000 || (tol_n > 0.0 && N.iters >= N.cap)) {
     mask[j] = 0;
+  } else if (tol_n > 0.0 && r < kNewtonFinalRes) {
+    // quadratic convergence: ||M_{k+1} - I|| ~ (p+1)/(2p) ||M_k - I||^2 < 1e-13 -- only X_{k+1}
+    // is still needed (the hybrid pre-pass; the reference-semantics NEWTON solver keeps its count)
+    N.fin = 1;
+    mask2[j] = 0;
   }
+  if (!mask[j]) mask2[j] = 0;
   if (mask[j]) atomicAdd(count, 1);
 }
 
@@ -1467,6 +1483,7 @@ RootInverseBatch::~RootInverseBatch() {
   dev_free(d_newton_);
   dev_free(d_resbits_);
   dev_free(d_improved_);
+  dev_free(d_mask2_);
   dev_free(d_pair_begin_);
   dev_free(d_item_begin_);
   dev_free(d_elem_begin_);
@@ -1800,6 +1817,7 @@ int RootInverseBatch::build_newton() {
   SH_CUDA_CHECK(dev_malloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(cudaMemset(d_resbits_, 0, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(dev_malloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_mask2_, std::max(nj, 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_newton_, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice));
   // GEMM sets for cur = 0/1: X_nxt = X_cur T ; T^p ; M_nxt = T^p M_cur (tcgen05 Ozaki, FP64 class)
   size_t nsteps = 0;
@@ -1870,6 +1888,8 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
   k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, cand,
                                                    hybrid ? 1 : 0);
   SH_LAUNCH_CHECK();
+  int32_t* mask2 = d_mask2_;
+  SH_CUDA_CHECK(cudaMemcpyAsync(mask2, mask, nj * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   prof_mark("nw_init");
   int cur = 0;
   for (int it = 1; it <= budget; ++it) {
@@ -1879,16 +1899,16 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     if ((rc = newton_x_[cur].launch(s, mask))) return rc;
     prof_mark("nw_gemm_x");
     for (auto& p : newton_pow_)
-      if ((rc = p->launch(s, mask))) return rc;
+      if ((rc = p->launch(s, mask2))) return rc;
     prof_mark("nw_gemm_pow");
-    if ((rc = newton_m_[cur].launch(s, mask))) return rc;
+    if ((rc = newton_m_[cur].launch(s, mask2))) return rc;
     prof_mark("nw_gemm_m");
     SH_CUDA_CHECK(cudaMemsetAsync(d_count_, 0, sizeof(int32_t), s));
-    k_newton_rowmax<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, total_elem_chunks_, nx_, cur ^ 1,
+    k_newton_rowmax<<<total_elem_chunks_, 256, 0, s>>>(dn, mask2, d_elem_begin_, nj, total_elem_chunks_, nx_, cur ^ 1,
                                                        d_resbits_);
     SH_LAUNCH_CHECK();
-    k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, nj, d_resbits_, tol, hybrid ? kHybridNewtonTolN : 0.0,
-                                                    d_improved_, d_count_);
+    k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, mask2, nj, d_resbits_, tol,
+                                                    hybrid ? kHybridNewtonTolN : 0.0, d_improved_, d_count_);
     SH_LAUNCH_CHECK();
     k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
     SH_LAUNCH_CHECK();

@@ -64,7 +64,7 @@ struct NewtonJob {
   double best;
   int32_t iters, converged;
   int32_t cap;  // hybrid pre-pass: iteration cap (conditioning gate, kHybridNewtonKappa)
-  int32_t pad;
+  int32_t fin;  // hybrid pre-pass: residual small enough that one more X <- X T is final
   double lam;   // hybrid pre-pass: power-iteration estimate of lambda_max(A) (scales X0, M0)
 };
 
@@ -143,6 +143,7 @@ class RootInverseBatch {
   NewtonJob* d_newton_ = nullptr;
   unsigned long long* d_resbits_ = nullptr;  // per job max row sum of |M - I| (bit pattern)
   int32_t* d_improved_ = nullptr;
+  int32_t* d_mask2_ = nullptr;  // Newton: jobs that still need T^p and M (not in their final step)
   bool newton_built_ = false;
   OzakiGemmBatch<double> newton_x_[2], newton_m_[2];
   std::vector<std::unique_ptr<OzakiGemmBatch<double>>> newton_pow_;
