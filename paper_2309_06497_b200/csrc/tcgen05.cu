@@ -261,6 +261,56 @@ __device__ __forceinline__ void ozaki_slices(double x, int e, int8_t (&q)[S]) {
   q[S - 1] = (int8_t)(neg ? -last : last);
 }
 
+// The same slices as ozaki_slices, split for packing: the magnitude digits 0..S-2 are bit fields of
+// `top`, the rounded last digit is `last`, the sign `neg` (applied per byte after packing).
+template <int S>
+__device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& top, uint32_t& last, uint32_t& neg) {
+  constexpr int G = 7;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int bexp = (int)((bits >> 52) & 0x7ff);
+  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
+  if (bexp) m |= 1ull << 52;
+  const int sh = (bexp ? bexp : 1) - 1075 - e + 7 * S + G;
+  unsigned long long yg;
+  bool sticky;
+  if (sh >= 0) {
+    yg = m << sh;
+    sticky = false;
+  } else if (sh > -64) {
+    yg = m >> (-sh);
+    sticky = (m & ((1ull << (-sh)) - 1ull)) != 0ull;
+  } else {
+    yg = 0ull;
+    sticky = m != 0ull;
+  }
+  top = yg >> G;
+  const unsigned frac = (unsigned)(yg & ((1u << G) - 1u)), half = 1u << (G - 1);
+  uint32_t l = (uint32_t)(top & 127ull);
+  if (frac > half || (frac == half && (sticky || (l & 1u)))) ++l;
+  last = l > 127u ? 127u : l;
+  neg = (uint32_t)(bits >> 63);
+}
+
+// Four consecutive elements -> S words of packed int8 slices (byte i = element i): magnitudes
+// gathered with byte permutes, the signs applied per byte (two's complement: (v ^ m) - m).
+template <int S>
+__device__ __forceinline__ void ozaki_pack4(const double (&x)[4], int e, uint32_t (&w)[S]) {
+  unsigned long long t[4];
+  uint32_t l[4], n[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ozaki_mag<S>(x[i], e, t[i], l[i], n[i]);
+  const uint32_t msk = (n[0] ? 0x000000FFu : 0u) | (n[1] ? 0x0000FF00u : 0u) | (n[2] ? 0x00FF0000u : 0u) |
+                       (n[3] ? 0xFF000000u : 0u);
+#pragma unroll
+  for (int sl = 0; sl < S; ++sl) {
+    uint32_t b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = (sl + 1 < S) ? ((uint32_t)(t[i] >> (7 * (S - 1 - sl))) & 127u) : l[i];
+    const uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    w[sl] = __vsub4(word ^ msk, msk);
+  }
+}
+
 // Operands -> int8 slice planes, slice-major per stage: byte offset
 // ((stage * S + s) * rc + core) * 256 + kc * 128 + r8 * 16 holds row 8 core + r8,
 // k = 32 stage + 16 kc .. +15 of slice s.  Unit u = ((stage * rc + core) * 2 + kc) * 8 + r8.
@@ -288,15 +338,23 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
     const T* __restrict__ src = static_cast<const T*>(J.src);
     const int64_t rb = evx(J.r, row);
     const int e = max(exps[J.exp + row], kExpFloor);
+    const Idx2 kx = J.k;
     double xv[16];
+    if (kx.div == 0x7fffffff) {  // one stride along k (the common case): no per-element index map
+      const T* rp = src + rb + (int64_t)k0 * kx.lo;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(J.k, k0 + i)] : 0.0;
+      for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)rp[(int64_t)i * kx.lo] : 0.0;
+    } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      int8_t q[S];
-      ozaki_slices<S>(xv[i], e, q);
+      for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
+    }
 #pragma unroll
-      for (int s = 0; s < S; ++s) w[s][i >> 2] |= ((uint32_t)(uint8_t)q[s]) << (8 * (i & 3));
+    for (int g = 0; g < 4; ++g) {
+      const double x4[4] = {xv[4 * g], xv[4 * g + 1], xv[4 * g + 2], xv[4 * g + 3]};
+      uint32_t ws[S];
+      ozaki_pack4<S>(x4, e, ws);
+#pragma unroll
+      for (int s = 0; s < S; ++s) w[s][g] = ws[s];
     }
   }
   int8_t* dst = arena + J.dst + ((int64_t)stage * S * J.rc + core) * 256 + kc * 128 + r8 * 16;
