@@ -1946,7 +1946,7 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   for (int j = 0; j < nj; ++j) {
     const bool sk = skip && (*skip)[j];
     any_skip |= sk;
-    cand[j] = (!sk && hybrid && host_[j].m > 0 && (!newton_hint || (*newton_hint)[j])) ? 1 : 0;
+    cand[j] = (!sk && hybrid && host_[j].n >= 8 && (!newton_hint || (*newton_hint)[j])) ? 1 : 0;
     any_cand |= cand[j] != 0;
     warm[j] = (!sk && allow_warm && solver == SHAMPOO_SOLVER_EIGH && host_[j].m > 0 && vec_valid_[j] && !cand[j]) ? 1
                                                                                                               : 0;
