@@ -63,43 +63,62 @@ __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restric
     inv_norm = n2 > 0.0 ? 1.0 / sqrt(n2) : 1.0;
   }
   double acc = 0.0;
-  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
-    const int64_t j = c.start + e;
-    T g;
-    if (pass == 0 || !normalized) {
-      if (sc.gbuf) {  // reduced gradient: this block's slice of the gather-layout buffer
-        g = T(sc.gscale * (double)static_cast<const T*>(ar.GBUF)[B.gofs + j]);
-        if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
+  // U elements per thread per iteration: every load of the batch is issued before the first store
+  // (the state arrays may alias the caller's pointers as far as the compiler knows), same element
+  // order as a plain strided loop, so the partial sums are unchanged
+  constexpr int U = 4;
+  for (int64_t e0 = threadIdx.x; e0 < c.count; e0 += U * NT) {
+    T gq[U], aq[U], fq[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * NT;
+      gq[u] = aq[u] = fq[u] = T(0);
+      if (e >= c.count) continue;
+      const int64_t j = c.start + e;
+      if (pass == 0 || !normalized) {
+        if (sc.gbuf) {  // reduced gradient: this block's slice of the gather-layout buffer
+          gq[u] = T(sc.gscale * (double)static_cast<const T*>(ar.GBUF)[B.gofs + j]);
+          if (sc.l2) gq[u] += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
+        } else {
+          const int64_t po = block_to_param_offset(B, j);
+          gq[u] = load_as<T>(gp, po, sc.pdtype);
+          if (sc.l2) gq[u] += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
+        }
       } else {
-        const int64_t po = block_to_param_offset(B, j);
-        g = load_as<T>(gp, po, sc.pdtype);
-        if (sc.l2) g += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
+        gq[u] = G[j];
       }
-      G[j] = g;
-    } else {
-      g = G[j];
+      if (pass != 0 && sc.graft != SHAMPOO_GRAFT_SGD) aq[u] = GA[j];
+      if (pass != 0 && sc.use_filter) fq[u] = F[j];
     }
-    if (pass == 0) {
-      acc += (double)g * (double)g;
-      continue;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * NT;
+      if (e >= c.count) continue;
+      const int64_t j = c.start + e;
+      const T g = gq[u];
+      if (pass == 0 || !normalized) G[j] = g;
+      if (pass == 0) {
+        acc += (double)g * (double)g;
+        continue;
+      }
+      T a = T(0);
+      if (sc.graft != SHAMPOO_GRAFT_SGD) {
+        const T gg = normalized ? T((double)g * inv_norm) : g;
+        const T sq = gg * gg;
+        a = aq[u];
+        a = graft_summed(sc.graft) ? a + sq : T(sc.beta2g) * a + T(sc.one_minus_beta2g) * sq;
+        GA[j] = a;
+      }
+      T ge = g;
+      if (sc.use_filter) {
+        const T f = T(sc.beta1) * fq[u] + T(sc.one_minus_beta1) * g;
+        F[j] = f;
+        ge = f * T(sc.inv_bc1);
+        GE[j] = ge;
+      }
+      const T pg = graft_dir<T>(sc.graft, ge, a, sc.inv_bc2g, sc.graft_eps);
+      acc += (double)pg * (double)pg;
     }
-    T a = T(0);
-    if (sc.graft != SHAMPOO_GRAFT_SGD) {
-      const T gg = normalized ? T((double)g * inv_norm) : g;
-      const T sq = gg * gg;
-      a = GA[j];
-      a = graft_summed(sc.graft) ? a + sq : T(sc.beta2g) * a + T(sc.one_minus_beta2g) * sq;
-      GA[j] = a;
-    }
-    T ge = g;
-    if (sc.use_filter) {
-      const T f = T(sc.beta1) * F[j] + T(sc.one_minus_beta1) * g;
-      F[j] = f;
-      ge = f * T(sc.inv_bc1);
-      GE[j] = ge;
-    }
-    const T pg = graft_dir<T>(sc.graft, ge, a, sc.inv_bc2g, sc.graft_eps);
-    acc += (double)pg * (double)pg;
   }
   acc = block_sum<double, NT>(acc, red);
   if (threadIdx.x == 0) ar.part[blockIdx.x] = acc;
@@ -152,22 +171,38 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
     ps_zero = (n2 == 0.0);
     if (!ps_zero) ratio = sqrt(ar.pg2[B.local]) / sqrt(n2);  // grafting.py:95-110
   }
-  for (int64_t e = threadIdx.x; e < c.count; e += NT) {
-    const int64_t j = c.start + e;
-    T p;
-    if (use_ps && !ps_zero) {
-      p = T(ratio * (double)PS[j]);
-    } else {
-      const T a = sc.graft != SHAMPOO_GRAFT_SGD ? GA[j] : T(0);
-      p = graft_dir<T>(sc.graft, G[j], a, sc.inv_bc2g, sc.graft_eps);
+  constexpr int U = 4;  // loads of U elements before their stores (see k_prepare)
+  for (int64_t e0 = threadIdx.x; e0 < c.count; e0 += U * NT) {
+    T pq[U], aq[U], wq[U], mq[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * NT;
+      pq[u] = aq[u] = wq[u] = mq[u] = T(0);
+      if (e >= c.count) continue;
+      const int64_t j = c.start + e;
+      if (use_ps && !ps_zero) {
+        pq[u] = PS[j];
+      } else {
+        pq[u] = G[j];
+        if (sc.graft != SHAMPOO_GRAFT_SGD) aq[u] = GA[j];
+      }
+      if (sc.decoupled) wq[u] = load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
+      if (sc.momentum > 0.0) mq[u] = M[j];
     }
-    if (sc.decoupled) p += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
-    if (sc.momentum > 0.0) {
-      const T m = T(sc.momentum) * M[j] + p;
-      M[j] = m;
-      p = sc.nesterov ? T(sc.momentum) * m + p : m;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * NT;
+      if (e >= c.count) continue;
+      const int64_t j = c.start + e;
+      T p = (use_ps && !ps_zero) ? T(ratio * (double)pq[u]) : graft_dir<T>(sc.graft, pq[u], aq[u], sc.inv_bc2g, sc.graft_eps);
+      if (sc.decoupled) p += T(sc.weight_decay) * wq[u];
+      if (sc.momentum > 0.0) {
+        const T m = T(sc.momentum) * mq[u] + p;
+        M[j] = m;
+        p = sc.nesterov ? T(sc.momentum) * m + p : m;
+      }
+      out[j] = p;
     }
-    out[j] = p;
   }
 }
 
