@@ -45,7 +45,7 @@ constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi swe
 // ((p+1)/p)^p per linear-phase iteration, then ~5 quadratic ones.  Jobs that need more than
 // 5 + log(kappa_max) / (p log((p+1)/p)) iterations are left to the Jacobi path.
 constexpr double kHybridNewtonKappa = 5e6;
-constexpr int kPowerIters = 12;  // power-iteration steps for the pre-pass scaling (k_pow_*)
+constexpr int kPowerIters = 8;  // power-iteration steps for the pre-pass scaling (k_pow_*)
 constexpr double kNewtonFinalRes = 3e-7;  // residual after which one X <- X T finishes (hybrid pre-pass)
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -1233,7 +1233,7 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
     // zero matrix: eps^(-1/p) I (matfun.py:182-188)
     const double v = eps > 0.0 ? pow(eps, -1.0 / J.root_p) : 0.0;
     for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x)
-      XB[e] = (e / n == e % n) ? v : 0.0;
+      XB[e] = X0[e] = (e / n == e % n) ? v : 0.0;  // X0 too: the hybrid finish reads buffer (iters & 1)
     if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) {
       mask[j] = 0;
       N.converged = eps > 0.0;
@@ -1381,7 +1381,9 @@ __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict
   if (st[j].status != kEigOk || (cand && !cand[j]) || (only_converged && !N.converged)) return;
   const int n = J.n;
   const int64_t tot = (int64_t)n * n;
-  const double* XB = nx + N.off + 7 * tot;
+  // hybrid pre-pass: only converged jobs are used and their last iterate is the best one, kept in
+  // the X ping-pong buffer (iters & 1) (no per-iteration best copy); NEWTON solver: Xbest
+  const double* XB = nx + N.off + (only_converged ? (int64_t)(N.iters & 1) : 7) * tot;
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     const int64_t i = e / n, k = e % n;
@@ -1910,8 +1912,10 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, mask2, nj, d_resbits_, tol,
                                                     hybrid ? kHybridNewtonTolN : 0.0, d_improved_, d_count_);
     SH_LAUNCH_CHECK();
-    k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
-    SH_LAUNCH_CHECK();
+    if (!hybrid) {
+      k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
+      SH_LAUNCH_CHECK();
+    }
     cur ^= 1;
     prof_mark("nw_misc");
     if ((it & 3) == 0 || it < 4 || (hybrid && it >= 6)) {
