@@ -1486,6 +1486,7 @@ RootInverseBatch::~RootInverseBatch() {
   dev_free(d_resbits_);
   dev_free(d_improved_);
   dev_free(d_mask2_);
+  dev_free(pack_arena_);
   dev_free(d_pair_begin_);
   dev_free(d_item_begin_);
   dev_free(d_elem_begin_);
@@ -1592,6 +1593,17 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     p.mask_index = (int32_t)j;
     recon_.add(p);
   }
+  // every Ozaki GEMM set of this batch (recon, Rayleigh-Ritz, warm start, Newton) runs in sequence
+  // on one stream: they share one pack space sized for two n x n operands per job
+  pack_cap_ = 0;
+  for (const RootJob& J : host_) {
+    const int64_t ks = (J.n + 31) / 32, rc = (J.n + 7) / 8;
+    pack_cap_ += 2 * ks * rc * OzakiGemmBatch<double>::S * 256;
+  }
+  SH_CUDA_CHECK(dev_malloc(&pack_arena_, std::max<int64_t>(pack_cap_, 256)));
+  for (auto* b : {&recon_, &rr_, &warm1_, &warm2_, &newton_x_[0], &newton_x_[1], &newton_m_[0], &newton_m_[1], &g_wv_,
+                  &g_s1_, &g_v1_, &g_s2_, &g_v2_})
+    b->set_external_arena(pack_arena_, pack_cap_);
   int rc = recon_.upload();
   if (rc) return rc;
   if ((rc = rr_.upload())) return rc;
@@ -1828,7 +1840,10 @@ int RootInverseBatch::build_newton() {
     nsteps = std::max(nsteps, power_plan(host_[j].root_p, &fb).size());
   }
   newton_pow_.clear();
-  for (size_t q = 0; q < nsteps; ++q) newton_pow_.emplace_back(new OzakiGemmBatch<double>());
+  for (size_t q = 0; q < nsteps; ++q) {
+    newton_pow_.emplace_back(new OzakiGemmBatch<double>());
+    newton_pow_.back()->set_external_arena(pack_arena_, pack_cap_);
+  }
   for (int j = 0; j < nj; ++j) {
     const int n = host_[j].n;
     const int64_t tot = (int64_t)n * n;

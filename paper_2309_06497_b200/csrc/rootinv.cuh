@@ -144,6 +144,8 @@ class RootInverseBatch {
   unsigned long long* d_resbits_ = nullptr;  // per job max row sum of |M - I| (bit pattern)
   int32_t* d_improved_ = nullptr;
   int32_t* d_mask2_ = nullptr;  // Newton: jobs that still need T^p and M (not in their final step)
+  int8_t* pack_arena_ = nullptr;  // one pack space for all of this batch's Ozaki GEMM sets (sequential)
+  int64_t pack_cap_ = 0;
   bool newton_built_ = false;
   OzakiGemmBatch<double> newton_x_[2], newton_m_[2];
   std::vector<std::unique_ptr<OzakiGemmBatch<double>>> newton_pow_;

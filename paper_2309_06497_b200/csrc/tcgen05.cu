@@ -906,7 +906,7 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
   }
   dev_free(d_rbegin_);
   dev_free(d_rprob_);
-  dev_free(arena_);
+  if (own_arena_) dev_free(arena_);
   dev_free(exps_);
   dev_free(ws_);
   dev_free(d_tmaps_);
@@ -1016,7 +1016,13 @@ int OzakiGemmBatch<T>::upload() {
   SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemmProblem)));
   SH_CUDA_CHECK(dev_malloc(&d_tp_, tp.size() * sizeof(OzProb)));
   SH_CUDA_CHECK(dev_malloc(&d_begin_, begin.size() * sizeof(int64_t)));
-  SH_CUDA_CHECK(dev_malloc(&arena_, std::max<int64_t>(arena, 256)));
+  if (ext_arena_ && arena <= ext_cap_ && sets_[1].pack_ctas == 0) {
+    arena_ = ext_arena_;
+    own_arena_ = false;
+  } else {
+    SH_CUDA_CHECK(dev_malloc(&arena_, std::max<int64_t>(arena, 256)));
+    own_arena_ = true;
+  }
   SH_CUDA_CHECK(dev_malloc(&exps_, std::max<int64_t>(exp_count[0] + exp_count[1], 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_prob_, host.data(), host.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_tp_, tp.data(), tp.size() * sizeof(OzProb), cudaMemcpyHostToDevice));

@@ -82,6 +82,12 @@ class OzakiGemmBatch {
   // operands flagged kGemmConstA/B (inverse factors: they change once per refresh) are packed
   // on the first launch after upload() or invalidate_cached() only
   void invalidate_cached() { cached_valid_ = false; }
+  // Pack space shared with other batches that are only ever launched one after another on one
+  // stream (no cached operands): used by upload() when large enough, never freed here.
+  void set_external_arena(int8_t* p, int64_t cap) {
+    ext_arena_ = p;
+    ext_cap_ = cap;
+  }
   double flops() const;      // algorithmic 2*M*N*K (SYM counted as full)
   double int8_ops() const;   // executed tensor-core int8 ops
 
@@ -102,6 +108,9 @@ class OzakiGemmBatch {
   int64_t* d_rbegin_ = nullptr;    // reduce tile prefix
   int32_t* d_rprob_ = nullptr;
   int8_t* arena_ = nullptr;        // packed slice planes
+  bool own_arena_ = true;
+  int8_t* ext_arena_ = nullptr;
+  int64_t ext_cap_ = 0;
   int32_t* exps_ = nullptr;        // row exponents
   double* ws_ = nullptr;           // split-K partial tiles
   void* d_tmaps_ = nullptr;        // per problem 3 TMA tensor maps (A first/second slice half, B)
