@@ -71,7 +71,21 @@ cudaError_t dev_malloc_bytes(void** p, size_t bytes) {
     char* base = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMalloc(&base, sz);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {  // give back the slabs that are entirely idle, then retry once
+      cudaGetLastError();
+      for (size_t i = 0; i < H.slabs.size();) {
+        auto it2 = H.free_by_addr.find(H.slabs[i].first);
+        if (it2 != H.free_by_addr.end() && it2->second == H.slabs[i].second) {
+          H.remove_free(it2);
+          cudaFree(H.slabs[i].first);
+          H.slabs.erase(H.slabs.begin() + i);
+        } else {
+          ++i;
+        }
+      }
+      e = cudaMalloc(&base, sz);
+      if (e != cudaSuccess) return e;
+    }
     if (H.log)
       std::fprintf(stderr, "[devmem] slab %zu: %.2f GB in %.1f ms\n", H.slabs.size(), sz / 1e9,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
