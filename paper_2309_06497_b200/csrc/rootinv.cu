@@ -1761,7 +1761,9 @@ int RootInverseBatch::run_eigh(double eta, double eps, cudaStream_t s, std::vect
     }
     k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_, MAX_SWEEPS);
     SH_LAUNCH_CHECK();
-    if ((R & 7) == 7) {
+    // also after round 0: when the Newton pre-pass finished every big job there is nothing left
+    // after the first round (the small jobs are solved inside it)
+    if ((R & 7) == 7 || R == 0) {
       SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SH_CUDA_CHECK(timed_sync(s));
       if (h_count_[0] == 0) break;
