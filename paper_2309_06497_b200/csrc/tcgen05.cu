@@ -202,8 +202,17 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
     if (wu >= (int64_t)J.rows * nkc) return;  // whole warps exit together
     row = (int)(wu / nkc);
     const int k0 = (int)(wu % nkc) * EXP_WARP_CHUNK, k1 = min(J.K, k0 + EXP_WARP_CHUNK);
-    const T* rp = src + evx(J.r, row);
-    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs((double)rp[k]));
+    const T* __restrict__ rp = src + evx(J.r, row);
+    double m1 = 0.0, m2 = 0.0, m3 = 0.0;  // four independent chains: 4 loads in flight per lane
+    int k = k0 + lane;
+    for (; k + 96 < k1; k += 128) {
+      m = fmax(m, fabs((double)rp[k]));
+      m1 = fmax(m1, fabs((double)rp[k + 32]));
+      m2 = fmax(m2, fabs((double)rp[k + 64]));
+      m3 = fmax(m3, fabs((double)rp[k + 96]));
+    }
+    for (; k < k1; k += 32) m = fmax(m, fabs((double)rp[k]));
+    m = fmax(fmax(m, m1), fmax(m2, m3));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane != 0) return;
