@@ -230,47 +230,11 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
   }
 }
 
-// The S signed 7-bit slices of y = x 2^-e (|y| < 1) -- the digits of the fixed-point |y| in base
-// 128 with the sign of x, the last one rounded half-to-even on the remaining bits and clamped to
-// +-127; i.e. exactly  t = 128 y, q = trunc(t), y = t - q  for the first S - 1 slices and
-// q = rint(t) for the last (unbiased truncation of the dropped remainder), computed on the
-// integer mantissa (no FP64 / conversion-pipe work).
-template <int S>
-__device__ __forceinline__ void ozaki_slices(double x, int e, int8_t (&q)[S]) {
-  constexpr int G = 7;  // guard bits below the last slice
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-  const int bexp = (int)((bits >> 52) & 0x7ff);
-  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
-  if (bexp) m |= 1ull << 52;
-  // |x| = m 2^(max(bexp,1) - 1075);  Yg = |y| 2^(7S + G) = m 2^sh
-  const int sh = (bexp ? bexp : 1) - 1075 - e + 7 * S + G;
-  unsigned long long yg;
-  bool sticky;
-  if (sh >= 0) {
-    yg = m << sh;  // |y| < 1 keeps yg < 2^(7S+G) <= 2^63
-    sticky = false;
-  } else if (sh > -64) {
-    yg = m >> (-sh);
-    sticky = (m & ((1ull << (-sh)) - 1ull)) != 0ull;
-  } else {
-    yg = 0ull;
-    sticky = m != 0ull;
-  }
-  const unsigned long long top = yg >> G;
-  const unsigned frac = (unsigned)(yg & ((1u << G) - 1u)), half = 1u << (G - 1);
-  const int neg = (int)(bits >> 63);
-#pragma unroll
-  for (int s = 0; s + 1 < S; ++s) {
-    const int d = (int)((top >> (7 * (S - 1 - s))) & 127ull);
-    q[s] = (int8_t)(neg ? -d : d);
-  }
-  int last = (int)(top & 127ull);
-  if (frac > half || (frac == half && (sticky || (last & 1)))) ++last;
-  last = last > 127 ? 127 : last;
-  q[S - 1] = (int8_t)(neg ? -last : last);
-}
-
-// The same slices as ozaki_slices, split for packing: the magnitude digits 0..S-2 are bit fields of
+// The S signed 7-bit slices of y = x 2^-e (|y| < 1): the digits of the fixed-point |y| in base 128
+// with the sign of x, the last one rounded half-to-even on the remaining bits and clamped to +-127
+// -- exactly  t = 128 y, q = trunc(t), y = t - q  for the first S - 1 slices and q = rint(t) for
+// the last (unbiased truncation of the dropped remainder), computed on the integer mantissa (no
+// FP64 / conversion-pipe work).  Split for packing: the magnitude digits 0..S-2 are bit fields of
 // `top`, the rounded last digit is `last`, the sign `neg` (applied per byte after packing).
 template <int S>
 __device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& top, uint32_t& last, uint32_t& neg) {
