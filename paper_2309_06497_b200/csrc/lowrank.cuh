@@ -7,11 +7,14 @@
 //     f(A) = f(0) I + Q (f(B) - f(0) I) Q^T,      f(lambda) = (lambda - min(lambda_min, 0) + eps)^(-eta/p),
 //
 // exactly (the null space of A is the orthogonal complement of range(Q) plus the junk directions of
-// Q, on which B vanishes).  Pipeline (FP64; the n^2 r' GEMMs on the tcgen05 Ozaki engine):
-//   Y = Omega^T A (Gaussian Omega, r' = r + 8 columns) -> CGS2 (one CTA per factor, rows of Y^T,
-//   numerically dependent rows replaced by unit vectors) -> T = Q^T A, B = T Q -> f(B) by the
-//   batched Jacobi eigensolver -> X = f(0) I + Q^T^T (f(B) - f(0) I) Q^T, symmetrised.
-// Cost ~6 n^2 r' instead of ~100 n^3 for the Jacobi rounds on the full factor.
+// Q, on which B vanishes).  r is the structural rank bound itself (no oversampling: Y = Omega^T A has
+// rank <= r, so r rows span range(A)).  Pipeline (FP64; the n^2 r GEMMs on the tcgen05 Ozaki engine):
+//   Y = Omega^T A (Gaussian Omega, r rows) -> block CGS2 (64-row blocks: projections on the earlier
+//   blocks as Ozaki GEMMs, the in-block pass on an 8-CTA cluster holding the block in shared memory;
+//   numerically dependent rows replaced by unit vectors and re-projected) -> T = Q A, B = T Q^T ->
+//   f(B) by RootInverseBatch (B is full rank: Newton pre-pass, Jacobi if gated) ->
+//   X = f(0) I + Q^T (f(B) - f(0) I) Q (symmetric-output GEMM).
+// Cost ~6 n^2 r + r^3-class solve instead of the full-size Jacobi rounds.
 #pragma once
 
 #include <vector>
