@@ -48,17 +48,47 @@ __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict
   const int p = find64(begin, nprob, blockIdx.x);
   const GemmProblem& P = probs[p];
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
+  // CTA item = (block of R rows, chunk of KOUT_ITEMS columns): wide problems spread over many CTAs
   const int R = max(1, KOUT_ITEMS / P.N);
-  const int r0 = (int)(blockIdx.x - begin[p]) * R;
+  const int nchunk = (P.N + KOUT_ITEMS - 1) / KOUT_ITEMS;
+  const int64_t item = blockIdx.x - begin[p];
+  const int r0 = (int)(item / nchunk) * R;
+  const int cbeg = (int)(item % nchunk) * KOUT_ITEMS, cend = min(P.N, cbeg + KOUT_ITEMS);
   const int rows = min(R, P.M - r0);
   const T* __restrict__ A = static_cast<const T*>(P.A);
   const T* __restrict__ B = static_cast<const T*>(P.B);
   T* __restrict__ C = static_cast<T*>(P.C);
   const bool readc = (P.flags & kGemmReadC) != 0;
+  if (P.N <= 8 && P.K <= 8) {
+    // tall and narrow (the 3x3 / 7x7 kernel modes: M up to ~10^6, N = K = 3): a thread per row,
+    // its K inputs loaded once, the N x K operand in shared memory; same k order as below
+    __shared__ double bs[64];
+    for (int t = threadIdx.x; t < P.N * P.K; t += blockDim.x) bs[t] = (double)B[ev(P.b_r, t / P.K) + ev(P.b_k, t % P.K)];
+    __syncthreads();
+    for (int i = r0 + threadIdx.x; i < r0 + rows; i += blockDim.x) {
+      const int64_t ai = ev(P.a_r, i), ci = ev(P.c_r, i);
+      double a[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = k < P.K ? (double)A[ai + ev(P.a_k, k)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= P.N) break;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < P.K) acc = fma(a[k], bs[j * P.K + k], acc);
+        const int64_t at = ci + ev(P.c_c, j);
+        double v = P.alpha * acc;
+        if (readc) v = fma(P.beta, (double)C[at], v);
+        C[at] = (T)v;
+      }
+    }
+    return;
+  }
   if (P.N >= 64) {  // wide rows: row loop outside, coalesced column loop inside (no divisions)
     for (int i = r0; i < r0 + rows; ++i) {
       const int64_t ai = ev(P.a_r, i), ci = ev(P.c_r, i);
-      for (int j = threadIdx.x; j < P.N; j += blockDim.x) {
+      for (int j = cbeg + threadIdx.x; j < cend; j += blockDim.x) {
         const int64_t bj = ev(P.b_r, j);
         double acc = 0.0;
         for (int k = 0; k < P.K; ++k) acc = fma((double)A[ai + ev(P.a_k, k)], (double)B[bj + ev(P.b_k, k)], acc);
@@ -214,7 +244,8 @@ int ThinGemmBatch<T>::upload() {
   for (const auto& p : outp) {
     ob.push_back(n_out_items_);
     const int R = std::max(1, KOUT_ITEMS / std::max(p.N, 1));
-    n_out_items_ += (p.M + R - 1) / R;
+    const int nchunk = std::max(1, (p.N + KOUT_ITEMS - 1) / KOUT_ITEMS);
+    n_out_items_ += (int64_t)((p.M + R - 1) / R) * nchunk;
   }
   n_red_ctas_ = 0;
   int64_t wsz = 0;
