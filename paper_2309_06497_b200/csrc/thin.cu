@@ -128,6 +128,22 @@ __global__ void __launch_bounds__(256) k_thin_rank1(const GemmProblem* __restric
   const double xi = (double)x[ev(P.a_r, i)];
   const bool readc = (P.flags & kGemmReadC) != 0;
   const int64_t step = P.a_r.lo;
+  if (sizeof(T) == 8 && step == 1 && (P.N & 1) == 0 && ((reinterpret_cast<uintptr_t>(row) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+    // 16-byte accesses (same per-element arithmetic)
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    double2* __restrict__ r2 = reinterpret_cast<double2*>(row);
+    for (int j = threadIdx.x; j < P.N / 2; j += blockDim.x) {
+      const double2 xv = x2[j];
+      double2 cv = readc ? r2[j] : make_double2(0.0, 0.0);
+      double v0 = P.alpha * (xi * xv.x), v1 = P.alpha * (xi * xv.y);
+      if (readc) {
+        v0 = fma(P.beta, cv.x, v0);
+        v1 = fma(P.beta, cv.y, v1);
+      }
+      r2[j] = make_double2(v0, v1);
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < P.N; j += blockDim.x) {
     double v = P.alpha * (xi * (double)x[j * step]);
     if (readc) v = fma(P.beta, (double)row[j], v);
