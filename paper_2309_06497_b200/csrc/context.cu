@@ -779,14 +779,6 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   int64_t lstats[4] = {0, 0, 0, 0};
   int lrc = SHAMPOO_OK;
   std::string lerr;
-  std::thread lr_thread;
-  if (!lr_jobs.empty()) {
-    SH_CUDA_CHECK(cudaStreamWaitEvent(c->lr_stream, c->ev_fork, 0));
-    lr_thread = std::thread([&] {
-      lrc = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, c->lr_stream, lstats);
-      if (lrc) lerr = shampoo_last_error();
-    });
-  }
   int64_t gstats[kRootGroups][4] = {};
   int grc[kRootGroups] = {};
   std::string gerr[kRootGroups];
@@ -796,13 +788,31 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
                             st, gstats[g], nullptr, nullptr, /*allow_warm=*/true, &full_rank[g], &low_rank[g]);
     if (grc[g]) gerr[g] = shampoo_last_error();
   };
+  std::thread lr_thread;
   std::vector<std::thread> threads;
+  struct JoinAll {  // every early return below still joins the worker threads
+    std::thread& a;
+    std::vector<std::thread>& b;
+    ~JoinAll() {
+      if (a.joinable()) a.join();
+      for (auto& t : b)
+        if (t.joinable()) t.join();
+    }
+  } join_all{lr_thread, threads};
+  if (!lr_jobs.empty()) {
+    SH_CUDA_CHECK(cudaStreamWaitEvent(c->lr_stream, c->ev_fork, 0));
+    lr_thread = std::thread([&] {
+      lrc = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, c->lr_stream, lstats);
+      if (lrc) lerr = shampoo_last_error();
+    });
+  }
   for (int g = 1; g < kRootGroups; ++g) {
     SH_CUDA_CHECK(cudaStreamWaitEvent(c->side[g], c->ev_fork, 0));
     threads.emplace_back(solve, g, c->side[g]);
   }
   solve(0, s);
-  for (auto& th : threads) th.join();
+  for (auto& th : threads)
+    if (th.joinable()) th.join();
   if (lr_thread.joinable()) {
     lr_thread.join();
     SH_CUDA_CHECK(cudaEventRecord(c->ev_lr, c->lr_stream));
