@@ -759,7 +759,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
       const int64_t numel = c->plan.blocks[c->owned[l]].var_count;
       const int64_t rank = (int64_t)c->step[l] * (numel / std::max<int64_t>(d, 1));
       full_rank[g][j] = rank >= d ? 1 : 0;
-      if (k.solver == SHAMPOO_SOLVER_EIGH && k.epsilon > 0.0 && !c->f32 && d > 64 &&
+      if (k.solver == SHAMPOO_SOLVER_EIGH && k.epsilon > 0.0 && !c->f32 && d >= 16 &&
           rank + kLowRankGap <= d && c->low_rank) {
         low_rank[g][j] = 1;
         LowRankJob L{};
