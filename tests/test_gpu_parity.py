@@ -466,3 +466,28 @@ def test_low_rank_path_multiblock_matches_oracle(cuda_device, eps, dup):
     assert wp <= (1e-7 if eps < 1e-9 else 1e-9), wp
     assert worst <= (1e-5 if eps < 1e-9 else 1e-7), worst
     assert opt.guard_stats.fallback_identity == 0 and opt.guard_stats.fallback_previous == 0
+
+
+def test_low_rank_path_small_factors_matches_oracle(cuda_device):
+    """The range-compression path down to d = 16 (csrc/context.cu: d >= 16, rank <= d - 8): a 48-vector
+    block and a (40, 5) block refreshed every step for 30 steps (ranks 1..30 < d - 8 for most of the
+    run, then the full-size solvers), against the float64 oracle at eps = 1e-6."""
+    shapes = [(48,), (40, 5), (24,)]
+    rng = np.random.default_rng(21)
+    params = [rng.standard_normal(s) * 0.3 for s in shapes]
+    kw = dict(max_preconditioner_dim=512, precondition_frequency=1, epsilon=1e-6)
+    opt = P.Shampoo([torch.as_tensor(p, device=cuda_device) for p in params],
+                    P.ShampooConfig(grafting=P.GraftKind.ADAGRAD, **kw))
+    ref = O.OracleShampoo(params, O.OracleConfig(grafting=O.GraftKind.ADAGRAD, **kw))
+    worst = 0.0
+    for _ in range(30):
+        g = [rng.standard_normal(s) * 0.1 for s in shapes]
+        d_ref = ref.step(g)
+        opt.step([torch.as_tensor(x, device=cuda_device) for x in g])
+        torch.cuda.synchronize()
+        for (i, b), want in d_ref.items():
+            worst = max(worst, rel(opt.direction(i, b).cpu().numpy(), want))
+    wp = max(rel(a.cpu().numpy(), b) for a, b in zip(opt.params(), ref.params))
+    assert wp <= 1e-9, wp
+    assert worst <= 1e-7, worst
+    assert opt.guard_stats.fallback_identity == 0 and opt.guard_stats.fallback_previous == 0
