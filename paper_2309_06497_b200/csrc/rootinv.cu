@@ -46,6 +46,8 @@ constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi swe
 // 5 + log(kappa_max) / (p log((p+1)/p)) iterations are left to the Jacobi path.
 constexpr double kHybridNewtonKappa = 5e6;
 constexpr int kPowerIters = 8;  // power-iteration steps for the pre-pass scaling (k_pow_*)
+constexpr double kNewtonScale = 1.5;     // scaled pre-pass steps (SHAMPOO_NEWTON_SCALE=1): M <- 1.5 M
+constexpr double kNewtonScaleRes = 0.9;  // ... while ||M - I||_inf >= 0.9
 constexpr double kNewtonFinalRes = 3e-7;  // residual after which one X <- X T finishes (hybrid pre-pass)
 
 constexpr double U64 = 1.1102230246251565e-16;
@@ -1265,6 +1267,8 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
     N.iters = 0;
     N.converged = 0;
     N.fin = 0;
+    N.scale = 1.0;
+    N.vit = 0.0;
   }
 }
 
@@ -1276,9 +1280,19 @@ __global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ 
   if (!mask[j]) return;
   const NewtonJob& N = nj[j];
   const int64_t tot = (int64_t)N.n * N.n;
-  const double* M = nx + N.off + (2 + cur) * tot;
+  double* M = nx + N.off + (2 + cur) * tot;
   double* T = nx + N.off + 4 * tot;
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  if (N.scale != 1.0) {
+    // scaled step: M <- s M, X <- s^(1/p) X keeps M = X^p (A + eps I); lifts the small eigenvalues
+    // of M (the linear phase) while the spectrum stays inside (0, p + 1) (s max(M) <= s < 2)
+    double* X = nx + N.off + (int64_t)cur * tot;
+    const double s = N.scale, sx = pow(s, 1.0 / N.p);
+    for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+      M[e] *= s;
+      X[e] *= sx;
+    }
+  }
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     const bool d = (e / N.n == e % N.n);
     T[e] = ((d ? (double)(N.p + 1) : 0.0) - M[e]) / N.p;
@@ -1314,7 +1328,7 @@ __global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restri
 
 // Residual part 2 (thread per job): best-iterate tracking and the stopping rule r < max(tol, tol_n n).
 __global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int32_t* mask2, int njobs, unsigned long long* resbits,
-                               double tol, double tol_n, int32_t* improved, int32_t* count) {
+                               double tol, double tol_n, int32_t* improved, int32_t* count, int scale_on) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= njobs) return;
   improved[j] = 0;
@@ -1339,16 +1353,22 @@ __global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int32_t* mask2, int
     N.best = r;
     improved[j] = 1;
   }
+  // conditioning gate counter: a scaled iteration lifted the small eigenvalues by s more
+  const double lg = N.p * log((N.p + 1.0) / N.p);
+  N.vit += 1.0 + (N.scale != 1.0 ? log(N.scale) / lg : 0.0);
+  N.scale = 1.0;
   if (r < fmax(tol, tol_n * N.n)) {
     N.converged = 1;
     mask[j] = 0;
-  } else if (N.iters >= 1000 || (tol_n > 0.0 && N.iters >= N.cap)) {
+  } else if (N.iters >= 1000 || (tol_n > 0.0 && N.vit >= N.cap)) {
     mask[j] = 0;
   } else if (tol_n > 0.0 && r < kNewtonFinalRes) {
     // quadratic convergence: ||M_{k+1} - I|| ~ (p+1)/(2p) ||M_k - I||^2 < 1e-13 -- only X_{k+1}
     // is still needed (the hybrid pre-pass; the reference-semantics NEWTON solver keeps its count)
     N.fin = 1;
     mask2[j] = 0;
+  } else if (tol_n > 0.0 && scale_on && N.iters >= 1 && r >= kNewtonScaleRes) {
+    N.scale = kNewtonScale;  // far from I: eigenvalues near 0 (all are <= 1 after one step)
   }
   if (!mask[j]) mask2[j] = 0;
   if (mask[j]) atomicAdd(count, 1);
@@ -1926,8 +1946,13 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     k_newton_rowmax<<<total_elem_chunks_, 256, 0, s>>>(dn, mask2, d_elem_begin_, nj, total_elem_chunks_, nx_, cur ^ 1,
                                                        d_resbits_);
     SH_LAUNCH_CHECK();
+    static const int scale_on = [] {
+      const char* e = std::getenv("SHAMPOO_NEWTON_SCALE");
+      return e ? std::atoi(e) : 0;
+    }();
     k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, mask2, nj, d_resbits_, tol,
-                                                    hybrid ? kHybridNewtonTolN : 0.0, d_improved_, d_count_);
+                                                    hybrid ? kHybridNewtonTolN : 0.0, d_improved_, d_count_,
+                                                    hybrid ? scale_on : 0);
     SH_LAUNCH_CHECK();
     if (!hybrid) {
       k_newton_copybest<<<total_elem_chunks_, 256, 0, s>>>(dn, d_improved_, d_elem_begin_, nj, nx_, cur ^ 1);
