@@ -46,7 +46,7 @@ constexpr int kHybridNewtonBudget = 24;  // one iteration costs ~0.35 Jacobi swe
 // 5 + log(kappa_max) / (p log((p+1)/p)) iterations are left to the Jacobi path.
 constexpr double kHybridNewtonKappa = 5e6;
 constexpr int kPowerIters = 8;  // power-iteration steps for the pre-pass scaling (k_pow_*)
-constexpr double kNewtonScale = 1.5;     // scaled pre-pass steps (SHAMPOO_NEWTON_SCALE=1): M <- 1.5 M
+constexpr double kNewtonScale = 1.5;     // scaled pre-pass steps (SHAMPOO_NEWTON_SCALE=0 disables): M <- 1.5 M
 constexpr double kNewtonScaleRes = 0.9;  // ... while ||M - I||_inf >= 0.9
 constexpr double kNewtonFinalRes = 3e-7;  // residual after which one X <- X T finishes (hybrid pre-pass)
 
@@ -1367,7 +1367,9 @@ __global__ void k_newton_check(NewtonJob* nj, int32_t* mask, int32_t* mask2, int
     // is still needed (the hybrid pre-pass; the reference-semantics NEWTON solver keeps its count)
     N.fin = 1;
     mask2[j] = 0;
-  } else if (tol_n > 0.0 && scale_on && N.iters >= 1 && r >= kNewtonScaleRes) {
+  } else if (tol_n > 0.0 && scale_on && N.p <= 2 && N.iters >= 1 && r >= kNewtonScaleRes) {
+    // (p <= 2 only: measured 15 -> 12 iterations on the ill-conditioned vector factors; for p >= 4
+    // the lifted top of the spectrum costs as many iterations as the scaling saves)
     N.scale = kNewtonScale;  // far from I: eigenvalues near 0 (all are <= 1 after one step)
   }
   if (!mask[j]) mask2[j] = 0;
@@ -1948,7 +1950,7 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
     SH_LAUNCH_CHECK();
     static const int scale_on = [] {
       const char* e = std::getenv("SHAMPOO_NEWTON_SCALE");
-      return e ? std::atoi(e) : 0;
+      return e ? std::atoi(e) : 1;
     }();
     k_newton_check<<<(nj + 127) / 128, 128, 0, s>>>(dn, mask, mask2, nj, d_resbits_, tol,
                                                     hybrid ? kHybridNewtonTolN : 0.0, d_improved_, d_count_,
