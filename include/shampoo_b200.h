@@ -213,6 +213,9 @@ SHAMPOO_API int shampoo_work_tc(shampoo_ctx* ctx, double* stats_int8_ops, double
                                 double* stats_tc_flops, double* precond_tc_flops);
 /* number of kernel launches issued by this library since load (bench evidence) */
 SHAMPOO_API int64_t shampoo_launch_count(void);
+/* int8 tensor-core ops executed by the tcgen05 GEMM engine since load (or the last reset), counted
+ * on the device per output tile (masked-out problems are not counted).  Synchronises the device. */
+SHAMPOO_API int shampoo_tc_counter(int32_t reset, double* int8_ops);
 
 /* ---- state export/import: device views into the context's arena.
  * name: "factor","inv_factor","graft_accumulator","filtered_grad","momentum",

@@ -93,6 +93,7 @@ SIGNATURES = {
     "shampoo_guard_stats_get": (C.c_int, [_P, C.POINTER(GuardStatsC)]),
     "shampoo_guard_stats_set": (C.c_int, [_P, C.POINTER(GuardStatsC)]),
     "shampoo_launch_count": (_I64, []),
+    "shampoo_tc_counter": (C.c_int, [_I32, C.POINTER(C.c_double)]),
     "shampoo_timing_enable": (C.c_int, [_P, _I32]),
     "shampoo_timing_get": (C.c_int, [_P, C.POINTER(C.c_double), _PI64]),
     "shampoo_work": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),

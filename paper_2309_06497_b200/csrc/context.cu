@@ -282,6 +282,20 @@ int build_engine(shampoo_ctx* c) {
   T* INV = static_cast<T*>(c->INV);
   T* PS = static_cast<T*>(c->PS);
   T* tmp[2] = {static_cast<T*>(c->T1), static_cast<T*>(c->T2)};
+  {
+    // Slices of the mode-product operands (SHAMPOO_PREC_SLICES overrides).  The directions need 1e-3
+    // (north_star), not FP64: measured against S = 8 and the oracle (scripts/slices_probe.py,
+    // tests/test_gpu_parity.py::test_resnet_shapes_vs_oracle), S = 5 is indistinguishable from S = 8 on
+    // the rank-deficient early steps at eps = 1e-12 (2e-5 vs the oracle, the solver's own floor) and
+    // 1.3e-8 from S = 8 at the steady state; S = 4 reaches 9e-4 early on (no margin).  The factor
+    // statistics feed the root inverse and keep the FP64-class default.
+    const char* ev = std::getenv("SHAMPOO_PREC_SLICES");
+    const int ps = ev ? std::atoi(ev) : 5;
+    for (auto& b : e->prec) {
+      const int rc = b.set_slices(ps);
+      if (rc) return rc;
+    }
+  }
   for (size_t l = 0; l < c->owned.size(); ++l) {
     const BlockPlan& b = c->plan.blocks[c->owned[l]];
     if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;

@@ -33,6 +33,7 @@ constexpr int HB = 32;            // row-block size
 constexpr int LDS_ = NS + 1;      // padded smem leading dim
 constexpr int SLOT = 2 * NS * NS + NS + 2;  // U (64x64) + S (64x64) + D (64) + flag
 constexpr int ECH = 4096;         // elements per chunk for elementwise job kernels
+constexpr int kNTSlot = 4;        // Newton scratch slot of T (also holds (A + eps I)^2 before the iterations)
 constexpr int MAX_SWEEPS = 40;
 // eigh Newton pre-pass: well-conditioned factors reach ||M - I||_inf ~ 1e-15 in 8-12 iterations
 // (error vs eigh ~ 3e-15); the budget bounds the time spent on factors that need the Jacobi path
@@ -1147,8 +1148,8 @@ __global__ void k_count(const RootJob* __restrict__ jobs, RootState* st, int njo
 // c^p = 2 ||A + eps I||_F / (p + 1) (matfun.py:190-198) guarantees that but overestimates
 // lambda_max by up to sqrt(n), which costs log(ratio) / (p log((p+1)/p)) extra iterations.  The
 // Rayleigh quotient after kPowerIters steps from a random start is within a few % below
-// lambda_max (its top-eigenvector weight grows like (lambda_1 / lambda_i)^(2k)); a divergent run
-// (scaled spectrum beyond p + 1) is caught by the residual check and handed to the Jacobi path.
+// lambda_max (its top-eigenvector weight grows like (lambda_1 / lambda_i)^(2k)) -- but it is a lower
+// bound only, so the scaling is clamped from below by a guaranteed bound (k_newton_ub).
 __global__ void __launch_bounds__(256) k_pow_start(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
                                                    const NewtonJob* __restrict__ nj, const int32_t* __restrict__ ebegin,
                                                    int njobs, double* __restrict__ nx, const int32_t* __restrict__ cand) {
@@ -1211,6 +1212,56 @@ __global__ void __launch_bounds__(256) k_pow_norm(const RootJob* __restrict__ jo
   for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = y[i] * inv;
 }
 
+// Guaranteed lambda_max bound for the pre-pass scaling (the power-iteration Rayleigh quotient is a
+// LOWER bound: a start vector nearly orthogonal to the top eigenvectors would leave M0 with an
+// eigenvalue beyond p + 1, and for even p the iteration then still converges in M while X takes the
+// wrong sign on that eigenvector -- undetectable from the residual).  lambda_max^4 <= tr((A+eps I)^4)
+// = ||(A + eps I)^2||_F^2, and lambda_max <= ||A + eps I||_F.  Part 1: candidates whose Frobenius bound
+// does not already cover the power estimate get M0 <- A + eps I (the squaring GEMM reads it).
+__global__ void __launch_bounds__(256) k_newton_ub_prep(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                        const NewtonJob* __restrict__ nj, int32_t* mask,
+                                                        const int32_t* __restrict__ ebegin, int njobs,
+                                                        const double* __restrict__ ws, double* __restrict__ nx,
+                                                        double eps, const int32_t* __restrict__ cand) {
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  const RootJob& J = jobs[j];
+  const NewtonJob& N = nj[j];
+  const int n = J.n, p = J.root_p;
+  const double fro2 = st[j].norm2 + (eps > 0.0 ? 2.0 * eps * st[j].trace + n * eps * eps : 0.0);
+  const bool need = st[j].status == kEigOk && (!cand || cand[j]) && sqrt(st[j].norm2) > 0.0 &&
+                    N.lam > 0.0 && isfinite(N.lam) && sqrt(fro2) / (p + 1) > 1.05 * N.lam + eps;
+  if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) mask[j] = need ? 1 : 0;
+  if (!need) return;
+  const int64_t tot = (int64_t)n * n;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  double* M0 = nx + N.off + 2 * tot;
+  const double* A = ws + J.ws_off;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
+    const int64_t i = e / n, k = e % n;
+    M0[e] = A[i * J.np + k] + ((i == k && eps > 0.0) ? eps : 0.0);
+  }
+}
+
+// Part 2 (block per job, fixed reduction order): ub = min(||A + eps I||_F, ||(A + eps I)^2||_F^(1/2)).
+__global__ void __launch_bounds__(256) k_newton_ub(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
+                                                   NewtonJob* nj, const int32_t* __restrict__ mask,
+                                                   const double* __restrict__ nx, double eps) {
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  const int n = jobs[j].n;
+  const double fro = sqrt(st[j].norm2 + (eps > 0.0 ? 2.0 * eps * st[j].trace + n * eps * eps : 0.0));
+  if (!mask[j]) {
+    if (threadIdx.x == 0) nj[j].ub = fro;
+    return;
+  }
+  const int64_t tot = (int64_t)n * n;
+  const double* Q = nx + nj[j].off + kNTSlot * tot;
+  double q = 0.0;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) q = fma(Q[e], Q[e], q);
+  q = block_sum<double, 256>(q, red);
+  if (threadIdx.x == 0) nj[j].ub = fmin(fro, sqrt(sqrt(q)));
+}
+
 __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__ jobs, RootState* st,
                                                      NewtonJob* nj, int32_t* mask,
                                                      const int32_t* __restrict__ ebegin, int njobs,
@@ -1249,9 +1300,11 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
   const double tr = st[j].trace;
   const double fro2 = st[j].norm2 + (eps > 0.0 ? 2.0 * eps * tr + n * eps * eps : 0.0);
   const int p = J.root_p;
-  // reference scaling, or (hybrid) 1.05 x the power-iteration lambda_max(A + eps I) when usable
+  // reference scaling, or (hybrid) 1.05 x the power-iteration lambda_max(A + eps I) when usable, never
+  // below ub / (p + 1) (ub >= lambda_max guaranteed, k_newton_ub): the scaled spectrum stays in (0, p + 1)
   double cpow = 2.0 * sqrt(fro2) / (p + 1);
-  if (lam_scale && N.lam > 0.0 && isfinite(N.lam)) cpow = fmin(cpow * (p + 1) / 2.0, 1.05 * N.lam + eps);
+  if (lam_scale && N.lam > 0.0 && isfinite(N.lam))
+    cpow = fmin(sqrt(fro2), fmax(1.05 * N.lam + eps, N.ub * (1.0 + 1e-6) / (p + 1)));
   const double c = pow(cpow, 1.0 / p);
   const double cp = pow(c, (double)p);
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
@@ -1620,7 +1673,7 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   pack_cap_ = 0;
   for (const RootJob& J : host_) {
     const int64_t ks = (J.n + 31) / 32, rc = (J.n + 7) / 8;
-    pack_cap_ += 2 * ks * rc * OzakiGemmBatch<double>::S * 256;
+    pack_cap_ += 2 * ks * rc * OzakiGemmBatch<double>::kDefaultSlices * 256;
   }
   SH_CUDA_CHECK(dev_malloc(&pack_arena_, std::max<int64_t>(pack_cap_, 256)));
   for (auto* b : {&recon_, &rr_, &warm1_, &warm2_, &newton_x_[0], &newton_x_[1], &newton_m_[0], &newton_m_[1], &g_wv_,
@@ -1890,6 +1943,7 @@ int RootInverseBatch::build_newton() {
     }
     for (size_t q = 0; q < plan.size(); ++q)
       newton_pow_[q]->add(sym_gemm(buf(plan[q].lhs), buf(plan[q].rhs), buf(plan[q].dst)));
+    newton_sq_.add(sym_gemm(buf(2), buf(2), buf(kNT)));  // (A + eps I)^2 (SYRK: one shared pack)
   }
   int rc;
   for (int c = 0; c < 2; ++c) {
@@ -1898,6 +1952,8 @@ int RootInverseBatch::build_newton() {
   }
   for (auto& p : newton_pow_)
     if ((rc = p->upload())) return rc;
+  newton_sq_.set_external_arena(pack_arena_, pack_cap_);
+  if ((rc = newton_sq_.upload())) return rc;
   newton_built_ = true;
   return SHAMPOO_OK;
 }
@@ -1924,6 +1980,12 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
       k_pow_norm<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, nx_, cand);
       SH_LAUNCH_CHECK();
     }
+    k_newton_ub_prep<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_,
+                                                        eps, cand);
+    SH_LAUNCH_CHECK();
+    if ((rc = newton_sq_.launch(s, mask))) return rc;
+    k_newton_ub<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, nx_, eps);
+    SH_LAUNCH_CHECK();
     prof_mark("nw_power");
   }
   k_newton_init<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, ws_, nx_, eps, cand,

@@ -68,6 +68,7 @@ struct NewtonJob {
   double lam;   // hybrid pre-pass: power-iteration estimate of lambda_max(A) (scales X0, M0)
   double scale; // hybrid pre-pass: spectrum scaling applied at the start of the next iteration
   double vit;   // hybrid pre-pass: iterations counted for the conditioning gate (scaled ones count more)
+  double ub;    // hybrid pre-pass: guaranteed upper bound on lambda_max(A + eps I) (k_newton_ub)
 };
 
 class RootInverseBatch {
@@ -150,6 +151,7 @@ class RootInverseBatch {
   int64_t pack_cap_ = 0;
   bool newton_built_ = false;
   OzakiGemmBatch<double> newton_x_[2], newton_m_[2];
+  OzakiGemmBatch<double> newton_sq_;  // (A + eps I)^2 for the guaranteed lambda_max bound (hybrid pre-pass)
   std::vector<std::unique_ptr<OzakiGemmBatch<double>>> newton_pow_;
   int32_t* d_cand_ = nullptr;  // eigh jobs tried with the Newton pre-pass
   bool hybrid_ = true;          // SHAMPOO_EIG_NEWTON=0 disables the pre-pass

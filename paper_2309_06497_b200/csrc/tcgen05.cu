@@ -23,6 +23,11 @@ constexpr int EXP_CHUNK = 64;                 // k per rowexp thread (strided ro
 constexpr int EXP_WARP_CHUNK = 2048;          // k per rowexp warp (contiguous rows)
 constexpr int kExpFloor = -1100;              // exponent of an all-zero row (ldexp -> 0)
 
+// Executed MMA work (bench evidence for the tensor-pipe roofline of phases whose problem sets are
+// masked on the device, e.g. the root-inverse Newton iterations): one unit = one 32-wide k stage of
+// one slice pair on a 128 x 32 tile, i.e. 2 * 128 * 32 * 32 int8 ops.  One atomic per tile.
+__device__ unsigned long long g_oz_mma_units = 0;
+
 template <int S>
 struct OzCfg {
   static constexpr int A_BYTES = (TM / 8) * S * 256;     // one stage of a 128-row tile, all slices
@@ -468,6 +473,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* 
         tc_commit(&empty_bar[st]);  // frees the stage once these MMAs have read it
       }
       tc_commit(&done_bar);
+      atomicAdd(&g_oz_mma_units, (unsigned long long)nk * (S * (S + 1) / 2));
     }
   } else {
     // epilogue (128 threads): TMEM -> FP64 diagonal combination -> smem tile -> coalesced stores
@@ -721,6 +727,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
           tc_commit(&empty_bar[st]);
         }
         tc_commit(&tfull[b]);  // accumulators of this tile complete
+        atomicAdd(&g_oz_mma_units, (unsigned long long)it.nk * (S * (S + 1) / 2));
         ++tcount;
       }
     }
@@ -867,6 +874,38 @@ bool same_operand(const GemmProblem& p) {
 }
 }  // namespace
 
+// Runs BODY with `constexpr int S` = the batch's slice count (the instantiated set).
+#define OZ_DISPATCH(SV, ...)                                 \
+  switch (SV) {                                              \
+    case 3: { constexpr int S = 3; __VA_ARGS__; } break;     \
+    case 4: { constexpr int S = 4; __VA_ARGS__; } break;     \
+    case 5: { constexpr int S = 5; __VA_ARGS__; } break;     \
+    case 6: { constexpr int S = 6; __VA_ARGS__; } break;     \
+    default: { constexpr int S = 8; __VA_ARGS__; } break;    \
+  }
+
+template <typename T>
+int OzakiGemmBatch<T>::set_slices(int s) {
+  if (s != 3 && s != 4 && s != 5 && s != 6 && s != 8) {
+    set_error("Ozaki slice count must be one of 3, 4, 5, 6, 8");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  S_ = s;
+  return SHAMPOO_OK;
+}
+
+template <typename T, int S>
+static cudaError_t oz_set_smem_attrs() {
+  static const cudaError_t e = [] {
+    cudaError_t a = cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OzCfg<S>::SMEM);
+    cudaError_t b = cudaFuncSetAttribute(k_oz_gemm_p<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)OzPCfg<S>::SMEM);
+    return a != cudaSuccess ? a : b;
+  }();  // once per instantiation, thread-safe
+  return e;
+}
+
 template <typename T>
 OzakiGemmBatch<T>::~OzakiGemmBatch() {
   dev_free(d_prob_);
@@ -888,12 +927,12 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
 template <typename T>
 int OzakiGemmBatch<T>::upload() {
   if (host.empty()) return SHAMPOO_OK;
-  static const cudaError_t attr = cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)OzCfg<S>::SMEM);  // once, thread-safe
-  SH_CUDA_CHECK(attr);
-  static const cudaError_t attr_p = cudaFuncSetAttribute(
-      k_oz_gemm_p<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OzPCfg<S>::SMEM);
-  SH_CUDA_CHECK(attr_p);
+  const int S = S_;
+  {
+    cudaError_t attr = cudaSuccess;
+    OZ_DISPATCH(S, attr = oz_set_smem_attrs<T, S>());
+    SH_CUDA_CHECK(attr);
+  }
   std::vector<OzProb> tp(host.size());
   std::vector<int> a_set(host.size(), 0), b_set(host.size(), 0);
   std::vector<int64_t> begin(host.size()), rbegin, pbegin[2], ebegin[2];
@@ -1025,7 +1064,7 @@ int OzakiGemmBatch<T>::upload() {
     }();
     std::vector<CUtensorMap> maps(3 * host.size());
     bool ok = encode != nullptr && std::getenv("SHAMPOO_OZ_NO_TMA") == nullptr;
-    constexpr int SH = (S + 1) / 2;
+    const int SH = (S + 1) / 2;
     auto make = [&](CUtensorMap* m, int64_t off, int rc, int ks, int cores, int slices) {
       const cuuint64_t dims[3] = {256, (cuuint64_t)rc, (cuuint64_t)S * ks};
       const cuuint64_t strides[2] = {256, (cuuint64_t)rc * 256};
@@ -1063,7 +1102,8 @@ int OzakiGemmBatch<T>::launch_pack(const PackSet& ps, cudaStream_t s, const int3
   SH_CUDA_CHECK(cudaMemsetAsync(exps_ + ps.exp_begin, 0x80, ps.exp_elems * sizeof(int32_t), s));  // very negative
   k_oz_rowexp<T><<<(unsigned)ps.exp_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_ebegin, ps.njobs, mask, exps_);
   SH_LAUNCH_CHECK();
-  k_oz_pack<T, S><<<(unsigned)ps.pack_ctas, PACK_UNITS, 0, s>>>(ps.d_jobs, ps.d_pbegin, ps.njobs, mask, exps_, arena_);
+  OZ_DISPATCH(S_, k_oz_pack<T, S><<<(unsigned)ps.pack_ctas, PACK_UNITS, 0, s>>>(ps.d_jobs, ps.d_pbegin, ps.njobs,
+                                                                                mask, exps_, arena_));
   SH_LAUNCH_CHECK();
   return SHAMPOO_OK;
 }
@@ -1083,13 +1123,13 @@ int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   }();
   if (persist) {
     const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
-    k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(d_prob_, d_tp_, d_begin_, (int)host.size(),
-                                                                 total_items_, mask, arena_, exps_, ws_,
-                                                                 static_cast<const CUtensorMap*>(d_tmaps_));
+    OZ_DISPATCH(S_, k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(
+                        d_prob_, d_tp_, d_begin_, (int)host.size(), total_items_, mask, arena_, exps_, ws_,
+                        static_cast<const CUtensorMap*>(d_tmaps_)));
   } else {
-    k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(
-        d_prob_, d_tp_, d_begin_, (int)host.size(), mask, arena_, exps_, ws_,
-        static_cast<const CUtensorMap*>(d_tmaps_));
+    OZ_DISPATCH(S_, k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(
+                        d_prob_, d_tp_, d_begin_, (int)host.size(), mask, arena_, exps_, ws_,
+                        static_cast<const CUtensorMap*>(d_tmaps_)));
   }
   SH_LAUNCH_CHECK();
   if (total_red_ > 0) {
@@ -1117,6 +1157,18 @@ template class OzakiGemmBatch<double>;
 }  // namespace shampoo
 
 // ---------------------------------------------------------------- C ABI utility
+
+extern "C" int shampoo_tc_counter(int32_t reset, double* int8_ops) {
+  using namespace shampoo;
+  unsigned long long units = 0;
+  SH_CUDA_CHECK(cudaMemcpyFromSymbol(&units, g_oz_mma_units, sizeof(units)));
+  if (int8_ops) *int8_ops = (double)units * 2.0 * TM * TN * TKB;
+  if (reset) {
+    const unsigned long long zero = 0;
+    SH_CUDA_CHECK(cudaMemcpyToSymbol(g_oz_mma_units, &zero, sizeof(zero)));
+  }
+  return SHAMPOO_OK;
+}
 
 extern "C" int shampoo_tc_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                                int32_t symmetric, double alpha, double beta, int32_t dtype, void* stream) {

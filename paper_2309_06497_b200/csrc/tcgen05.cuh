@@ -69,8 +69,13 @@ struct OzPackJob {
 template <typename T>
 class OzakiGemmBatch {
  public:
-  static constexpr int S = sizeof(T) == 8 ? 8 : 5;  // slices per operand
+  // slices per operand: 8 for double (FP64 class), 5 for single; set_slices() before upload() trades
+  // accuracy (operand truncation 2^-7S of the row maximum) for S(S+1)/2 int8 products per MAC
+  static constexpr int kDefaultSlices = sizeof(T) == 8 ? 8 : 5;
+  static constexpr int kMaxSlices = 8;
   std::vector<GemmProblem> host;
+  int set_slices(int s);     // 3..8 (supported: 3, 4, 5, 6, 8); SHAMPOO_ERR_INVALID_ARGUMENT otherwise
+  int slices() const { return S_; }
   OzakiGemmBatch() = default;
   OzakiGemmBatch(const OzakiGemmBatch&) = delete;
   OzakiGemmBatch& operator=(const OzakiGemmBatch&) = delete;
@@ -117,6 +122,7 @@ class OzakiGemmBatch {
   int64_t total_items_ = 0, total_red_ = 0;
   int nred_ = 0;
   double mma_count_ = 0;
+  int S_ = kDefaultSlices;
 };
 
 }  // namespace shampoo

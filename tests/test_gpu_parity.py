@@ -119,6 +119,41 @@ def test_root_inverse_batch_mixed_sizes(cuda_device):
         assert rel(x.cpu().numpy(), ref) <= 1e-8
 
 
+def _power_start_vector(n: int, job: int = 0) -> np.ndarray:
+    """The deterministic start vector of the Newton pre-pass power iteration (rootinv.cu k_pow_start)."""
+    m = (1 << 64) - 1
+    x = np.empty(n)
+    for e in range(n):
+        h = (((e + 1) * 0x9E3779B97F4A7C15) & m) ^ (((job + 1) * 0xBF58476D1CE4E5B9) & m)
+        h = ((h ^ (h >> 31)) * 0x94D049BB133111EB) & m
+        h ^= h >> 29
+        x[e] = (h >> 11) * 2.0 ** -52 - 1.0
+    return x
+
+
+@pytest.mark.parametrize("ratio", [3.7, 4.5])
+def test_newton_prepass_scaling_survives_blind_power_start(cuda_device, ratio):
+    """the pre-pass scales by a power-iteration estimate of lambda_max, a LOWER bound.  With
+    the top eigenvector orthogonal to the power start the estimate misses lambda_1; for p = 2 and
+    lambda_1 / (1.05 lambda_2) in (3, ~4.6) the coupled iteration still converges in M while X takes
+    the wrong sign on v_1.  The guaranteed bound (k_newton_ub) must keep the result right."""
+    n = 96
+    rng = np.random.default_rng(11)
+    x0 = _power_start_vector(n)
+    v1 = rng.standard_normal(n)
+    v1 -= x0 * (v1 @ x0) / (x0 @ x0)
+    v1 /= np.linalg.norm(v1)
+    basis, _ = np.linalg.qr(np.column_stack([v1, rng.standard_normal((n, n - 1))]))  # basis[:, 0] = +-v1
+    assert abs(basis[:, 0] @ x0) < 1e-12 * np.linalg.norm(x0)
+    lam = np.concatenate([[ratio * 1.05], np.linspace(1.0, 0.02, n - 1)])
+    a = (basis * lam) @ basis.T
+    a = (a + a.T) / 2
+    ref = O.root_inverse_eigh(a, 2, eps=1e-12)
+    (x,), status, its = P.batched_root_inverse([torch.as_tensor(a, device=cuda_device)], 2, epsilon=1e-12)
+    assert status == [0]
+    assert rel(x.cpu().numpy(), ref) <= 1e-8, (rel(x.cpu().numpy(), ref), its)
+
+
 def test_root_inverse_guard_conventions(cuda_device):
     # matfun.py:240-293: NaN input -> fallback (identity here: no previous);
     # zero matrix with eps=1e-4 -> 100 I at p=2; eps=0 singular -> identity fallback
