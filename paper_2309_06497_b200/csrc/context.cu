@@ -285,12 +285,13 @@ int build_engine(shampoo_ctx* c) {
   {
     // Slices of the mode-product operands (SHAMPOO_PREC_SLICES overrides).  The directions need 1e-3
     // (north_star), not FP64: measured against S = 8 and the oracle (scripts/slices_probe.py,
-    // tests/test_gpu_parity.py::test_resnet_shapes_vs_oracle), S = 5 is indistinguishable from S = 8 on
-    // the rank-deficient early steps at eps = 1e-12 (2e-5 vs the oracle, the solver's own floor) and
-    // 1.3e-8 from S = 8 at the steady state; S = 4 reaches 9e-4 early on (no margin).  The factor
+    // tests/test_gpu_parity.py): at the steady state S = 4/5/6 are 1.2e-6/1.3e-8/1.1e-10 from S = 8; on
+    // the rank-deficient early steps at eps = 1e-12 (inverse factors ~eps^(-1/4) on the null space,
+    // heavy cancellation) S = 4 reaches 9e-4 and S = 5 moves the parameters by 4e-6 (S = 8: < 1e-7),
+    // so double keeps 2^-42 operand truncation (S = 6; 21 instead of 36 products).  The factor
     // statistics feed the root inverse and keep the FP64-class default.
     const char* ev = std::getenv("SHAMPOO_PREC_SLICES");
-    const int ps = ev ? std::atoi(ev) : 5;
+    const int ps = ev ? std::atoi(ev) : (sizeof(T) == 8 ? 6 : OzakiGemmBatch<T>::kDefaultSlices);
     for (auto& b : e->prec) {
       const int rc = b.set_slices(ps);
       if (rc) return rc;

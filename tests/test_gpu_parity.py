@@ -462,8 +462,9 @@ def test_low_rank_path_matches_oracle(cuda_device, eps):
     wp = max(rel(a.cpu().numpy(), b) for a, b in zip(opt.params(), ref.params))
     print(f"low-rank eps={eps:g}: worst direction rel {worst:.2e}, params rel {wp:.2e}")
     # eps = 1e-12 sits below the null-space eigenvalue noise of float64 (see the root-inverse test
-    # above): the reference's own answer carries ~1e-9 noise there
-    assert wp <= (1e-7 if eps < 1e-9 else 1e-9), wp
+    # above): the reference's own answer carries ~1e-9 noise there; the mode products truncate their
+    # operands at 2^-42 of the row maximum (6 slices, context.cu)
+    assert wp <= (1e-7 if eps < 1e-9 else 1e-8), wp
     assert worst <= (1e-5 if eps < 1e-9 else 1e-7), worst
     assert opt.guard_stats.fallback_identity == 0 and opt.guard_stats.fallback_previous == 0
 
