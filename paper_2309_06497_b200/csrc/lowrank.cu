@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_lr_gauss(const LRDev* __restrict__ jobs
   const int64_t tot = (int64_t)J.r * J.d;
   const int64_t base = (int64_t)(blockIdx.x - cbegin[j]) * LR_ECH;
   for (int64_t e = base + threadIdx.x; e < base + LR_ECH && e < tot; e += blockDim.x) {
-    const uint64_t key = ((uint64_t)j << 40) ^ (uint64_t)e;
+    const uint64_t key = ((uint64_t)J.d << 40) ^ (uint64_t)e;  // by size, not batch position (world-size invariance)
     const double u1 = ((splitmix64(2 * key) >> 11) + 1) * 0x1.0p-53;  // (0, 1]
     const double u2 = (splitmix64(2 * key + 1) >> 11) * 0x1.0p-53;
     ws[J.t_off + e] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);

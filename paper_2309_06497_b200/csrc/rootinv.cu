@@ -1159,7 +1159,9 @@ __global__ void __launch_bounds__(256) k_pow_start(const RootJob* __restrict__ j
   double* x = nx + nj[j].off + 5 * (int64_t)n * n;
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < n; e += blockDim.x) {
-    uint64_t h = (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(j + 1) * 0xBF58476D1CE4E5B9ull;
+    // seeded by the size only: a factor's result must not depend on its position in the batch (the
+    // batch composition changes with the world size; world-size invariance, dist.py:173-185)
+    uint64_t h = (uint64_t)(e + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)n * 0xBF58476D1CE4E5B9ull;
     h = (h ^ (h >> 31)) * 0x94D049BB133111EBull;
     h ^= h >> 29;
     x[e] = (double)(h >> 11) * 0x1.0p-52 - 1.0;  // uniform in [-1, 1)

@@ -14,7 +14,8 @@ rank keeps state only for the blocks its group rank owns, writes their
 directions into its region of the padded gather buffer, and an in-place NCCL
 all-gather inside each group of ``num_trainers_per_group`` ranks replicates
 all directions before every rank applies every block.  Groups are exact
-replicas (the assignment is replicated across groups).
+replicas (the assignment is replicated across groups); the optional replica
+check (dist.py:361-368) raises ``DivergedReplicasError`` when they are not.
 """
 
 from __future__ import annotations
@@ -24,23 +25,32 @@ from typing import Optional
 import torch
 import torch.distributed as dist
 
-from .config import GraftKind, LargeDimMethod, ShampooConfig, Solver
+from .config import DivergedReplicasError, GraftKind, LargeDimMethod, ShampooConfig, Solver, lr_at
 from .optimizer import GuardStats, Shampoo
 
-__all__ = ["DistributedShampoo", "GroupExchange"]
+__all__ = ["DistributedShampoo", "GroupExchange", "REPLICA_TOLERANCE"]
+
+REPLICA_TOLERANCE = 1e-12  # dist.py:53
 
 
 class GroupExchange:
     """Replica groups of ``group_size`` consecutive ranks and the region all-gather.
 
     Mirrors dist.py:350-359: every group gathers independently; group g holds
-    ranks [g*J_G, (g+1)*J_G).  ``__call__(buf, group_rank, max_payload)`` fills
-    ``buf`` (group_size * max_payload scalars) from every rank's region.
+    group-local ranks [g*J_G, (g+1)*J_G) of ``process_group`` (default: WORLD).
+    ``__call__(buf, group_rank, max_payload)`` fills ``buf`` (group_size *
+    max_payload scalars) from every rank's region.  Backends without CUDA
+    collectives (gloo with device tensors, used by the one-GPU multi-process
+    tests) are served through a host staging copy.
     """
 
     def __init__(self, group_size: int, process_group=None):
+        self.pg = process_group
         self.world = dist.get_world_size(process_group)
         self.rank = dist.get_rank(process_group)
+        # new_group() takes GLOBAL ranks: map the group-local indices through the process group
+        gl = (dist.get_process_group_ranks(process_group) if process_group is not None
+              else list(range(self.world)))
         if group_size <= 0:
             group_size = self.world
         if self.world % group_size:
@@ -53,7 +63,7 @@ class GroupExchange:
         else:
             for g in range(self.world // group_size):  # every rank creates every group
                 ranks = list(range(g * group_size, (g + 1) * group_size))
-                pg = dist.new_group(ranks)
+                pg = dist.new_group([gl[r] for r in ranks])
                 if self.rank in ranks:
                     self.group = pg
         self.bytes_per_step = 0
@@ -62,9 +72,22 @@ class GroupExchange:
         if self.world // group_size > 1:
             for k in range(group_size):
                 ranks = list(range(k, self.world, group_size))
-                pg = dist.new_group(ranks)
+                pg = dist.new_group([gl[r] for r in ranks])
                 if self.rank in ranks:
                     self.cross = pg
+        self.backend = dist.get_backend(process_group)
+        self.staged = self.backend == "gloo"
+
+    # -- helpers
+
+    def _stage(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if (self.staged and t.is_cuda) else t
+
+    def _unstage(self, host: torch.Tensor, t: torch.Tensor) -> None:
+        if host is not t:
+            t.copy_(host)
+
+    # -- collectives of the step
 
     def reduce_gradients(self, buf: torch.Tensor, group_rank: int, max_payload: int) -> None:
         """Sum every rank's packed local gradients into the owner's region:
@@ -75,33 +98,65 @@ class GroupExchange:
         full = buf[: self.group_size * max_payload]
         region = buf[group_rank * max_payload:(group_rank + 1) * max_payload]
         if self.group_size > 1:
-            try:
+            if self.staged:  # gloo: no reduce_scatter; all-reduce the whole group layout
+                h = self._stage(full)
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+                self._unstage(h, full)
+            else:
                 dist.reduce_scatter_tensor(region, full, op=dist.ReduceOp.SUM, group=self.group)  # in place
-            except (RuntimeError, NotImplementedError, AttributeError, ValueError):
-                dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.group)  # backends without it (gloo)
         if self.cross is not None:
-            dist.all_reduce(region, op=dist.ReduceOp.SUM, group=self.cross)
+            h = self._stage(region)
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.cross)
+            self._unstage(h, region)
 
     def max_flag(self, flag: torch.Tensor) -> None:
-        """Max over all ranks of a device flag (non-finite gradient anywhere aborts everywhere)."""
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        """Max over the optimizer's ranks of a device flag (non-finite gradient anywhere aborts everywhere)."""
+        h = self._stage(flag)
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.pg)
+        self._unstage(h, flag)
 
     def __call__(self, buf: torch.Tensor, group_rank: int, max_payload: int) -> None:
         if max_payload == 0 or self.group_size == 1:
             return
         region = buf[group_rank * max_payload:(group_rank + 1) * max_payload]
         out = buf[: self.group_size * max_payload]
-        try:
+        if self.staged:
+            # gloo: list all-gather of host copies (same bytes)
+            hr = region.cpu()
+            parts = [torch.empty_like(hr) for _ in range(self.group_size)]
+            dist.all_gather(parts, hr, group=self.group)
+            out.copy_(torch.cat(parts).to(out.device))
+        else:
             dist.all_gather_into_tensor(out, region, group=self.group)  # in place (NCCL)
-        except (RuntimeError, NotImplementedError, AttributeError):
-            # backends without the flat collective (e.g. gloo on CPU): list form, same bytes
-            parts = list(out.split(max_payload))
-            dist.all_gather(parts, region.clone(), group=self.group)
         self.bytes_per_step = (self.group_size - 1) * max_payload * buf.element_size()
+
+    def check_replicas(self, params, tolerance: float = REPLICA_TOLERANCE) -> float:
+        """dist.py:361-368: every rank's parameters must match to ``tolerance`` (max abs).  Exact
+        elementwise check: all-reduce MAX and MIN of the flat float64 parameters over all ranks;
+        raises DivergedReplicasError with the largest drift.  Costs two all-reduces of the
+        parameters, so the optimizer runs it only every ``check_replicas_every`` steps."""
+        flat = torch.cat([p.detach().reshape(-1).to(torch.float64) for p in params]) if params else None
+        if flat is None or flat.numel() == 0:
+            return 0.0
+        hi, lo = self._stage(flat.clone()), self._stage(flat.clone())
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.pg)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.pg)
+        drift = float((hi - lo).abs().max().item())
+        if not drift <= tolerance:
+            raise DivergedReplicasError(f"replicas drifted {drift:.3e} (max over ranks) > {tolerance:g}")
+        return drift
 
 
 class DistributedShampoo(torch.optim.Optimizer):
-    """Drop-in ``torch.optim.Optimizer`` running the B200 Shampoo step."""
+    """Drop-in ``torch.optim.Optimizer`` running the B200 Shampoo step.
+
+    ``step()`` reads ``p.grad`` and updates ``p`` in place.  Learning rate: with the constant
+    schedule the param group's ``lr`` is used every step (so torch LR schedulers work); with
+    ``lr_schedule="warmup_cosine"`` the schedule lr_at(t) (optim.py:133-151) is scaled by
+    ``param_groups[0]['lr'] / lr``.  Parameters whose ``grad`` is None take a zero gradient: their
+    blocks still receive the decoupled weight decay, momentum and factor decay of a zero-gradient
+    step (the reference step requires a gradient for every parameter, optim.py:358-374).
+    """
 
     def __init__(self, params, lr: float = 0.1, betas=(0.0, 0.999), epsilon: float = 1e-12,
                  momentum: float = 0.9, use_nesterov: bool = True, weight_decay: float = 1e-4,
@@ -113,13 +168,18 @@ class DistributedShampoo(torch.optim.Optimizer):
                  newton_tolerance: float = 1e-6, num_trainers_per_group: int = -1,
                  large_dim_method=LargeDimMethod.BLOCKING, precision: str = "double",
                  lr_schedule: str = "constant", warmup_steps: int = 0, total_steps: int = 0,
-                 process_group=None, reduce_gradients: Optional[str] = None):
+                 process_group=None, reduce_gradients: Optional[str] = None,
+                 check_replicas_every: int = 0):
         """``reduce_gradients``: None (p.grad already holds the global gradient, e.g. after DDP) or
         "mean" / "sum": p.grad holds this rank's LOCAL gradient and the optimizer reduce-scatters
-        it to the block owners itself (no separate DDP all-reduce needed)."""
+        it to the block owners itself (no separate DDP all-reduce needed).
+        ``check_replicas_every``: run the replica drift check (dist.py:361-368) every N steps (0: off)."""
         if reduce_gradients not in (None, "mean", "sum"):
             raise ValueError("reduce_gradients must be None, 'mean' or 'sum'")
+        if check_replicas_every < 0:
+            raise ValueError("check_replicas_every must be non-negative")
         self.reduce_gradients = reduce_gradients
+        self.check_replicas_every = int(check_replicas_every)
         grafting = GraftKind(grafting) if not isinstance(grafting, GraftKind) else grafting
         solver = Solver(solver) if not isinstance(solver, Solver) else solver
         large_dim_method = (LargeDimMethod(large_dim_method)
@@ -154,6 +214,17 @@ class DistributedShampoo(torch.optim.Optimizer):
     def guard_stats(self) -> GuardStats:
         return self.engine.guard_stats
 
+    @property
+    def step_count(self) -> int:
+        return self.engine.step_count
+
+    def current_lr(self) -> float:
+        """The learning rate the next step applies (see the class docstring)."""
+        group_lr = float(self.param_groups[0]["lr"])
+        if self.config.lr_schedule == "constant":
+            return group_lr
+        return lr_at(self.config, self.engine.step_count) * (group_lr / self.config.lr)
+
     @torch.no_grad()
     def step(self, closure=None):
         loss = None
@@ -161,10 +232,14 @@ class DistributedShampoo(torch.optim.Optimizer):
             with torch.enable_grad():
                 loss = closure()
         grads = [p.grad if p.grad is not None else torch.zeros_like(p) for p in self._plist]
+        lr = self.current_lr()
         if self.reduce_gradients is None:
-            self.engine.step(grads)
+            self.engine.step(grads, lr=lr)
         else:
-            self.engine.step_local(grads, average=self.reduce_gradients == "mean")
+            self.engine.step_local(grads, average=self.reduce_gradients == "mean", lr=lr)
+        if (self.exchange is not None and self.check_replicas_every
+                and self.engine.step_count % self.check_replicas_every == 0):
+            self.exchange.check_replicas(self._plist)
         return loss
 
     def state_dict(self) -> dict:
@@ -174,3 +249,7 @@ class DistributedShampoo(torch.optim.Optimizer):
 
     def load_state_dict(self, state_dict: dict) -> None:
         self.engine.load_state_tree(state_dict["state"])
+        for g, saved in zip(self.param_groups, state_dict.get("param_groups", [])):
+            for k, v in saved.items():
+                if k != "params":
+                    g[k] = v

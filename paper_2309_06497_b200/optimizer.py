@@ -200,16 +200,18 @@ class Shampoo:
         N.check(lib.shampoo_root_inverse(self._ctx, t, C.byref(r), s), "root_inverse")
         N.check(lib.shampoo_precondition_graft(self._ctx, pp, dtype, t, s), "precondition_graft")
 
-    def apply_gathered(self, t: Optional[int] = None) -> None:
-        """W -= lr(t) * P for every block, from the (gathered) buffer (optim.py:346-354)."""
+    def apply_gathered(self, t: Optional[int] = None, lr: Optional[float] = None) -> None:
+        """W -= lr(t) * P for every block, from the (gathered) buffer (optim.py:346-354).
+        ``lr`` overrides the configured schedule (the torch facade's param-group lr)."""
         t = self._t if t is None else t
-        lr = lr_at(self.config, t)
+        lr = lr_at(self.config, t) if lr is None else float(lr)
         dtype = _dtype_code(self._params[0]) if self._params else N.DTYPE_F32
         pp = N.ptr_array([p.data_ptr() for p in self._params])
         N.check(N.lib().shampoo_apply(self._ctx, pp, dtype, lr, self._stream()), "apply")
 
-    def step(self, grads) -> None:
-        """One full optimizer step (optim.py:356-383); raises before any mutation on bad input."""
+    def step(self, grads, lr: Optional[float] = None) -> None:
+        """One full optimizer step (optim.py:356-383); raises before any mutation on bad input.
+        ``lr``: overrides lr_at(config, t) for this step (torch LR schedulers through the facade)."""
         grads = self._as_grads(grads)
         if self._params:
             dt = {p.dtype for p in self._params}
@@ -223,10 +225,12 @@ class Shampoo:
             N.check(rc, "check_finite")
         t = self._t
         lr_at(self.config, t)  # OutOfRangeError before any mutation
+        if lr is not None and not (float(lr) >= 0.0):
+            raise ValueError("lr must be non-negative")
         self.compute_directions(grads, t)
         if self.exchange is not None and self.group_size > 1:
             self.exchange(self.gather_buffer, self.group_rank, self.max_payload)
-        self.apply_gathered(t)
+        self.apply_gathered(t, lr)
         self._t += 1
 
     # -- gradient reduction to block owners
@@ -248,7 +252,8 @@ class Shampoo:
                 "pack_gradients")
         return buf
 
-    def step_reduced(self, scale: float = 1.0, flag: Optional[torch.Tensor] = None) -> None:
+    def step_reduced(self, scale: float = 1.0, flag: Optional[torch.Tensor] = None,
+                     lr: Optional[float] = None) -> None:
         """One step whose gradients are the reduced buffer (``reduced_gradient_buffer()`` after the
         reduce-scatter): only this rank's owned blocks are read, scaled by ``scale``.  Raises
         NonFiniteGradientError before any mutation if an owned block holds a non-finite entry;
@@ -262,7 +267,7 @@ class Shampoo:
         self.compute_directions_from_buffer(scale, t)
         if self.exchange is not None and self.group_size > 1:
             self.exchange(self.gather_buffer, self.group_rank, self.max_payload)
-        self.apply_gathered(t)
+        self.apply_gathered(t, lr)
         self._t += 1
 
     def compute_directions_from_buffer(self, scale: float = 1.0, t: Optional[int] = None) -> None:
@@ -285,7 +290,7 @@ class Shampoo:
                 "reduced_nonfinite")
         return self._gflag
 
-    def step_local(self, grads, average: bool = True) -> None:
+    def step_local(self, grads, average: bool = True, lr: Optional[float] = None) -> None:
         """Step from this rank's LOCAL gradients: reduce-scatter them to the block owners (+ all-reduce
         across replica groups) instead of a full DDP all-reduce, then the usual step.  ``average``
         divides by the world size (DDP mean).  Single process: identical to ``step(grads)``."""
@@ -297,7 +302,7 @@ class Shampoo:
         flag = self.nonfinite_flag()
         if distributed:
             ex.max_flag(flag)
-        self.step_reduced(1.0 / self.world_size if average else 1.0, flag=flag)
+        self.step_reduced(1.0 / self.world_size if average else 1.0, flag=flag, lr=lr)
 
     # -- parity helpers
 

@@ -119,12 +119,12 @@ def test_root_inverse_batch_mixed_sizes(cuda_device):
         assert rel(x.cpu().numpy(), ref) <= 1e-8
 
 
-def _power_start_vector(n: int, job: int = 0) -> np.ndarray:
+def _power_start_vector(n: int) -> np.ndarray:
     """The deterministic start vector of the Newton pre-pass power iteration (rootinv.cu k_pow_start)."""
     m = (1 << 64) - 1
     x = np.empty(n)
     for e in range(n):
-        h = (((e + 1) * 0x9E3779B97F4A7C15) & m) ^ (((job + 1) * 0xBF58476D1CE4E5B9) & m)
+        h = (((e + 1) * 0x9E3779B97F4A7C15) & m) ^ ((n * 0xBF58476D1CE4E5B9) & m)
         h = ((h ^ (h >> 31)) * 0x94D049BB133111EB) & m
         h ^= h >> 29
         x[e] = (h >> 11) * 2.0 ** -52 - 1.0
