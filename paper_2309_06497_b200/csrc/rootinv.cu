@@ -1247,10 +1247,14 @@ __global__ void __launch_bounds__(256) k_newton_ub_prep(const RootJob* __restric
 // Part 2 (block per job, fixed reduction order): ub = min(||A + eps I||_F, ||(A + eps I)^2||_F^(1/2)).
 __global__ void __launch_bounds__(256) k_newton_ub(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
                                                    NewtonJob* nj, const int32_t* __restrict__ mask,
-                                                   const double* __restrict__ nx, double eps) {
+                                                   const double* __restrict__ nx, double eps, int on) {
   __shared__ double red[32];
   const int j = blockIdx.x;
   const int n = jobs[j].n;
+  if (!on) {  // SHAMPOO_NEWTON_UB=0 (diagnostics only): the power estimate alone, no guarantee
+    if (threadIdx.x == 0) nj[j].ub = 0.0;
+    return;
+  }
   const double fro = sqrt(st[j].norm2 + (eps > 0.0 ? 2.0 * eps * st[j].trace + n * eps * eps : 0.0));
   if (!mask[j]) {
     if (threadIdx.x == 0) nj[j].ub = fro;
@@ -1693,6 +1697,8 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     hybrid_ = nw ? std::atoi(nw) != 0 : true;
     const char* sc = std::getenv("SHAMPOO_NEWTON_SCALE");
     scale_on_ = sc ? std::atoi(sc) != 0 : true;
+    const char* ub = std::getenv("SHAMPOO_NEWTON_UB");
+    ub_on_ = ub ? std::atoi(ub) != 0 : true;
   }
   if (mixed_ && has_big_) {
     SH_CUDA_CHECK(dev_malloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
@@ -1906,6 +1912,10 @@ int RootInverseBatch::build_newton() {
     {
       const double p = host_[j].root_p;
       hn[j].cap = 5 + (int)std::ceil(std::log(kHybridNewtonKappa) / (p * std::log((p + 1.0) / p)));
+      // the stopping test is an inf-norm residual (<= sqrt(n) x the 2-norm): large factors need about
+      // one more quadratic step per doubling past 2048 to reach it (measured: cond 1e6, p = 2 converges
+      // in 18 iterations at n = 4096 and misses the cap by one at 8192)
+      if (host_[j].n > 2048) hn[j].cap += (int)std::ceil(std::log2(host_[j].n / 2048.0));
     }
   }
   SH_CUDA_CHECK(dev_malloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
@@ -1992,7 +2002,7 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
                                                         eps, cand);
     SH_LAUNCH_CHECK();
     if ((rc = newton_sq_.launch(s, mask))) return rc;
-    k_newton_ub<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, nx_, eps);
+    k_newton_ub<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, nx_, eps, ub_on_ ? 1 : 0);
     SH_LAUNCH_CHECK();
     prof_mark("nw_power");
   }
@@ -2135,6 +2145,15 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     std::fprintf(stderr, "[eig] host: run %.2f ms, blocked in syncs %.2f ms, build_newton %.2f ms (jobs %d)\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run0).count(),
                  g_sync_ms, g_build_ms, nj);
+  if (prof.on && newton_built_) {  // pre-pass diagnostics per job
+    std::vector<NewtonJob> hn(nj);
+    SH_CUDA_CHECK(cudaMemcpy(hn.data(), d_newton_, nj * sizeof(NewtonJob), cudaMemcpyDeviceToHost));
+    for (int j = 0; j < nj; ++j)
+      if (host_[j].n >= 512)
+        std::fprintf(stderr, "[eig]   job %d n=%d p=%d: newton its %d vit %.2f cap %d conv %d lam %.6e ub %.6e\n", j,
+                     host_[j].n, host_[j].root_p, hn[j].iters, hn[j].vit, hn[j].cap, hn[j].converged, hn[j].lam,
+                     hn[j].ub);
+  }
   if (prof.on) {  // per-size solver histogram: n:{newton its | jacobi sweeps (w = warm started)}
     std::map<int, std::string> by_n;
     for (int j = 0; j < nj; ++j) {

@@ -155,6 +155,7 @@ class RootInverseBatch {
   std::vector<std::unique_ptr<OzakiGemmBatch<double>>> newton_pow_;
   int32_t* d_cand_ = nullptr;  // eigh jobs tried with the Newton pre-pass
   bool hybrid_ = true;          // SHAMPOO_EIG_NEWTON=0 disables the pre-pass
+  bool ub_on_ = true;           // SHAMPOO_NEWTON_UB=0 (diagnostics): no guaranteed lambda_max bound
   bool scale_on_ = true;        // SHAMPOO_NEWTON_SCALE=0 disables the scaled pre-pass steps (read at setup)
   // reconstruction X = Y Y^T for all jobs (into xs_)
   OzakiGemmBatch<double> recon_;
