@@ -352,8 +352,13 @@ def run_ours(args):
     # ---- 1) the timed window (no per-phase instrumentation)
     grads = resident(args.steps)
     lib.shampoo_tc_counter(1, None)
+    prof = os.environ.get("SHAMPOO_BENCH_PROFILE") == "1"  # ncu --profile-from-start off: this window only
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     with Clocks(local) as clk:
         per, refr, total_ms, host_s, launches = window(grads)
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     value, plain_ms, refresh_ms = amortise(per, refr, f)
     value, plain_ms, refresh_ms, total_ms = max_over_ranks([value, plain_ms, refresh_ms, total_ms])
     window_ms = total_ms / args.steps

@@ -1244,28 +1244,44 @@ __global__ void __launch_bounds__(256) k_newton_ub_prep(const RootJob* __restric
   }
 }
 
-// Part 2 (block per job, fixed reduction order): ub = min(||A + eps I||_F, ||(A + eps I)^2||_F^(1/2)).
-__global__ void __launch_bounds__(256) k_newton_ub(const RootJob* __restrict__ jobs, const RootState* __restrict__ st,
-                                                   NewtonJob* nj, const int32_t* __restrict__ mask,
-                                                   const double* __restrict__ nx, double eps, int on) {
+// Part 2: per element chunk, the partial sum of squares of (A + eps I)^2 (fixed order: deterministic).
+__global__ void __launch_bounds__(256) k_newton_ub_part(const NewtonJob* __restrict__ nj, const int32_t* __restrict__ mask,
+                                                        const int32_t* __restrict__ ebegin, int njobs,
+                                                        const double* __restrict__ nx, double* __restrict__ part) {
   __shared__ double red[32];
-  const int j = blockIdx.x;
-  const int n = jobs[j].n;
+  const int j = find_job(ebegin, njobs, blockIdx.x);
+  if (!mask[j]) return;
+  const int64_t tot = (int64_t)nj[j].n * nj[j].n;
+  const double* Q = nx + nj[j].off + kNTSlot * tot;
+  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
+  double q = 0.0;
+  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) q = fma(Q[e], Q[e], q);
+  q = block_sum<double, 256>(q, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = q;
+}
+
+// Part 3 (warp per job): ub = min(||A + eps I||_F, ||(A + eps I)^2||_F^(1/2) (1 + margin)).
+__global__ void k_newton_ub(const RootJob* __restrict__ jobs, const RootState* __restrict__ st, NewtonJob* nj,
+                            const int32_t* __restrict__ mask, const int32_t* __restrict__ ebegin, int njobs,
+                            int echunks, const double* __restrict__ part, double eps, int on) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= njobs) return;
   if (!on) {  // SHAMPOO_NEWTON_UB=0 (diagnostics only): the power estimate alone, no guarantee
-    if (threadIdx.x == 0) nj[j].ub = 0.0;
+    if (lane == 0) nj[j].ub = 0.0;
     return;
   }
+  const int n = jobs[j].n;
   const double fro = sqrt(st[j].norm2 + (eps > 0.0 ? 2.0 * eps * st[j].trace + n * eps * eps : 0.0));
   if (!mask[j]) {
-    if (threadIdx.x == 0) nj[j].ub = fro;
+    if (lane == 0) nj[j].ub = fro;
     return;
   }
-  const int64_t tot = (int64_t)n * n;
-  const double* Q = nx + nj[j].off + kNTSlot * tot;
+  const int c0 = ebegin[j], c1 = j + 1 < njobs ? ebegin[j + 1] : echunks;
   double q = 0.0;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) q = fma(Q[e], Q[e], q);
-  q = block_sum<double, 256>(q, red);
-  if (threadIdx.x == 0) nj[j].ub = fmin(fro, sqrt(sqrt(q)) * (1.0 + 1e-3));  // 3-slice square: margin
+  for (int c = c0 + lane; c < c1; c += 32) q += part[c];
+  q = warp_sum(q);
+  if (lane == 0) nj[j].ub = fmin(fro, sqrt(sqrt(q)) * (1.0 + 1e-3));  // 3-slice square: margin
 }
 
 __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__ jobs, RootState* st,
@@ -1567,6 +1583,7 @@ RootInverseBatch::~RootInverseBatch() {
   dev_free(d_resbits_);
   dev_free(d_improved_);
   dev_free(d_mask2_);
+  dev_free(d_part_);
   dev_free(pack_arena_);
   dev_free(d_pair_begin_);
   dev_free(d_item_begin_);
@@ -1923,6 +1940,7 @@ int RootInverseBatch::build_newton() {
   SH_CUDA_CHECK(cudaMemset(d_resbits_, 0, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(dev_malloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
   SH_CUDA_CHECK(dev_malloc(&d_mask2_, std::max(nj, 1) * sizeof(int32_t)));
+  SH_CUDA_CHECK(dev_malloc(&d_part_, std::max(total_elem_chunks_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMemcpy(d_newton_, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice));
   // GEMM sets for cur = 0/1: X_nxt = X_cur T ; T^p ; M_nxt = T^p M_cur (tcgen05 Ozaki, FP64 class)
   size_t nsteps = 0;
@@ -2002,7 +2020,10 @@ int RootInverseBatch::newton_phase(double eps, double tol, int budget, const int
                                                         eps, cand);
     SH_LAUNCH_CHECK();
     if ((rc = newton_sq_.launch(s, mask))) return rc;
-    k_newton_ub<<<nj, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, nx_, eps, ub_on_ ? 1 : 0);
+    k_newton_ub_part<<<total_elem_chunks_, 256, 0, s>>>(dn, mask, d_elem_begin_, nj, nx_, d_part_);
+    SH_LAUNCH_CHECK();
+    k_newton_ub<<<(nj + 7) / 8, 256, 0, s>>>(d_jobs_, d_state_, dn, mask, d_elem_begin_, nj, total_elem_chunks_, d_part_,
+                                             eps, ub_on_ ? 1 : 0);
     SH_LAUNCH_CHECK();
     prof_mark("nw_power");
   }

@@ -146,7 +146,8 @@ class RootInverseBatch {
   NewtonJob* d_newton_ = nullptr;
   unsigned long long* d_resbits_ = nullptr;  // per job max row sum of |M - I| (bit pattern)
   int32_t* d_improved_ = nullptr;
-  int32_t* d_mask2_ = nullptr;  // Newton: jobs that still need T^p and M (not in their final step)
+  int32_t* d_mask2_ = nullptr;
+  double* d_part_ = nullptr;    // per element-chunk partial sums (lambda_max bound)  // Newton: jobs that still need T^p and M (not in their final step)
   int8_t* pack_arena_ = nullptr;  // one pack space for all of this batch's Ozaki GEMM sets (sequential)
   int64_t pack_cap_ = 0;
   bool newton_built_ = false;
