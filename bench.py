@@ -431,8 +431,9 @@ def run_ours(args):
                   note="steady-state refresh: coupled-Newton pre-pass GEMMs on the tcgen05 Ozaki engine (+ "
                        "power iterations, residual checks); fp64_equivalent counts a tridiagonal eigh (9 n^3)")
         kernels["root_inverse"] = ri
-    graft_bytes = n_el * (esz * 4 + 4)  # P_sh read, momentum r/w, direction write, fp32 W read (WD)
-    apply_bytes = n_el * (esz + 8)      # direction read + fp32 W read/write
+    besz = opt.gather_buffer.element_size()  # float32 directions for float32 parameters
+    graft_bytes = n_el * (esz * 3 + 4 + besz)  # P_sh read, momentum r/w, fp32 W read (WD), direction write
+    apply_bytes = n_el * (besz + 8)            # direction read + fp32 W read/write
     for k, b in (("graft_momentum", graft_bytes), ("apply", apply_bytes)):
         m = per_call[k]
         a = b / (m * 1e-3) / 1e9 if m else 0.0

@@ -75,6 +75,8 @@ extern "C" {
 
 #define SHAMPOO_DTYPE_F32 0        /* element type of caller tensors */
 #define SHAMPOO_DTYPE_F64 1
+#define SHAMPOO_GATHER_STATE 0     /* shampoo_config.gather_dtype */
+#define SHAMPOO_GATHER_F32 1
 
 #define SHAMPOO_BLOCK_SHAMPOO 0    /* BlockSlot.kind */
 #define SHAMPOO_BLOCK_GRAFT_ONLY 1
@@ -122,6 +124,11 @@ typedef struct {
   int32_t solver;                      /* SHAMPOO_SOLVER_* */
   double newton_tolerance;
   int32_t precision;                   /* SHAMPOO_PRECISION_* */
+  /* search-direction gather buffer: SHAMPOO_GATHER_STATE (0) = the precision's dtype,
+   * SHAMPOO_GATHER_F32 (1) = float32 (for float32 parameters: the update W -= lr * p lands in
+   * float32 anyway, and the all-gather moves half the bytes).  Not a reference field: the
+   * reference's f64 wire scalar (dist.py:48-50) is a simulation detail. */
+  int32_t gather_dtype;
 } shampoo_config;
 
 /* Counters of matfun.GuardStats (matfun.py:98-105). */

@@ -50,7 +50,7 @@ class Config(C.Structure):
         ("exponent_multiplier", C.c_double), ("grafting", C.c_int32),
         ("grafting_epsilon", C.c_double), ("grafting_beta2", C.c_double),
         ("large_dim_method", C.c_int32), ("solver", C.c_int32), ("newton_tolerance", C.c_double),
-        ("precision", C.c_int32),
+        ("precision", C.c_int32), ("gather_dtype", C.c_int32),
     ]
 
 

@@ -113,6 +113,7 @@ struct shampoo_ctx {
   shampoo_config cfg{};
   int32_t rank = 0, grank = 0, device = 0;
   bool f32 = false;
+  bool buf_f32 = false;  // float32 gather buffer (cfg.gather_dtype)
   bool low_rank = true;  // low-rank root-inverse path (SHAMPOO_EIG_LOWRANK=0 disables)
   size_t esz = 8;
   int32_t nparams = 0;
@@ -228,6 +229,7 @@ StepScalars make_scalars(const shampoo_ctx* c, int64_t t, int32_t dtype, int64_t
   sc.precond = (double)t >= k.start_preconditioning_step;
   sc.pdtype = dtype;
   sc.lr = k.lr;
+  sc.buf_f32 = c->buf_f32;
   return sc;
 }
 
@@ -378,6 +380,8 @@ int check_cfg(const shampoo_config* k) {
   if (k->grafting < 0 || k->grafting > 6) return bad("unknown grafting kind");
   if (k->solver == SHAMPOO_SOLVER_NEWTON && k->exponent_multiplier != 1.0)
     return bad("the coupled Newton solver supports exponent_multiplier=1 only");
+  if (k->gather_dtype != SHAMPOO_GATHER_STATE && k->gather_dtype != SHAMPOO_GATHER_F32)
+    return bad("gather_dtype must be SHAMPOO_GATHER_STATE or SHAMPOO_GATHER_F32");
   return SHAMPOO_OK;
 }
 
@@ -405,6 +409,7 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   c->grank = rank % plan->group;
   c->device = device;
   c->f32 = cfg->precision == SHAMPOO_PRECISION_SINGLE;
+  c->buf_f32 = c->f32 || cfg->gather_dtype == SHAMPOO_GATHER_F32;
   c->esz = c->f32 ? 4 : 8;
   c->nparams = (int32_t)plan->params.size();
   const int nb = (int)plan->blocks.size();
@@ -511,7 +516,7 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
       {&c->T2, c->any_order3 ? E * es : 0},
       {&c->FACT, (size_t)c->n_fac * es},
       {&c->INV, (size_t)c->n_fac * es},
-      {&c->BUF, std::max<size_t>(buf_elems, 1) * es},
+      {&c->BUF, std::max<size_t>(buf_elems, 1) * (c->buf_f32 ? 4 : es)},
       {(void**)&c->part, std::max<size_t>(oc.size(), 1) * 8},
       {(void**)&c->gnorm2, std::max<size_t>(no, 1) * 8},
       {(void**)&c->pg2, std::max<size_t>(no, 1) * 8},
@@ -894,6 +899,7 @@ int shampoo_apply(shampoo_ctx* c, void* const* params, int32_t dtype, double lr,
   StepScalars sc{};
   sc.lr = lr;
   sc.pdtype = dtype;
+  sc.buf_f32 = c->buf_f32;
   void* const* pp = (void* const*)(c->d_ptrs + c->nparams);
   {
     PhaseScope scope(&c->timer, 4, s);
@@ -973,7 +979,7 @@ int shampoo_work_tc(shampoo_ctx* c, double* stats_int8_ops, double* precond_int8
 
 void* shampoo_gather_buffer(shampoo_ctx* c, int64_t* scalars, int32_t* dtype) {
   if (scalars) *scalars = (int64_t)c->plan.group * c->plan.max_payload;
-  if (dtype) *dtype = c->f32 ? SHAMPOO_DTYPE_F32 : SHAMPOO_DTYPE_F64;
+  if (dtype) *dtype = c->buf_f32 ? SHAMPOO_DTYPE_F32 : SHAMPOO_DTYPE_F64;
   return c->BUF;
 }
 

@@ -149,7 +149,7 @@ __global__ void k_block_reduce(const int32_t* __restrict__ cb, const int32_t* __
   if (lane == 0) out[b] = s;
 }
 
-template <typename T>
+template <typename T, typename BT>
 __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
                                               const DevBlock* __restrict__ blocks,
                                               const void* const* __restrict__ params, StepScalars sc,
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
   const T* GA = static_cast<const T*>(ar.GA) + B.vofs;
   const T* PS = static_cast<const T*>(ar.PS) + B.vofs;
   T* M = static_cast<T*>(ar.MOM) + B.vofs;
-  T* out = static_cast<T*>(ar.BUF) + B.gofs;
+  BT* out = static_cast<BT*>(ar.BUF) + B.gofs;
   const void* wp = params[B.param];
   const bool use_ps = sc.precond && ((B.kind == SHAMPOO_BLOCK_SHAMPOO && ar.ready[B.local]) ||
                                      B.kind == SHAMPOO_BLOCK_ADAGRAD || B.kind == SHAMPOO_BLOCK_DIAGONAL);
@@ -201,19 +201,19 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
         M[j] = m;
         p = sc.nesterov ? T(sc.momentum) * m + p : m;
       }
-      out[j] = p;
+      out[j] = BT(p);
     }
   }
 }
 
-template <typename T>
+template <typename BT>
 __global__ void __launch_bounds__(NT) k_apply(const Chunk* __restrict__ chunks,
                                               const DevBlock* __restrict__ blocks,
                                               void* const* __restrict__ params,
-                                              const T* __restrict__ buf, double lr, int32_t pdtype) {
+                                              const BT* __restrict__ buf, double lr, int32_t pdtype) {
   const Chunk c = chunks[blockIdx.x];
   const DevBlock& B = blocks[c.block];
-  const T* p = buf + B.gofs;
+  const BT* p = buf + B.gofs;
   void* wp = params[B.param];
   for (int64_t e = threadIdx.x; e < c.count; e += NT) {
     const int64_t j = c.start + e;
@@ -388,7 +388,8 @@ template <typename T>
 int launch_final(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* params,
                  const StepScalars& sc, const ElemArenas& ar, cudaStream_t s) {
   if (!nchunks) return SHAMPOO_OK;
-  k_final<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, sc, ar);
+  if (sc.buf_f32) k_final<T, float><<<nchunks, NT, 0, s>>>(chunks, blocks, params, sc, ar);
+  else k_final<T, T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, sc, ar);
   SH_LAUNCH_CHECK();
   return SHAMPOO_OK;
 }
@@ -397,7 +398,9 @@ template <typename T>
 int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
                  const void* buf, const StepScalars& sc, cudaStream_t s) {
   if (!nchunks) return SHAMPOO_OK;
-  k_apply<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const T*>(buf), sc.lr, sc.pdtype);
+  if (sc.buf_f32) k_apply<float><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const float*>(buf), sc.lr,
+                                                        sc.pdtype);
+  else k_apply<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const T*>(buf), sc.lr, sc.pdtype);
   SH_LAUNCH_CHECK();
   return SHAMPOO_OK;
 }

@@ -22,6 +22,7 @@ struct StepScalars {
   int32_t precond;     // t >= start_preconditioning_step
   int32_t pdtype;      // caller tensor dtype
   int32_t gbuf;        // gradients come from the reduced gradient buffer (ElemArenas::GBUF), not grads[]
+  int32_t buf_f32;     // the gather buffer holds float32 directions (else the context dtype)
   double gscale;       // multiplier on buffer gradients (1/world for a mean reduction)
 };
 

@@ -1,7 +1,7 @@
-// Grouped, strided GEMM on CUDA cores (FP64 DFMA / FP32 FFMA) and a grouped
-// GEMV.  One launch covers every problem of a phase (all blocks, all modes)
-// through a device-side tile table, so a step costs O(phases) launches, not
-// O(blocks).
+// Grouped, strided GEMM problem descriptors (executed by the tcgen05 Ozaki engine, tcgen05.cuh, or
+// the thin-problem kernels, thin.cuh) and a grouped GEMV.  One launch covers every problem of a
+// phase (all blocks, all modes) through a device-side tile table, so a step costs O(phases)
+// launches, not O(blocks).
 //
 //   C[i,j] = alpha * sum_k A(i,k) * B(j,k) + beta * C[i,j]
 //   X(r,k) = X + idx2(r; rdiv, rhi, rlo) + idx2(k; kdiv, khi, klo)
@@ -62,32 +62,6 @@ struct GemvProblem {
   const void* x;  // n
   void* y;        // n
   double alpha;
-};
-
-// A set of problems uploaded once and launched many times.
-template <typename T>
-class GemmBatch {
- public:
-  std::vector<GemmProblem> host;
-  bool fp64_accumulate = false;  // float storage, FP64 tensor-core accumulation (exact products)
-  GemmBatch() = default;
-  GemmBatch(const GemmBatch&) = delete;
-  GemmBatch& operator=(const GemmBatch&) = delete;
-  ~GemmBatch();
-  void add(const GemmProblem& p) { host.push_back(p); }
-  bool empty() const { return host.empty(); }
-  int upload();
-  int launch(cudaStream_t s, const int32_t* mask = nullptr) const;
-  double flops() const;  // algorithmic 2*M*N*K (SYM counted as full)
-
- private:
-  GemmProblem* d_prob_ = nullptr;
-  int64_t* d_begin_ = nullptr;
-  int64_t* d_rbegin_ = nullptr;   // split-K reduce tile prefix
-  int32_t* d_rprob_ = nullptr;
-  double* ws_ = nullptr;          // split-K partial tiles
-  int64_t total_items_ = 0, total_red_ = 0;
-  int nred_ = 0;
 };
 
 template <typename T>

@@ -688,293 +688,6 @@ __global__ void __launch_bounds__(256) k_book(const RootJob* __restrict__ jobs, 
   if (threadIdx.x == 0) *count = act;
 }
 
-// ---------------------------------------------------------------- FP32 phase (mixed precision)
-//
-// Phase 1 of the mixed-precision eigensolver: the same block-Jacobi rounds on an FP32 copy of A
-// (big jobs only) accumulate an FP32 eigenvector estimate V32.  Phase 2 (FP64) promotes V32,
-// re-orthonormalises it with two Newton-Schulz steps, forms B = V^T A0 V from the ORIGINAL A0
-// and finishes with the FP64 rounds (quadratic convergence: 2-3 sweeps instead of 10-16).
-// FP32 rounding only changes the starting basis of the FP64 phase, never the result's accuracy.
-
-constexpr int S32_U = 0, S32_D = NS * NS, S32_F = NS * NS + NS, S32_S = NS * NS + NS + 4;
-constexpr int SLOT32 = S32_S + NS * NS;  // multiple of 4 floats: every slot is 16-byte aligned
-constexpr int LDF = NS + 4;             // 68 floats: 16-byte aligned smem rows
-constexpr int MAX_SWEEPS32 = 30;
-
-__device__ __forceinline__ float tol32_abs(double norm2) { return (float)(0.1 * 5.9604645e-8 * sqrt(norm2)); }
-__device__ __forceinline__ float tol32_null(double norm2) { return (float)(8.0 * 5.9604645e-8 * sqrt(norm2)); }
-
-// Phase counters: round = sweep = rotated = 0; active = (big_only ? m > 0 : true) && status ok && n > 0.
-__global__ void k_phase_reset(const RootJob* __restrict__ jobs, RootState* st, int32_t* mask, int njobs,
-                              int big_only) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= njobs) return;
-  RootState& s = st[j];
-  s.sweep32 = big_only ? 0 : (jobs[j].m > 0 ? s.sweep : 0);
-  s.round = 0;
-  s.sweep = 0;
-  s.rotated = 0;
-  s.capped = 0;
-  s.active = (s.status == kEigOk && jobs[j].n > 0 && (!big_only || jobs[j].m > 0)) ? 1 : 0;
-  mask[j] = s.active;
-}
-
-// ws32 = (float) ws (np x np, zero padding included), vs32 = I, for active (big) jobs.
-__global__ void __launch_bounds__(256) k_init32(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
-                                                const int32_t* __restrict__ ebegin, int njobs,
-                                                const double* __restrict__ ws, float* __restrict__ ws32,
-                                                float* __restrict__ vs32) {
-  const int j = find_job(ebegin, njobs, blockIdx.x);
-  if (!mask[j]) return;
-  const RootJob& J = jobs[j];
-  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
-  const int64_t tot = (int64_t)J.np * J.np;
-  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
-    ws32[J.ws_off + e] = (float)ws[J.ws_off + e];
-    vs32[J.ws_off + e] = (e / J.np == e % J.np) ? 1.f : 0.f;
-  }
-}
-
-__global__ void __launch_bounds__(256, 6) k_subsolve32(const RootJob* __restrict__ jobs, RootState* st,
-                                                    const int32_t* __restrict__ pbegin, int njobs,
-                                                    float* __restrict__ ws32, float* __restrict__ us32) {
-  extern __shared__ float smf[];
-  float* S = smf;
-  float* U = smf + NS * LDS_;
-  const int j = find_job(pbegin, njobs, blockIdx.x);
-  if (!st[j].active) return;
-  const RootJob& J = jobs[j];
-  const int pair = blockIdx.x - pbegin[j];
-  const int np = J.np, r = st[j].round;
-  const int ra = circle_pos(r, pair, J.m), rb = circle_pos(r, J.m - 1 - pair, J.m);
-  const float* A = ws32 + J.ws_off;
-  auto gidx = [&](int x) { return x < HB ? ra * HB + x : rb * HB + (x - HB); };
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-    const int i = e >> 6, k = e & 63;
-    S[i * LDS_ + k] = A[(int64_t)gidx(i) * np + gidx(k)];
-  }
-  __syncthreads();
-  const float tol_abs = tol32_abs(st[j].norm2), tol_null = tol32_null(st[j].norm2);
-  constexpr float UR = EigU<float>::u;
-  float* slot = us32 + (J.u_off / SLOT) * SLOT32 + (int64_t)pair * SLOT32;
-  int need = 0;
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-    const int i = e >> 6, k = e & 63;
-    if (i >= k) continue;
-    const float app = S[i * LDS_ + i], aqq = S[k * LDS_ + k];
-    float thr = fmaxf(4.f * UR * sqrtf(fabsf(app)) * sqrtf(fabsf(aqq)), tol_abs);
-    if (fabsf(app) <= tol_null && fabsf(aqq) <= tol_null) thr = fmaxf(thr, tol_null);
-    if (fabsf(S[i * LDS_ + k]) > thr) need = 1;
-  }
-  if (!__syncthreads_or(need)) {
-    if (threadIdx.x == 0) slot[S32_F] = 0.f;
-    return;
-  }
-  const int any = cta_jacobi64_sweep<float>(S, U, tol_abs, tol_null);
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-    const int a = e >> 6, b = e & 63;
-    slot[S32_U + e] = U[a * LDS_ + b];
-    slot[S32_S + e] = (a <= b) ? S[a * LDS_ + b] : S[b * LDS_ + a];
-  }
-  if (threadIdx.x == 0) {
-    slot[S32_F] = any ? 1.f : 0.f;
-    if (any) st[j].rotated = 1;
-  }
-}
-
-// C(64x64) = X' Y on CUDA cores (FFMA); X'(r,k) = TX ? X[k][r] : X[r][k]; smem ld LDF.
-// Thread (ty, tx) owns rows 4ty..4ty+3 and columns 4tx..4tx+3.
-template <bool TX>
-__device__ __forceinline__ void mm64f(const float* X, const float* Y, float (&c)[4][4]) {
-  const int r0 = (threadIdx.x >> 4) * 4, c0 = (threadIdx.x & 15) * 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) c[i][q] = 0.f;
-#pragma unroll 8
-  for (int k = 0; k < NS; ++k) {
-    float a[4];
-    if (TX) {
-      const float4 v = *reinterpret_cast<const float4*>(X + k * LDF + r0);
-      a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = X[(r0 + i) * LDF + k];
-    }
-    const float4 b = *reinterpret_cast<const float4*>(Y + k * LDF + c0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      c[i][0] = fmaf(a[i], b.x, c[i][0]);
-      c[i][1] = fmaf(a[i], b.y, c[i][1]);
-      c[i][2] = fmaf(a[i], b.z, c[i][2]);
-      c[i][3] = fmaf(a[i], b.w, c[i][3]);
-    }
-  }
-}
-
-__device__ __forceinline__ void mm64f_store(float* Z, const float (&c)[4][4]) {
-  const int r0 = (threadIdx.x >> 4) * 4, c0 = (threadIdx.x & 15) * 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    *reinterpret_cast<float4*>(Z + (r0 + i) * LDF + c0) = make_float4(c[i][0], c[i][1], c[i][2], c[i][3]);
-}
-
-__device__ __forceinline__ void load_pair_tile32(float* dst, const float* src, int64_t ld, const int* rows,
-                                                 int col0, int col1) {
-  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
-    const int a = e >> 4, b = (e & 15) * 4;
-    const int gc = b < HB ? col0 + b : col1 + (b - HB);
-    float* d = dst + a * LDF + b;
-    if (rows[a] >= 0) cp16(d, src + (int64_t)rows[a] * ld + gc);
-    else cp16_zero(d, src);
-  }
-}
-
-__device__ __forceinline__ void load_slot32(float* dst, const float* slot) {
-  for (int e = threadIdx.x; e < NS * 16; e += blockDim.x) {
-    const int a = e >> 4, b = (e & 15) * 4;
-    cp16(dst + a * LDF + b, slot + a * NS + b);
-  }
-}
-
-// FP32 counterpart of k_apply: A <- W^T A W (pair tiles P<=Q), V <- V W.
-__global__ void __launch_bounds__(256, 4) k_apply32(const RootJob* __restrict__ jobs,
-                                                    const RootState* __restrict__ st,
-                                                    const int32_t* __restrict__ ibegin, int njobs,
-                                                    float* __restrict__ ws32, float* __restrict__ vs32,
-                                                    const float* __restrict__ us32) {
-  extern __shared__ __align__(16) float smf[];
-  float* X = smf;
-  float* WQ = smf + NS * LDF;
-  float* WP = smf + 2 * NS * LDF;
-  __shared__ int rows[NS];
-  const int j = find_job(ibegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
-  if (J.m == 0 || !st[j].active) return;
-  const int item = blockIdx.x - ibegin[j];
-  const int h = J.m / 2, np = J.np, r = st[j].round;
-  const int nA = h * (h + 1) / 2;
-  const float* slots = us32 + (J.u_off / SLOT) * SLOT32;
-  auto blk = [&](int P, int half) { return half == 0 ? circle_pos(r, P, J.m) : circle_pos(r, J.m - 1 - P, J.m); };
-  float acc[4][4];
-  float* A = ws32 + J.ws_off;
-  if (item < nA) {
-    int Q, P;
-    tri_decode(item, Q, P);  // Q >= P
-    const float* sP = slots + (int64_t)P * SLOT32;
-    const float* sQ = slots + (int64_t)Q * SLOT32;
-    const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
-    if (P == Q) {
-      if (sP[S32_F] == 0.f) return;
-      const float* Sp = sP + S32_S;
-      for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-        const int a = e >> 6, b = e & 63;
-        A[(int64_t)(a < HB ? p0 + a : p1 + a - HB) * np + (b < HB ? p0 + b : p1 + b - HB)] = Sp[e];
-      }
-      return;
-    }
-    const bool rp = sP[S32_F] != 0.f, rq = sQ[S32_F] != 0.f;
-    if (!rp && !rq) return;
-    const int q0 = blk(Q, 0) * HB, q1 = blk(Q, 1) * HB;
-    if (threadIdx.x < NS) rows[threadIdx.x] = threadIdx.x < HB ? p0 + threadIdx.x : p1 + threadIdx.x - HB;
-    __syncthreads();
-    load_pair_tile32(X, A, np, rows, q0, q1);
-    if (rq) load_slot32(WQ, sQ);
-    if (rp) load_slot32(WP, sP);
-    cp_commit_wait_all();
-    __syncthreads();
-    if (rq) {  // T = X UQ
-      mm64f<false>(X, WQ, acc);
-      __syncthreads();
-      mm64f_store(X, acc);
-      __syncthreads();
-    }
-    if (rp) {  // R = UP^T T
-      mm64f<true>(WP, X, acc);
-      __syncthreads();
-      mm64f_store(X, acc);
-      __syncthreads();
-    }
-    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-      const int a = e >> 6, b = e & 63;
-      A[(int64_t)rows[a] * np + (b < HB ? q0 + b : q1 + b - HB)] = X[a * LDF + b];
-    }
-    for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-      const int b = e >> 6, a = e & 63;
-      A[(int64_t)(b < HB ? q0 + b : q1 + b - HB) * np + rows[a]] = X[a * LDF + b];
-    }
-    return;
-  }
-  const int v = item - nA;
-  const int P = v % h, R = v / h;
-  const float* sP = slots + (int64_t)P * SLOT32;
-  if (sP[S32_F] == 0.f) return;
-  float* V = vs32 + J.ws_off;
-  const int r0 = R * NS;
-  const int p0 = blk(P, 0) * HB, p1 = blk(P, 1) * HB;
-  if (threadIdx.x < NS) rows[threadIdx.x] = (r0 + threadIdx.x < np) ? r0 + threadIdx.x : -1;
-  __syncthreads();
-  load_pair_tile32(X, V, np, rows, p0, p1);
-  load_slot32(WP, sP);
-  cp_commit_wait_all();
-  __syncthreads();
-  mm64f<false>(X, WP, acc);
-  __syncthreads();
-  mm64f_store(X, acc);
-  __syncthreads();
-  for (int e = threadIdx.x; e < NS * NS; e += blockDim.x) {
-    const int a = e >> 6, b = e & 63;
-    if (rows[a] >= 0) V[(int64_t)rows[a] * np + (b < HB ? p0 + b : p1 + b - HB)] = X[a * LDF + b];
-  }
-}
-
-// dst (ld np, n x n block) = (double) vs32; dst = ws for warm jobs (then ts = V_prev ws), else ts.
-__global__ void __launch_bounds__(256) k_promote32(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
-                                                   const int32_t* __restrict__ ebegin, int njobs,
-                                                   const float* __restrict__ vs32, double* __restrict__ ws,
-                                                   double* __restrict__ ts) {
-  const int j = find_job(ebegin, njobs, blockIdx.x);
-  if (!mask[j]) return;
-  const RootJob& J = jobs[j];
-  double* dst = J.warm ? ws : ts;
-  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
-  const int64_t tot = (int64_t)J.np * J.np;
-  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
-    const int i = (int)(e / J.np), k = (int)(e % J.np);
-    if (i < J.n && k < J.n) dst[J.ws_off + e] = (double)vs32[J.ws_off + e];
-  }
-}
-
-// Newton-Schulz polynomial: ws <- (3 I - ws) / 2 on the n x n block.
-__global__ void __launch_bounds__(256) k_ns_poly(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
-                                                 const int32_t* __restrict__ ebegin, int njobs,
-                                                 double* __restrict__ ws) {
-  const int j = find_job(ebegin, njobs, blockIdx.x);
-  if (!mask[j]) return;
-  const RootJob& J = jobs[j];
-  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
-  const int64_t tot = (int64_t)J.np * J.np;
-  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
-    const int i = (int)(e / J.np), k = (int)(e % J.np);
-    if (i < J.n && k < J.n) ws[J.ws_off + e] = (i == k ? 1.5 : 0.0) - 0.5 * ws[J.ws_off + e];
-  }
-}
-
-// dst <- src on the n x n block (ld np).
-__global__ void __launch_bounds__(256) k_copy_n(const RootJob* __restrict__ jobs, const int32_t* __restrict__ mask,
-                                                const int32_t* __restrict__ ebegin, int njobs,
-                                                const double* __restrict__ src, double* __restrict__ dst) {
-  const int j = find_job(ebegin, njobs, blockIdx.x);
-  if (!mask[j]) return;
-  const RootJob& J = jobs[j];
-  const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
-  const int64_t tot = (int64_t)J.np * J.np;
-  for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
-    const int i = (int)(e / J.np), k = (int)(e % J.np);
-    if (i < J.n && k < J.n) dst[J.ws_off + e] = src[J.ws_off + e];
-  }
-}
-
 // ---------------------------------------------------------------- reconstruction
 
 // Rayleigh-Ritz eigenvalues lambda_k = v_k^T A0 v_k from the ORIGINAL matrix (T = A0 V in ws):
@@ -1591,10 +1304,6 @@ RootInverseBatch::~RootInverseBatch() {
   dev_free(d_col_begin_);
   dev_free(d_count_);
   dev_free(d_stats_);
-  dev_free(ws32_);
-  dev_free(vs32_);
-  dev_free(us32_);
-  dev_free(d_mix_);
 }
 
 double RootInverseBatch::work_n3() const {
@@ -1699,15 +1408,12 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     pack_cap_ += 2 * ks * rc * OzakiGemmBatch<double>::kDefaultSlices * 256;
   }
   SH_CUDA_CHECK(dev_malloc(&pack_arena_, std::max<int64_t>(pack_cap_, 256)));
-  for (auto* b : {&recon_, &rr_, &warm1_, &warm2_, &newton_x_[0], &newton_x_[1], &newton_m_[0], &newton_m_[1], &g_wv_,
-                  &g_s1_, &g_v1_, &g_s2_, &g_v2_})
+  for (auto* b : {&recon_, &rr_, &warm1_, &warm2_, &newton_x_[0], &newton_x_[1], &newton_m_[0], &newton_m_[1]})
     b->set_external_arena(pack_arena_, pack_cap_);
   int rc = recon_.upload();
   if (rc) return rc;
   if ((rc = rr_.upload())) return rc;
   {
-    const char* env = std::getenv("SHAMPOO_EIG_MIXED");
-    mixed_ = env ? std::atoi(env) != 0 : false;  // measured: no net gain with SIMT FP32 rounds
     const char* cr = std::getenv("SHAMPOO_EIG_CROSS");
     cross_only_ = cr ? std::atoi(cr) != 0 : true;
     const char* nw = std::getenv("SHAMPOO_EIG_NEWTON");
@@ -1717,40 +1423,12 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
     const char* ub = std::getenv("SHAMPOO_NEWTON_UB");
     ub_on_ = ub ? std::atoi(ub) != 0 : true;
   }
-  if (mixed_ && has_big_) {
-    SH_CUDA_CHECK(dev_malloc(&ws32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
-    SH_CUDA_CHECK(dev_malloc(&vs32_, std::max<int64_t>(ws_elems_, 1) * sizeof(float)));
-    SH_CUDA_CHECK(dev_malloc(&us32_, std::max<int64_t>(u_elems_ / SLOT * SLOT32, 1) * sizeof(float)));
-    SH_CUDA_CHECK(dev_malloc(&d_mix_, nj * sizeof(int32_t)));
-    if (!ts_) SH_CUDA_CHECK(dev_malloc(&ts_, std::max<int64_t>(ws_elems_, 1) * sizeof(double)));
-    if ((rc = build_warm_gemms())) return rc;
-    for (size_t j = 0; j < nj; ++j) {
-      const RootJob& J = host_[j];
-      if (J.m == 0) continue;
-      double *ws = ws_ + J.ws_off, *vs = vs_ + J.v_off, *ts = ts_ + J.ws_off;
-      auto add = [&](OzakiGemmBatch<double>& b, bool ta, const double* A, const double* B, double* Cm, bool sym) {
-        GemmProblem g = make_gemm(ta, false, J.n, J.n, J.n, A, J.np, B, J.np, Cm, J.np, 1.0, 0.0);
-        g.flags |= kGemmMasked | (sym ? kGemmSym : 0);
-        g.mask_index = (int32_t)j;
-        b.add(g);
-      };
-      add(g_wv_, false, vs, ws, ts, false);  // ts = V_prev V32 (warm jobs)
-      add(g_s1_, true, ts, ts, ws, true);    // S = ts^T ts
-      add(g_v1_, false, ts, ws, vs, false);  // vs = ts (3I - S)/2
-      add(g_s2_, true, vs, vs, ws, true);    // S = vs^T vs
-      add(g_v2_, false, vs, ws, ts, false);  // ts = vs (3I - S)/2
-    }
-    for (auto* b : {&g_wv_, &g_s1_, &g_v1_, &g_s2_, &g_v2_})
-      if ((rc = b->upload())) return rc;
-  }
   static bool attr_done = false;
   if (!attr_done) {
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_subsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        2 * NS * LDS_ * (int)sizeof(double)));
     SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        NS * LDT * (int)sizeof(double)));
-    SH_CUDA_CHECK(cudaFuncSetAttribute(k_apply32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       3 * NS * LDF * (int)sizeof(float)));
     attr_done = true;
   }
   return SHAMPOO_OK;
@@ -1794,56 +1472,6 @@ int RootInverseBatch::prepare_warm(cudaStream_t s) {
   if ((rc = warm2_.launch(s, d_warm_))) return rc;
   k_symmetrize<<<total_elem_chunks_, 256, 0, s>>>(d_jobs_, d_warm_, d_elem_begin_, (int)host_.size(), ws_);
   SH_LAUNCH_CHECK();
-  return SHAMPOO_OK;
-}
-
-int RootInverseBatch::run_mixed_phase(cudaStream_t s, bool any_warm) {
-  const int nj = (int)host_.size();
-  int32_t* mask = d_count_ + 4;
-  const int eb = total_elem_chunks_;
-  k_phase_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, d_mix_, nj, 1);
-  SH_LAUNCH_CHECK();
-  k_init32<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_, ws32_, vs32_);
-  SH_LAUNCH_CHECK();
-  for (int R = 0;; ++R) {
-    k_subsolve32<<<total_pairs_, 256, 2 * NS * LDS_ * sizeof(float), s>>>(d_jobs_, d_state_, d_pair_begin_, nj,
-                                                                         ws32_, us32_);
-    SH_LAUNCH_CHECK();
-    k_apply32<<<total_items_, 256, 3 * NS * LDF * sizeof(float), s>>>(d_jobs_, d_state_, d_item_begin_, nj,
-                                                                     ws32_, vs32_, us32_);
-    SH_LAUNCH_CHECK();
-    k_book<<<1, 256, 0, s>>>(d_jobs_, d_state_, mask, nj, d_count_, MAX_SWEEPS32);
-    SH_LAUNCH_CHECK();
-    if ((R & 7) == 7) {
-      SH_CUDA_CHECK(cudaMemcpyAsync(h_count_, d_count_, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      SH_CUDA_CHECK(timed_sync(s));
-      if (h_count_[0] == 0) break;
-    }
-    if (R > 256 * (MAX_SWEEPS32 + 1)) break;
-  }
-  prof_mark("fp32_rounds");
-  // FP64: V = (V_prev) V32, two Newton-Schulz steps, B = V^T A0 V
-  k_promote32<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, vs32_, ws_, ts_);
-  SH_LAUNCH_CHECK();
-  int rc;
-  if (any_warm && (rc = g_wv_.launch(s, d_warm_))) return rc;
-  if ((rc = g_s1_.launch(s, d_mix_))) return rc;
-  k_ns_poly<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
-  SH_LAUNCH_CHECK();
-  if ((rc = g_v1_.launch(s, d_mix_))) return rc;
-  if ((rc = g_s2_.launch(s, d_mix_))) return rc;
-  k_ns_poly<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
-  SH_LAUNCH_CHECK();
-  if ((rc = g_v2_.launch(s, d_mix_))) return rc;
-  k_copy_n<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ts_, vs_);
-  SH_LAUNCH_CHECK();
-  if ((rc = warm1_.launch(s, d_mix_))) return rc;
-  if ((rc = warm2_.launch(s, d_mix_))) return rc;
-  k_symmetrize<<<eb, 256, 0, s>>>(d_jobs_, d_mix_, d_elem_begin_, nj, ws_);
-  SH_LAUNCH_CHECK();
-  k_phase_reset<<<(nj + 127) / 128, 128, 0, s>>>(d_jobs_, d_state_, mask, nj, 0);
-  SH_LAUNCH_CHECK();
-  prof_mark("transition");
   return SHAMPOO_OK;
 }
 
@@ -2135,10 +1763,6 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
     if (rn) return rn;
     prof_mark("newton");
   }
-  if (solver == SHAMPOO_SOLVER_EIGH && mixed_ && has_big_) {
-    int rm = run_mixed_phase(s, any_warm);
-    if (rm) return rm;
-  }
   int rc = (solver == SHAMPOO_SOLVER_NEWTON) ? run_newton(eps, newton_tol, s, host_iters)
                                              : run_eigh(eta, eps, s, host_iters);
   if (rc) return rc;
@@ -2160,7 +1784,7 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   for (int j = 0; j < nj; ++j) {
     if (solver == SHAMPOO_SOLVER_EIGH) vec_valid_[j] = (hs[j].status == kEigOk && !hs[j].via_newton) ? 1 : 0;
     else vec_valid_[j] = 0;
-    sweeps_total_ += hs[j].sweep + hs[j].sweep32;
+    sweeps_total_ += hs[j].sweep;
   }
   if (prof.on)
     std::fprintf(stderr, "[eig] host: run %.2f ms, blocked in syncs %.2f ms, build_newton %.2f ms (jobs %d)\n",
@@ -2192,10 +1816,9 @@ int RootInverseBatch::run(double in_scale, const std::vector<int32_t>& has_prev,
   }
   if (host_iters) {
     host_iters->resize(nj);
-    // eigh: FP64 sweeps + 1000 x FP32-phase sweeps (mixed precision); Newton: iterations
-    // (jobs finished by the Newton pre-pass: 100000 + iterations)
+    // eigh: Jacobi sweeps; Newton: iterations (jobs finished by the Newton pre-pass: 100000 + iterations)
     for (int j = 0; j < nj; ++j)
-      (*host_iters)[j] = hs[j].via_newton ? 100000 + hs[j].sweep : hs[j].sweep + 1000 * hs[j].sweep32;
+      (*host_iters)[j] = hs[j].via_newton ? 100000 + hs[j].sweep : hs[j].sweep;
   }
   return SHAMPOO_OK;
 }

@@ -53,7 +53,6 @@ struct RootState {
   double tol_null;
   double trace;            // tr(A)
   int32_t nonfinite, capped;  // capped: sweep cap reached (result still used)
-  int32_t sweep32;            // FP32-phase sweeps (mixed-precision eigensolver)
   int32_t via_newton;         // eigh job solved by the coupled-Newton pre-pass (no eigenvectors kept)
 };
 
@@ -106,7 +105,6 @@ class RootInverseBatch {
   int newton_phase(double eps, double tol, int budget, const int32_t* cand, bool hybrid, cudaStream_t s);
   int prepare_warm(cudaStream_t s);
   int build_warm_gemms();
-  int run_mixed_phase(cudaStream_t s, bool any_warm);
   std::vector<RootJob> host_;
   RootJob* d_jobs_ = nullptr;
   RootState* d_state_ = nullptr;
@@ -121,14 +119,7 @@ class RootInverseBatch {
   std::vector<int32_t> vec_valid_;  // V holds eigenvectors of the last successful solve
   int64_t x_elems_ = 0, sweeps_total_ = 0;
   OzakiGemmBatch<double> rr_, warm1_, warm2_;  // big n^3 GEMMs on tcgen05 (Ozaki, FP64-class)
-  // mixed-precision eigensolver (FP32 Jacobi phase + FP64 Newton-Schulz re-orthonormalisation)
-  bool mixed_ = false;  // SHAMPOO_EIG_MIXED=1
   bool cross_only_ = true;  // SHAMPOO_EIG_CROSS=0: full inner sweeps in every outer round
-  float* ws32_ = nullptr;
-  float* vs32_ = nullptr;
-  float* us32_ = nullptr;
-  int32_t* d_mix_ = nullptr;
-  OzakiGemmBatch<double> g_wv_, g_s1_, g_v1_, g_s2_, g_v2_;
   int32_t* d_pair_begin_ = nullptr;
   int32_t* d_item_begin_ = nullptr;
   int32_t* d_elem_begin_ = nullptr;

@@ -42,7 +42,7 @@ class GuardStats:
     fallback_identity: int = 0
 
 
-def native_config(cfg: ShampooConfig) -> N.Config:
+def native_config(cfg: ShampooConfig, gather_f32: bool = False) -> N.Config:
     c = N.Config()
     c.lr = cfg.lr
     c.beta1, c.beta2 = float(cfg.betas[0]), float(cfg.betas[1])
@@ -64,6 +64,7 @@ def native_config(cfg: ShampooConfig) -> N.Config:
     c.solver = SOLVER_CODES[cfg.solver]
     c.newton_tolerance = cfg.newton_tolerance
     c.precision = 1 if cfg.precision == "single" else 0
+    c.gather_dtype = 1 if gather_f32 else 0  # SHAMPOO_GATHER_F32 / SHAMPOO_GATHER_STATE
     return c
 
 
@@ -115,7 +116,11 @@ class Shampoo:
         self.exchange = exchange
         self.check_finite = check_finite
         self._t = 0
-        self._ncfg = native_config(self.config)
+        # float32 parameters: directions travel (all-gather) and apply in float32 -- the update lands
+        # in float32 anyway; half the gather-buffer bytes
+        gather_f32 = bool(tensors) and all(t.dtype == torch.float32 for t in tensors)
+        self._ncfg = native_config(self.config, gather_f32)
+        self._state_f32 = self.config.precision == "single"
         h = C.c_void_p()
         with torch.cuda.device(device):
             N.check(N.lib().shampoo_ctx_create(self.plan.handle, C.byref(self._ncfg), rank,
@@ -239,7 +244,8 @@ class Shampoo:
         """Gather-layout gradient buffer (group_size * max_payload scalars, context dtype)."""
         if getattr(self, "_gbuf", None) is None:
             n = max(self.group_size * self.max_payload, 1)
-            self._gbuf = torch.zeros(n, dtype=torch.float32 if self._buf_f32 else torch.float64, device=self.device)
+            # gather LAYOUT, context (state) dtype: the reduced gradients feed the statistics
+            self._gbuf = torch.zeros(n, dtype=torch.float32 if self._state_f32 else torch.float64, device=self.device)
             self._gflag = torch.zeros(1, dtype=torch.int32, device=self.device)
         return self._gbuf
 
