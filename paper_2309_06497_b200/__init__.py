@@ -9,6 +9,7 @@ hand-written sm_100a kernels in ``libshampoo_b200.so`` (see include/shampoo_b200
 from .config import (BufferOverflowError, DivergedReplicasError, GraftKind, InvalidGroupSizeError,
                      LargeDimMethod, NativeError, NonFiniteGradientError, OutOfRangeError, ShampooConfig,
                      Solver, lr_at)
+from .checkpoint import CheckpointError, load_checkpoint, merge_state_trees, save_checkpoint
 from .planning import (AssignmentPlan, BlockPlan, BlockRegion, BlockSpec, CommReport, GlobalBlock, NativePlan,
                        block_partition, buffer_size, comm_meter, enumerate_blocks, greedy_assign, merge_dims,
                        plan_parameter, state_scalar_count)
@@ -28,7 +29,7 @@ def __getattr__(name):
 
 
 __all__ = [
-    "AssignmentPlan", "BlockPlan", "BlockRegion", "BlockSpec", "BufferOverflowError", "CommReport",
+    "AssignmentPlan", "BlockPlan", "CheckpointError", "load_checkpoint", "merge_state_trees", "save_checkpoint", "BlockRegion", "BlockSpec", "BufferOverflowError", "CommReport",
     "DistributedShampoo",
     "DivergedReplicasError", "GlobalBlock", "GraftKind", "GroupExchange", "GuardStats",
     "InvalidGroupSizeError", "LargeDimMethod", "NativeError", "NativePlan", "NonFiniteGradientError",

@@ -130,6 +130,14 @@ class GroupExchange:
             dist.all_gather_into_tensor(out, region, group=self.group)  # in place (NCCL)
         self.bytes_per_step = (self.group_size - 1) * max_payload * buf.element_size()
 
+    def gather_group_trees(self, tree: dict) -> list:
+        """Every rank's state tree of this rank's replica group (host objects), in group-rank order."""
+        out = [None] * self.group_size
+        if self.group_size == 1:
+            return [tree]
+        dist.all_gather_object(out, tree, group=self.group)
+        return out
+
     def check_replicas(self, params, tolerance: float = REPLICA_TOLERANCE) -> float:
         """dist.py:361-368: every rank's parameters must match to ``tolerance`` (max abs).  Exact
         elementwise check: all-reduce MAX and MIN of the flat float64 parameters over all ranks;
@@ -246,6 +254,26 @@ class DistributedShampoo(torch.optim.Optimizer):
         """``state_tree`` nesting (optim.py:387-423) plus the torch param-group metadata."""
         return {"state": self.engine.state_tree(), "param_groups": [
             {k: v for k, v in g.items() if k != "params"} for g in self.param_groups]}
+
+    def full_state_tree(self) -> dict:
+        """The union of the replica group's per-rank trees (train.py:346-353): every block once."""
+        from .checkpoint import merge_state_trees
+        tree = self.engine.state_tree()
+        if self.exchange is None:
+            return tree
+        return merge_state_trees(self.exchange.gather_group_trees(tree))
+
+    def save_checkpoint(self, path: str) -> None:
+        """Reference-format checkpoint of the whole optimizer (checkpoint.py:114-126): the sharded
+        state is merged across the replica group; rank 0 writes the file (collective call)."""
+        from .checkpoint import save_checkpoint
+        tree = self.full_state_tree()
+        if self.exchange is None or self.exchange.rank == 0:
+            save_checkpoint(path, self.engine.step_count, [p.detach().cpu().numpy() for p in self._plist], tree)
+
+    def load_checkpoint(self, path: str) -> None:
+        """Resume from a reference-format checkpoint (each rank loads its owned blocks)."""
+        self.engine.load_checkpoint(path)
 
     def load_state_dict(self, state_dict: dict) -> None:
         self.engine.load_state_tree(state_dict["state"])

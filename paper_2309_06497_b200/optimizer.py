@@ -408,6 +408,35 @@ class Shampoo:
         torch.cuda.synchronize(self.device)
 
 
+    # -- reference checkpoint files (checkpoint.py:114-144)
+
+    def save_checkpoint(self, path: str) -> None:
+        """Write this optimizer's parameters and state as a reference-format JSON checkpoint (one
+        file; a sharded optimizer writes only its owned blocks -- see DistributedShampoo for the
+        union)."""
+        from .checkpoint import save_checkpoint
+        tree = self.state_tree()
+        save_checkpoint(path, self._t, [p.detach().cpu().numpy() for p in self._params], tree)
+
+    def load_checkpoint(self, path: str) -> None:
+        """Resume from a reference-format checkpoint: parameters copied into this optimizer's tensors
+        (cast to their dtype), state loaded for the owned blocks."""
+        from .checkpoint import CheckpointError, load_checkpoint
+        step, params, tree = load_checkpoint(path)
+        if len(params) != len(self._params):
+            raise CheckpointError(f"checkpoint holds {len(params)} parameters, the optimizer {len(self._params)}")
+        for i, (dst, src) in enumerate(zip(self._params, params)):
+            if tuple(dst.shape) != tuple(src.shape):
+                raise CheckpointError(f"parameter {i}: checkpoint shape {src.shape}, optimizer {tuple(dst.shape)}")
+        if int(tree["t"]) != step:
+            raise CheckpointError(f"checkpoint step {step} and state step {tree['t']} differ")
+        self.load_state_tree(tree)
+        with torch.no_grad():
+            for dst, src in zip(self._params, params):
+                dst.copy_(torch.as_tensor(src, device=dst.device, dtype=dst.dtype))
+        torch.cuda.synchronize(self.device)
+
+
 def launch_count() -> int:
     """Kernel launches issued by libshampoo_b200 since load."""
     return int(N.lib().shampoo_launch_count())
