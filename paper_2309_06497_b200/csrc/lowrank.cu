@@ -333,6 +333,17 @@ int low_rank_root_inverse(const std::vector<LowRankJob>& jobs, double in_scale, 
   double *w = nullptr, *y0n = nullptr;
   LRDev* dj = nullptr;
   int32_t *dc = nullptr, *dx = nullptr, *fix = nullptr;
+  // every exit path: wait for the queued work on s, then hand the workspaces back to the heap
+  struct Release {
+    cudaStream_t s;
+    void* const* ptrs[6];
+    ~Release() {
+      cudaStreamSynchronize(s);
+      for (void* const* p : ptrs)
+        if (*p) dev_free(*p);
+    }
+  } release{s, {(void* const*)&w, (void* const*)&y0n, (void* const*)&dj, (void* const*)&dc, (void* const*)&dx,
+                (void* const*)&fix}};
   SH_CUDA_CHECK(dev_malloc(&w, ws * sizeof(double)));
   SH_CUDA_CHECK(dev_malloc(&y0n, n0s * sizeof(double)));
   SH_CUDA_CHECK(dev_malloc(&dj, nj * sizeof(LRDev)));
@@ -365,6 +376,14 @@ int low_rank_root_inverse(const std::vector<LowRankJob>& jobs, double in_scale, 
     // Y = Omega^T A (Omega^T in the T slot) ; T = Q A ; B = T Q^T ; Z = M Q ; X = Z^T Q (symmetric:
     // lower tiles + mirror)
     OzakiGemmBatch<double> gy, gt, gb, gz, gx;
+    const int nb = (rmax + LR_BS - 1) / LR_BS;
+    std::vector<std::unique_ptr<OzakiGemmBatch<double>>> ph(nb), pu(nb);
+    RootInverseBatch rb;
+    // destroyed first: the batches above release their workspaces only after s has drained
+    struct SyncOnExit {
+      cudaStream_t s;
+      ~SyncOnExit() { cudaStreamSynchronize(s); }
+    } drain{s};
     for (int j = 0; j < nj; ++j) {
       const LRDev& D = hj[j];
       const int r = D.r, d = D.d;
@@ -379,8 +398,6 @@ int low_rank_root_inverse(const std::vector<LowRankJob>& jobs, double in_scale, 
     // block CGS2: block b's rows minus their projection on the rows of blocks < b, twice
     // (H = Y_b Q_<b^T ; Y_b -= H Q_<b), then the in-block pass; jobs whose block needed a
     // unit-vector replacement repeat both once (masked by fix[j])
-    const int nb = (rmax + LR_BS - 1) / LR_BS;
-    std::vector<std::unique_ptr<OzakiGemmBatch<double>>> ph(nb), pu(nb);
     for (int b = 1; b < nb; ++b) {
       ph[b].reset(new OzakiGemmBatch<double>());
       pu[b].reset(new OzakiGemmBatch<double>());
@@ -442,7 +459,6 @@ int low_rank_root_inverse(const std::vector<LowRankJob>& jobs, double in_scale, 
     SH_LAUNCH_CHECK();
     // f(B) on the r x r compressions: B is the factor restricted to (a basis containing) its range,
     // full rank, so the Newton pre-pass applies (with its conditioning gate); Jacobi otherwise
-    RootInverseBatch rb;
     std::vector<int32_t> rn(nj), rp(nj), full(nj, 1);
     for (int j = 0; j < nj; ++j) {
       rn[j] = hj[j].r;
@@ -487,12 +503,6 @@ int low_rank_root_inverse(const std::vector<LowRankJob>& jobs, double in_scale, 
     else if (hj[j].has_prev) ++stats[2];
     else ++stats[3];
   }
-  dev_free(w);
-  dev_free(y0n);
-  dev_free(dj);
-  dev_free(dc);
-  dev_free(dx);
-  dev_free(fix);
   return rc;
 }
 
