@@ -12,7 +12,7 @@ from .config import (BufferOverflowError, DivergedReplicasError, GraftKind, Inva
 from .checkpoint import CheckpointError, load_checkpoint, merge_state_trees, save_checkpoint
 from .planning import (AssignmentPlan, BlockPlan, BlockRegion, BlockSpec, CommReport, GlobalBlock, NativePlan,
                        block_partition, buffer_size, comm_meter, enumerate_blocks, greedy_assign, merge_dims,
-                       plan_parameter, state_scalar_count)
+                       mlp_param_shapes, plan_parameter, plan_report, state_scalar_count)
 
 __version__ = "0.1.0"
 

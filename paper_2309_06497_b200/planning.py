@@ -17,7 +17,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass
 from itertools import product
-from typing import Sequence
+from typing import Optional, Sequence
 
 from . import _native as N
 from .config import LargeDimMethod, METHOD_CODES
@@ -278,3 +278,30 @@ def comm_meter(plan: AssignmentPlan, block_shapes: Sequence[Sequence[int]],
     return CommReport(steps=steps, bytes_gathered_per_step=per_group, world_bytes_per_step=world,
                       total_bytes_gathered=world * steps, per_worker_state_scalars=state,
                       per_worker_state_bytes=tuple(x * SCALAR_BYTES for x in state))
+
+
+def plan_report(param_shapes: Sequence[Sequence[int]], config, world_size: int = 1,
+                group_size: Optional[int] = None, steps: int = 100) -> dict:
+    """The JSON document of the reference's ``minishampoo plan`` command (cli.py:168-218):
+    the assignment plan, its communication report and per-parameter state accounting for every
+    large-dimension method.  ``param_shapes`` in the reference trainer's (d_out, d_in) layout
+    for MLP widths (cli.py:172); ``group_size`` None = the whole world (num_trainers_per_group -1)."""
+    group = world_size if group_size is None else int(group_size)
+    blocks = enumerate_blocks(param_shapes, config)
+    plan = greedy_assign([b.var_count for b in blocks], world_size, group)
+    report = comm_meter(plan, [b.shape for b in blocks], method=config.large_dim_method, steps=steps)
+    per_parameter = []
+    for shape in param_shapes:
+        methods = {}
+        for method in LargeDimMethod:
+            pp = plan_parameter(shape, config.max_preconditioner_dim, method)
+            methods[method.value] = sum(state_scalar_count(spec.shape, method) for spec in pp.blocks)
+        pp = plan_parameter(shape, config.max_preconditioner_dim, config.large_dim_method)
+        per_parameter.append({"shape": list(shape), "merged_shape": list(pp.merged_shape),
+                              "num_blocks": len(pp.blocks), "state_scalars_by_method": methods})
+    return {"plan": plan.to_json_dict(), "comm": report.to_json_dict(), "per_parameter": per_parameter}
+
+
+def mlp_param_shapes(widths: Sequence[int]) -> list[tuple[int, int]]:
+    """Weight shapes of the reference trainer's MLP: (d_out, d_in) per layer (cli.py:172, train.py:93)."""
+    return [(d_out, d_in) for d_in, d_out in zip(widths, widths[1:])]

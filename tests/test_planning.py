@@ -9,6 +9,7 @@ reference (tests/golden/plans.npz).
 from __future__ import annotations
 
 import math
+import os
 import re
 
 import numpy as np
@@ -224,3 +225,25 @@ class TestCommMeter:
         assert report.bytes_gathered_per_step == 204_472_320
         assert report.total_bytes_gathered == 50 * 204_472_320
         assert sum(report.per_worker_state_scalars) == 2 * 128_111_874
+
+
+def _plan_case(flags):
+    """The reference CLI's flags (RunConfig defaults: input 32, hidden 64, 10 classes) -> inputs."""
+    kv = dict(zip(flags[::2], flags[1::2]))
+    widths = [32, *[int(w) for w in kv.get("--hidden-widths", "64").split(",")], 10]
+    world = int(kv.get("--world-size", 1))
+    group = int(kv.get("--num-trainers-per-group", -1))
+    cfg = P.ShampooConfig(max_preconditioner_dim=int(kv["--max-preconditioner-dim"]),
+                          large_dim_method=P.LargeDimMethod(kv.get("--large-dim-method", "blocking")))
+    return P.mlp_param_shapes(widths), cfg, world, (world if group < 0 else group), int(kv.get("--steps", 100))
+
+
+def test_plan_report_matches_reference_cli():
+    """plan_report == the JSON `minishampoo plan` printed (cli.py:168-218), key for key."""
+    import json
+    cases = json.load(open(os.path.join(ROOT, "tests", "golden", "plan_reports.json")))
+    assert len(cases) == 5
+    for case in cases:
+        shapes, cfg, world, group, steps = _plan_case(case["flags"])
+        got = json.loads(json.dumps(P.plan_report(shapes, cfg, world, group, steps), sort_keys=True))
+        assert got == case["report"], case["flags"]
