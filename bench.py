@@ -289,7 +289,8 @@ def run_ours(args):
     cfg = P.ShampooConfig(grafting=P.GraftKind(wl["grafting"]), precision=args.precision,
                           max_preconditioner_dim=wl["max_preconditioner_dim"], **COMMON)
     exchange = GroupExchange(world) if world > 1 else None
-    opt = P.Shampoo(params, cfg, world_size=world, group_size=world, rank=rank, exchange=exchange)
+    opt = P.Shampoo(params, cfg, world_size=world, group_size=world, rank=rank, exchange=exchange,
+                    check_finite="deferred" if args.check_finite == "deferred" else True)
     lib = N.lib()
     stream = torch.cuda.current_stream(dev)
     pdt = N.DTYPE_F32
@@ -465,22 +466,26 @@ def run_ours(args):
                 "sum_n3_G": round(n3.value / 1e9, 2)}
 
     # ---- 3) e2e through the public API with host buffers, starting at the next refresh: every step's
-    # gradients H2D from pinned host memory and every step's parameters D2H, double-buffered (H2D of
-    # step k+1 and D2H of step k overlap step k+1's compute); all copies complete inside the window
+    # gradients H2D from pinned host memory and every step's parameters D2H.  Pipelined like a data
+    # loader: NB gradient buffers (the H2D of step k may start once step k - NB finished reading its
+    # buffer) and two parameter snapshots (the D2H of step k overlaps steps k+1, k+2); all copies
+    # complete inside the window
     e2e = None
     if not args.skip_e2e:
         to_refresh()
         del grads
         host_grads = [torch.cat([x.reshape(-1) for x in fresh()]).cpu().pin_memory() for _ in range(args.steps)]
         host_params = torch.empty(n_params, dtype=torch.float32).pin_memory()
-        dev_flat = [torch.empty(n_params, dtype=torch.float32, device=dev) for _ in range(2)]
+        NB = 3
+        dev_flat = [torch.empty(n_params, dtype=torch.float32, device=dev) for _ in range(NB)]
         dev_grads = [[v.view(s_) for v, s_ in zip(torch.split(fl, numels), shapes)] for fl in dev_flat]
-        snap_flat = torch.empty(n_params, dtype=torch.float32, device=dev)
-        snap = [v.view(s_) for v, s_ in zip(torch.split(snap_flat, numels), shapes)]
+        snap_flat = [torch.empty(n_params, dtype=torch.float32, device=dev) for _ in range(2)]
+        snap = [[v.view(s_) for v, s_ in zip(torch.split(fl, numels), shapes)] for fl in snap_flat]
         h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_used = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_snap, ev_out = torch.cuda.Event(), torch.cuda.Event()
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_used = [torch.cuda.Event() for _ in range(NB)]
+        ev_snap = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         erefr = []
         if world > 1:
@@ -488,33 +493,35 @@ def run_ours(args):
         torch.cuda.synchronize()
         ev[0].record(stream)
 
-        def upload(k, b):
+        def upload(k):
+            b = k % NB
             with torch.cuda.stream(h2d):
                 h2d.wait_event(ev[0])
-                if k >= 2:
-                    h2d.wait_event(ev_used[b])  # step k-2 finished reading this buffer
+                if k >= NB:
+                    h2d.wait_event(ev_used[b])  # step k - NB finished reading this buffer
                 dev_flat[b].copy_(host_grads[k], non_blocking=True)
                 ev_in[b].record(h2d)
 
-        upload(0, 0)
+        for k in range(min(NB - 1, args.steps)):
+            upload(k)
         for k in range(args.steps):
-            b = k % 2
-            if k + 1 < args.steps:
-                upload(k + 1, 1 - b)
+            b, q = k % NB, k % 2
+            if k + NB - 1 < args.steps:
+                upload(k + NB - 1)
             erefr.append(is_refresh(opt.step_count))
             stream.wait_event(ev_in[b])
             opt.step(dev_grads[b])
             ev_used[b].record(stream)
-            if k > 0:
-                stream.wait_event(ev_out)  # the previous read-back finished with the snapshot
-            torch._foreach_copy_(snap, list(opt.params()))  # device snapshot (D2D), read back below
-            ev_snap.record(stream)
+            if k >= 2:
+                stream.wait_event(ev_out[q])  # the read-back of step k-2 finished with this snapshot
+            torch._foreach_copy_(snap[q], list(opt.params()))  # device snapshot (D2D), read back below
+            ev_snap[q].record(stream)
             with torch.cuda.stream(d2h):
-                d2h.wait_event(ev_snap)
-                host_params.copy_(snap_flat, non_blocking=True)
-                ev_out.record(d2h)
+                d2h.wait_event(ev_snap[q])
+                host_params.copy_(snap_flat[q], non_blocking=True)
+                ev_out[q].record(d2h)
             if k + 1 == args.steps:
-                stream.wait_event(ev_out)
+                stream.wait_event(ev_out[q])
             ev[k + 1].record(stream)
         torch.cuda.synchronize()
         eper = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
@@ -601,7 +608,7 @@ def run_ours(args):
                            "max_preconditioner_dim": wl["max_preconditioner_dim"], "precondition_frequency": f,
                            "grafting": wl["grafting"], "momentum": "nesterov 0.9", "precision": args.precision,
                            "epsilon": 1e-12, "parallelism": f"dp{world} (block-sharded, all-gather)",
-                           "steady_state_from_step": T0, "fast_forward_s": round(ff_s, 1),
+                           "steady_state_from_step": T0, "check_finite": args.check_finite, "fast_forward_s": round(ff_s, 1),
                            "amortisation": "value = ((f-1) * mean(plain steps) + mean(refresh steps)) / f over the "
                                            "timed window, which starts at a steady-state refresh step",
                            "l2": "state (factors+inverses ~2 GB) >> 126 MB L2; no flush needed",
@@ -700,6 +707,9 @@ def main():
     ap.add_argument("--steady-step", type=int, default=-1,
                     help="first timed step (a refresh); -1: ceil(1.25 b / f) f (2600 for ResNet-50); 0: right "
                          "after the warm-up")
+    ap.add_argument("--check-finite", choices=["deferred", "strict"], default="deferred",
+                    help="non-finite gradient guard: device-predicated, raised one call late (no host sync), "
+                         "or the reference's eager raise (one host sync per step)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-adam", action="store_true")

@@ -172,6 +172,18 @@ SHAMPOO_API int64_t shampoo_ctx_device_bytes(const shampoo_ctx* ctx);
  * entry is NaN/Inf.  grads: host array of nparams device pointers. */
 SHAMPOO_API int shampoo_check_finite(shampoo_ctx* ctx, const void* const* grads, int32_t dtype, void* stream);
 
+/* The same guard without the host synchronisation (optim.py:362-366 semantics, raised one call
+ * late): the check writes a device go word that predicates every state-writing kernel of step t
+ * (graft accumulators, filter, factor statistics, momentum, gather-buffer directions, parameter
+ * update), so a non-finite step leaves the device state untouched.  A refresh step (t >= start,
+ * t % frequency == 0) is checked eagerly instead (*deferred = 0, identical to
+ * shampoo_check_finite).  With *deferred = 1 the caller must call shampoo_check_finite_resolve
+ * before the next check; it returns SHAMPOO_ERR_NONFINITE_GRAD (and *aborted = 1) if step t was
+ * skipped, having restored the context's host-side step counters. */
+SHAMPOO_API int shampoo_check_finite_deferred(shampoo_ctx* ctx, const void* const* grads, int32_t dtype,
+                                              int64_t t, int32_t* deferred, void* stream);
+SHAMPOO_API int shampoo_check_finite_resolve(shampoo_ctx* ctx, int32_t* aborted);
+
 /* Step t phase 1: gather owned gradient blocks (+ L2 weight decay), graft
  * accumulator update, Kronecker factor statistics (EMA or sum). */
 SHAMPOO_API int shampoo_stats_update(shampoo_ctx* ctx, const void* const* grads, const void* const* params,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "shampoo_ctx_destroy": (None, [_P]),
     "shampoo_ctx_device_bytes": (_I64, [_P]),
     "shampoo_check_finite": (C.c_int, [_P, C.POINTER(_P), _I32, _P]),
+    "shampoo_check_finite_deferred": (C.c_int, [_P, C.POINTER(_P), _I32, C.c_int64, C.POINTER(_I32), _P]),
+    "shampoo_check_finite_resolve": (C.c_int, [_P, C.POINTER(_I32)]),
     "shampoo_stats_update": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I32, _I64, _P]),
     "shampoo_root_inverse": (C.c_int, [_P, _I64, _PI32, _P]),
     "shampoo_pack_gradients": (C.c_int, [_P, C.POINTER(_P), _I32, _P, _P]),

@@ -150,7 +150,25 @@ struct shampoo_ctx {
   int n_owned_chunks = 0, n_all_chunks = 0, n_param_chunks = 0;
   void** d_ptrs = nullptr;  // [grads | params]
   int32_t* d_flag = nullptr;
-  int32_t* h_flag = nullptr;
+  int32_t* h_flag = nullptr;        // host-mapped pinned (written by k_publish_flag)
+  int32_t* h_flag_dev = nullptr;    // its device alias
+  // pointer-table uploads: host mirror of d_ptrs (uploads only on change) and a ring of host-mapped
+  // staging slots read by k_copy_ptrs (a slot is reused once its copy kernel has run)
+  std::vector<const void*> ptr_mirror;
+  static constexpr int kPtrRing = 16;
+  void** h_ptr_ring = nullptr;
+  void** h_ptr_ring_dev = nullptr;
+  cudaEvent_t ptr_ev[kPtrRing] = {};
+  bool ptr_ev_used[kPtrRing] = {};
+  int ptr_slot = 0;
+  // deferred non-finite check (shampoo_check_finite_deferred): the step's state-writing kernels are
+  // predicated on the device word d_go (= 1 - non-finite); the host reads the flag one call later
+  int32_t* d_go = nullptr;
+  bool go_armed = false;            // the step in flight is predicated on d_go
+  bool deferred_pending = false;    // a deferred check awaits shampoo_check_finite_resolve
+  cudaEvent_t ev_check = nullptr;   // after the deferred check's flag read-back
+  int64_t saved_graft_step = 0;     // host counters before the predicated step (restored if it aborted)
+  std::vector<int64_t> saved_step;
   std::unique_ptr<EngineBase> engine;
   // root-inverse jobs in kRootGroups load-balanced groups solved concurrently on their own streams
   // (host thread per group): one group's latency-bound sub-solves overlap another's DMMA rounds
@@ -179,6 +197,9 @@ struct shampoo_ctx {
     cudaFree(d_diag_blocks);
     cudaFree(d_ptrs);
     cudaFreeHost(h_flag);
+    cudaFreeHost(h_ptr_ring);
+    for (auto& e : ptr_ev)
+      if (e) cudaEventDestroy(e);
     for (int g = 1; g < kRootGroups; ++g) {
       if (side[g]) cudaStreamDestroy(side[g]);
       if (ev_join[g]) cudaEventDestroy(ev_join[g]);
@@ -188,6 +209,7 @@ struct shampoo_ctx {
     if (ev_lr) cudaEventDestroy(ev_lr);
     if (lr_stream) cudaStreamDestroy(lr_stream);
     if (ev_stats) cudaEventDestroy(ev_stats);
+    if (ev_check) cudaEventDestroy(ev_check);
   }
   template <typename T>
   Engine<T>& eng() { return *static_cast<Engine<T>*>(engine.get()); }
@@ -196,13 +218,30 @@ struct shampoo_ctx {
 namespace {
 
 int upload_ptrs(shampoo_ctx* c, const void* const* grads, const void* const* params, cudaStream_t s) {
-  std::vector<const void*> h(2 * c->nparams, nullptr);
+  // d_ptrs = [grads | params]; a null half keeps its previous entries.  Uploaded only when the
+  // table changed (a training loop passes the same p.grad / parameter tensors every step), through
+  // a host-mapped staging slot and a one-CTA copy kernel: no copy-engine transfer in the step
+  bool changed = false;
   for (int i = 0; i < c->nparams; ++i) {
-    if (grads) h[i] = grads[i];
-    if (params) h[c->nparams + i] = params[i];
+    if (grads && c->ptr_mirror[i] != grads[i]) {
+      c->ptr_mirror[i] = grads[i];
+      changed = true;
+    }
+    if (params && c->ptr_mirror[c->nparams + i] != params[i]) {
+      c->ptr_mirror[c->nparams + i] = params[i];
+      changed = true;
+    }
   }
-  // pageable source: staged by the driver before return, so the host vector may die
-  SH_CUDA_CHECK(cudaMemcpyAsync(c->d_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+  if (!changed) return SHAMPOO_OK;
+  const int slot = c->ptr_slot;
+  c->ptr_slot = (c->ptr_slot + 1) % shampoo_ctx::kPtrRing;
+  if (c->ptr_ev_used[slot]) SH_CUDA_CHECK(cudaEventSynchronize(c->ptr_ev[slot]));  // its last copy has run
+  const size_t n = 2 * (size_t)c->nparams;
+  std::memcpy(c->h_ptr_ring + slot * n, c->ptr_mirror.data(), n * sizeof(void*));
+  int rc = launch_copy_ptrs(c->h_ptr_ring_dev + slot * n, c->d_ptrs, (int)n, s);
+  if (rc) return rc;
+  SH_CUDA_CHECK(cudaEventRecord(c->ptr_ev[slot], s));
+  c->ptr_ev_used[slot] = true;
   return SHAMPOO_OK;
 }
 
@@ -265,6 +304,7 @@ ElemArenas arenas(shampoo_ctx* c) {
   a.pg2 = c->pg2;
   a.ps2 = c->ps2;
   a.ready = c->d_ready;
+  a.go = c->go_armed ? c->d_go : nullptr;
   return a;
 }
 
@@ -311,6 +351,8 @@ int build_engine(shampoo_ctx* c) {
       for (int q = m + 1; q < order; ++q) inner *= d[q];
       {
         GemmProblem g = make_mode_gram(G + c->vofs[l], outer, d[m], inner, FACT + off, alpha, beta);
+        g.flags |= kGemmMasked;  // predicated on the step's go word (deferred non-finite check)
+        g.mask_index = 0;
         if (thin(g)) e->stats_thin.add(g);
         else e->stats.add(g);
       }
@@ -525,6 +567,7 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
       {(void**)&c->d_cb, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_cc, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_flag, 16},
+      {(void**)&c->d_go, 16},
       {&c->FB, (size_t)c->n_fb * es},
       {(void**)&c->dsum, (size_t)c->n_fb * 8},
       {(void**)&c->dscale, (size_t)c->n_fb * 8},
@@ -555,7 +598,13 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     SH_CUDA_CHECK(cudaMemcpy(c->d_fb_chunks, fc.data(), fc.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
   if (!dblk.empty())
     SH_CUDA_CHECK(cudaMemcpy(c->d_diag_blocks, dblk.data(), dblk.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  SH_CUDA_CHECK(cudaMallocHost(&c->h_flag, 16));
+  SH_CUDA_CHECK(cudaHostAlloc(&c->h_flag, 16, cudaHostAllocMapped));
+  SH_CUDA_CHECK(cudaHostGetDevicePointer((void**)&c->h_flag_dev, c->h_flag, 0));
+  SH_CUDA_CHECK(cudaHostAlloc(&c->h_ptr_ring, (size_t)shampoo_ctx::kPtrRing * 2 * std::max(c->nparams, 1) * sizeof(void*),
+                              cudaHostAllocMapped));
+  SH_CUDA_CHECK(cudaHostGetDevicePointer((void**)&c->h_ptr_ring_dev, c->h_ptr_ring, 0));
+  for (auto& e : c->ptr_ev) SH_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->ptr_mirror.assign(2 * (size_t)c->nparams, nullptr);
   SH_CUDA_CHECK(cudaMemcpy(c->d_blocks, db.data(), nb * sizeof(DevBlock), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(c->d_params, dp.data(), c->nparams * sizeof(DevBlock), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(c->d_owned_chunks, oc.data(), oc.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
@@ -610,6 +659,7 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_lr, cudaEventDisableTiming));
   SH_CUDA_CHECK(cudaStreamCreateWithFlags(&c->lr_stream, cudaStreamNonBlocking));
   SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
+  SH_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_check, cudaEventDisableTiming));
   {
     const char* lr = std::getenv("SHAMPOO_EIG_LOWRANK");
     c->low_rank = lr ? std::atoi(lr) != 0 : true;
@@ -636,15 +686,67 @@ int shampoo_check_finite(shampoo_ctx* c, const void* const* grads, int32_t dtype
   if (rc) return rc;
   SH_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), s));
   if ((rc = launch_finite<double>(c->d_param_chunks, c->n_param_chunks, c->d_params,
-                                  (const void* const*)c->d_ptrs, dtype, c->d_flag, s)))
+                                  (const void* const*)c->d_ptrs, dtype, c->d_flag, nullptr, s)))
     return rc;
-  SH_CUDA_CHECK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if ((rc = launch_publish_flag(c->d_flag, c->h_flag_dev, s))) return rc;
   SH_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (c->h_flag[0]) {
+  if (*(volatile int32_t*)c->h_flag) {
     set_error("gradient contains non-finite entries; step aborted");
     return SHAMPOO_ERR_NONFINITE_GRAD;
   }
   return SHAMPOO_OK;
+}
+
+namespace {
+bool refresh_step(const shampoo_ctx* c, int64_t t) {
+  const shampoo_config& k = c->cfg;
+  if ((double)t < k.start_preconditioning_step || t % k.precondition_frequency != 0) return false;
+  for (const auto& r : c->rinv)
+    if (r.jobs()) return true;
+  return false;
+}
+}  // namespace
+
+int shampoo_check_finite_deferred(shampoo_ctx* c, const void* const* grads, int32_t dtype, int64_t t,
+                                  int32_t* deferred, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (deferred) *deferred = 0;
+  if (c->deferred_pending) {
+    set_error("check_finite_deferred: the previous deferred check was not resolved");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  // a refresh step's root inverse rewrites the inverses from host-side decisions: checked eagerly
+  if (refresh_step(c, t)) return shampoo_check_finite(c, grads, dtype, stream);
+  int rc = upload_ptrs(c, grads, nullptr, s);
+  if (rc) return rc;
+  static const int32_t kOne = 1;
+  SH_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0, sizeof(int32_t), s));
+  SH_CUDA_CHECK(cudaMemcpyAsync(c->d_go, &kOne, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if ((rc = launch_finite<double>(c->d_param_chunks, c->n_param_chunks, c->d_params,
+                                  (const void* const*)c->d_ptrs, dtype, c->d_flag, c->d_go, s)))
+    return rc;
+  if ((rc = launch_publish_flag(c->d_flag, c->h_flag_dev, s))) return rc;
+  SH_CUDA_CHECK(cudaEventRecord(c->ev_check, s));
+  c->saved_graft_step = c->graft_step;
+  c->saved_step = c->step;
+  c->go_armed = true;
+  c->deferred_pending = true;
+  if (deferred) *deferred = 1;
+  return SHAMPOO_OK;
+}
+
+int shampoo_check_finite_resolve(shampoo_ctx* c, int32_t* aborted) {
+  if (aborted) *aborted = 0;
+  if (!c->deferred_pending) return SHAMPOO_OK;
+  c->deferred_pending = false;
+  SH_CUDA_CHECK(cudaEventSynchronize(c->ev_check));
+  if (!*(volatile int32_t*)c->h_flag) return SHAMPOO_OK;
+  // the predicated step wrote no device state; undo its host-side counters
+  c->graft_step = c->saved_graft_step;
+  c->step = c->saved_step;
+  if (aborted) *aborted = 1;
+  set_error("gradient contains non-finite entries; step aborted (deferred check)");
+  return SHAMPOO_ERR_NONFINITE_GRAD;
 }
 
 namespace {
@@ -696,9 +798,11 @@ int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf
     SH_CUDA_CHECK(cudaStreamWaitEvent(c->side[1], c->ev_prep, 0));
     ss = c->side[1];
   }
-  rc = c->f32 ? c->eng<float>().stats.launch(ss) : c->eng<double>().stats.launch(ss);
+  // statistics problems are masked on word 0 of the go pointer (deferred check; null: unconditional)
+  const int32_t* go = c->go_armed ? c->d_go : nullptr;
+  rc = c->f32 ? c->eng<float>().stats.launch(ss, go) : c->eng<double>().stats.launch(ss, go);
   if (rc) return rc;
-  rc = c->f32 ? c->eng<float>().stats_thin.launch(ss) : c->eng<double>().stats_thin.launch(ss);
+  rc = c->f32 ? c->eng<float>().stats_thin.launch(ss, go) : c->eng<double>().stats_thin.launch(ss, go);
   if (rc) return rc;
   if (concurrent) {
     SH_CUDA_CHECK(cudaEventRecord(c->ev_stats, ss));
@@ -903,9 +1007,11 @@ int shampoo_apply(shampoo_ctx* c, void* const* params, int32_t dtype, double lr,
   void* const* pp = (void* const*)(c->d_ptrs + c->nparams);
   {
     PhaseScope scope(&c->timer, 4, s);
-    rc = c->f32 ? launch_apply<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s)
-                : launch_apply<double>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, s);
+    const int32_t* go = c->go_armed ? c->d_go : nullptr;
+    rc = c->f32 ? launch_apply<float>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, go, s)
+                : launch_apply<double>(c->d_all_chunks, c->n_all_chunks, c->d_blocks, pp, c->BUF, sc, go, s);
   }
+  c->go_armed = false;  // the predicated step ends here
   if (rc) return rc;
   return join_stats(c, s);  // the step ends with everything it launched ordered before the caller's stream
 }

@@ -30,7 +30,7 @@ __device__ __forceinline__ bool graft_normalized(int32_t g) {
 __global__ void __launch_bounds__(NT) k_finite(const Chunk* __restrict__ chunks,
                                                const DevBlock* __restrict__ params,
                                                const void* const* __restrict__ grads, int32_t dtype,
-                                               int32_t* flag) {
+                                               int32_t* flag, int32_t* go) {
   const Chunk c = chunks[blockIdx.x];
   const void* g = grads[params[c.block].param];
   int bad = 0;
@@ -38,8 +38,15 @@ __global__ void __launch_bounds__(NT) k_finite(const Chunk* __restrict__ chunks,
     const double v = load_as<double>(g, c.start + e, dtype);
     if (!isfinite(v)) bad = 1;
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    atomicOr(flag, 1);
+    if (go) *go = 0;  // deferred check: the step's state-writing kernels skip themselves
+  }
 }
+
+// Step predication (deferred non-finite check): the state-writing kernels of a step return at once
+// when the step's go word is 0; null = unconditional.
+__device__ __forceinline__ bool skip_step(const int32_t* go) { return go != nullptr && *go == 0; }
 
 template <typename T>
 __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restrict__ chunks,
@@ -48,6 +55,7 @@ __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restric
                                                 const void* const* __restrict__ params, StepScalars sc,
                                                 ElemArenas ar) {
   __shared__ double red[32];
+  if (skip_step(ar.go)) return;
   const Chunk c = chunks[blockIdx.x];
   const DevBlock& B = blocks[c.block];
   T* G = static_cast<T*>(ar.G) + B.vofs;
@@ -154,6 +162,7 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
                                               const DevBlock* __restrict__ blocks,
                                               const void* const* __restrict__ params, StepScalars sc,
                                               ElemArenas ar) {
+  if (skip_step(ar.go)) return;
   const Chunk c = chunks[blockIdx.x];
   const DevBlock& B = blocks[c.block];
   const T* G = static_cast<const T*>(sc.use_filter ? ar.GE : ar.G) + B.vofs;
@@ -210,7 +219,9 @@ template <typename BT>
 __global__ void __launch_bounds__(NT) k_apply(const Chunk* __restrict__ chunks,
                                               const DevBlock* __restrict__ blocks,
                                               void* const* __restrict__ params,
-                                              const BT* __restrict__ buf, double lr, int32_t pdtype) {
+                                              const BT* __restrict__ buf, double lr, int32_t pdtype,
+                                              const int32_t* __restrict__ go) {
+  if (skip_step(go)) return;
   const Chunk c = chunks[blockIdx.x];
   const DevBlock& B = blocks[c.block];
   const BT* p = buf + B.gofs;
@@ -241,6 +252,7 @@ template <typename T>
 __global__ void __launch_bounds__(NT) k_fb_update(const Chunk* __restrict__ chunks,
                                                   const DevBlock* __restrict__ blocks, ElemArenas ar,
                                                   FallbackArgs fa) {
+  if (skip_step(ar.go)) return;
   const Chunk c = chunks[blockIdx.x];
   const DevBlock& B = blocks[c.block];
   const T* G = static_cast<const T*>(ar.G) + B.vofs;
@@ -264,7 +276,9 @@ __global__ void __launch_bounds__(NT) k_fb_update(const Chunk* __restrict__ chun
 // DIAGONAL: diag = EMA(diag, dsum) ; dsum = 0 (one CTA per diagonal block)
 template <typename T>
 __global__ void __launch_bounds__(NT) k_fb_diag_ema(const DevBlock* __restrict__ blocks,
-                                                    const int32_t* __restrict__ dblocks, FallbackArgs fa) {
+                                                    const int32_t* __restrict__ dblocks, FallbackArgs fa,
+                                                    const int32_t* __restrict__ go) {
+  if (skip_step(go)) return;
   const DevBlock& B = blocks[dblocks[blockIdx.x]];
   int64_t n = 0;
   for (int k = 0; k < B.order; ++k) n += B.dims[k];
@@ -327,7 +341,7 @@ int launch_fallback_update(const Chunk* chunks, int nchunks, const DevBlock* blo
     SH_LAUNCH_CHECK();
   }
   if (ndiag) {
-    k_fb_diag_ema<T><<<ndiag, NT, 0, s>>>(blocks, dblocks, fa);
+    k_fb_diag_ema<T><<<ndiag, NT, 0, s>>>(blocks, dblocks, fa, ar.go);
     SH_LAUNCH_CHECK();
   }
   return SHAMPOO_OK;
@@ -350,9 +364,9 @@ int launch_fallback_precondition(const Chunk* chunks, int nchunks, const DevBloc
 
 template <typename T>
 int launch_finite(const Chunk* chunks, int nchunks, const DevBlock* params, const void* const* grads,
-                  int32_t dtype, int32_t* flag, cudaStream_t s) {
+                  int32_t dtype, int32_t* flag, int32_t* go, cudaStream_t s) {
   if (!nchunks) return SHAMPOO_OK;
-  k_finite<<<nchunks, NT, 0, s>>>(chunks, params, grads, dtype, flag);
+  k_finite<<<nchunks, NT, 0, s>>>(chunks, params, grads, dtype, flag, go);
   SH_LAUNCH_CHECK();
   return SHAMPOO_OK;
 }
@@ -396,11 +410,11 @@ int launch_final(const Chunk* chunks, int nchunks, const DevBlock* blocks, const
 
 template <typename T>
 int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
-                 const void* buf, const StepScalars& sc, cudaStream_t s) {
+                 const void* buf, const StepScalars& sc, const int32_t* go, cudaStream_t s) {
   if (!nchunks) return SHAMPOO_OK;
   if (sc.buf_f32) k_apply<float><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const float*>(buf), sc.lr,
-                                                        sc.pdtype);
-  else k_apply<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const T*>(buf), sc.lr, sc.pdtype);
+                                                        sc.pdtype, go);
+  else k_apply<T><<<nchunks, NT, 0, s>>>(chunks, blocks, params, static_cast<const T*>(buf), sc.lr, sc.pdtype, go);
   SH_LAUNCH_CHECK();
   return SHAMPOO_OK;
 }
@@ -451,9 +465,34 @@ int launch_region_finite(const Chunk* chunks, int nchunks, const DevBlock* block
   return SHAMPOO_OK;
 }
 
+// Small host<->device transfers of the step without the copy engines (a 4-byte cudaMemcpyAsync D2H
+// queues behind any bulk D2H the caller has in flight on another stream -- e.g. a parameter
+// read-back -- and stalls the step): the device writes host-mapped pinned memory / reads it.
+__global__ void k_publish_flag(const int32_t* __restrict__ src, volatile int32_t* dst) {
+  *dst = *src;
+  __threadfence_system();
+}
+
+__global__ void __launch_bounds__(256) k_copy_ptrs(const volatile uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                   int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+int launch_publish_flag(const int32_t* src, int32_t* mapped_dst, cudaStream_t s) {
+  k_publish_flag<<<1, 1, 0, s>>>(src, mapped_dst);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
+int launch_copy_ptrs(const void* mapped_src, void* dst, int n, cudaStream_t s) {
+  k_copy_ptrs<<<1, 256, 0, s>>>(static_cast<const volatile uint64_t*>(mapped_src), static_cast<uint64_t*>(dst), n);
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+
 #define SH_INST(T)                                                                                   \
   template int launch_finite<T>(const Chunk*, int, const DevBlock*, const void* const*, int32_t,    \
-                                int32_t*, cudaStream_t);                                             \
+                                int32_t*, int32_t*, cudaStream_t);                                             \
   template int launch_prepare<T>(int, const Chunk*, int, const DevBlock*, const void* const*,       \
                                  const void* const*, const StepScalars&, const ElemArenas&,         \
                                  cudaStream_t);                                                      \
@@ -461,7 +500,7 @@ int launch_region_finite(const Chunk* chunks, int nchunks, const DevBlock* block
   template int launch_final<T>(const Chunk*, int, const DevBlock*, const void* const*,              \
                                const StepScalars&, const ElemArenas&, cudaStream_t);                 \
   template int launch_apply<T>(const Chunk*, int, const DevBlock*, void* const*, const void*,        \
-                               const StepScalars&, cudaStream_t);                                    \
+                               const StepScalars&, const int32_t*, cudaStream_t);                                    \
   template int launch_fallback_update<T>(const Chunk*, int, const DevBlock*, const ElemArenas&,      \
                                          const FallbackArgs&, const int32_t*, int, cudaStream_t);    \
   template int launch_fallback_precondition<T>(const Chunk*, int, const DevBlock*, const ElemArenas&, \

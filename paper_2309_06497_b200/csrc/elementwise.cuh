@@ -40,11 +40,12 @@ struct ElemArenas {
   double* ps2;    // per owned block ||P_shampoo||^2
   const int32_t* ready;  // per owned block: inverse present
   const void* GBUF;       // reduced gradient buffer (gather-buffer layout, context dtype) or null
+  const int32_t* go;      // deferred non-finite check: 0 = skip the step's state writes; null = run
 };
 
 template <typename T>
 int launch_finite(const Chunk* chunks, int nchunks, const DevBlock* params, const void* const* grads,
-                  int32_t dtype, int32_t* flag, cudaStream_t s);
+                  int32_t dtype, int32_t* flag, int32_t* go, cudaStream_t s);
 template <typename T>
 int launch_prepare(int pass, const Chunk* chunks, int nchunks, const DevBlock* blocks,
                    const void* const* grads, const void* const* params, const StepScalars& sc,
@@ -75,10 +76,13 @@ int launch_fallback_precondition(const Chunk* chunks, int nchunks, const DevBloc
                                  cudaStream_t s);
 template <typename T>
 int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void* const* params,
-                 const void* buf, const StepScalars& sc, cudaStream_t s);
+                 const void* buf, const StepScalars& sc, const int32_t* go, cudaStream_t s);
 template <typename T>
 int launch_pack_grads(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* grads,
                       int32_t dtype, void* buf, cudaStream_t s);
+// host-mapped pinned memory transfers (no copy engine): flag -> host, pointer table <- host
+int launch_publish_flag(const int32_t* src, int32_t* mapped_dst, cudaStream_t s);
+int launch_copy_ptrs(const void* mapped_src, void* dst, int n, cudaStream_t s);
 template <typename T>
 int launch_region_finite(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* buf, int32_t* flag,
                          cudaStream_t s);

@@ -177,11 +177,13 @@ class DistributedShampoo(torch.optim.Optimizer):
                  large_dim_method=LargeDimMethod.BLOCKING, precision: str = "double",
                  lr_schedule: str = "constant", warmup_steps: int = 0, total_steps: int = 0,
                  process_group=None, reduce_gradients: Optional[str] = None,
-                 check_replicas_every: int = 0):
+                 check_replicas_every: int = 0, check_finite=True):
         """``reduce_gradients``: None (p.grad already holds the global gradient, e.g. after DDP) or
         "mean" / "sum": p.grad holds this rank's LOCAL gradient and the optimizer reduce-scatters
         it to the block owners itself (no separate DDP all-reduce needed).
-        ``check_replicas_every``: run the replica drift check (dist.py:361-368) every N steps (0: off)."""
+        ``check_replicas_every``: run the replica drift check (dist.py:361-368) every N steps (0: off).
+        ``check_finite``: True (raise from the bad step, one host sync per step), "deferred" (no host
+        sync; the bad step is skipped on the device and the next call raises), False."""
         if reduce_gradients not in (None, "mean", "sum"):
             raise ValueError("reduce_gradients must be None, 'mean' or 'sum'")
         if check_replicas_every < 0:
@@ -216,7 +218,7 @@ class DistributedShampoo(torch.optim.Optimizer):
                 raise ValueError("num_trainers_per_group > 1 needs torch.distributed to be initialised")
             self.exchange, world, rank, group = None, 1, 0, 1
         self.engine = Shampoo([p.data for p in self._plist], self.config, world_size=world,
-                              group_size=group, rank=rank, exchange=self.exchange)
+                              group_size=group, rank=rank, exchange=self.exchange, check_finite=check_finite)
 
     @property
     def guard_stats(self) -> GuardStats:

@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass
-from typing import Callable, Optional, Sequence
+from typing import Callable, Optional, Sequence, Union
 
 import numpy as np
 import torch
@@ -91,7 +91,7 @@ class Shampoo:
                  world_size: int = 1, group_size: int = 1, rank: int = 0,
                  device: Optional[torch.device] = None,
                  exchange: Optional[Callable[[torch.Tensor, int, int], None]] = None,
-                 check_finite: bool = True):
+                 check_finite: Union[bool, str] = True):
         self.config = config if config is not None else ShampooConfig()
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
@@ -114,7 +114,14 @@ class Shampoo:
         self.world_size, self.group_size, self.rank = world_size, group_size, rank
         self.group_rank = rank % group_size
         self.exchange = exchange
+        if check_finite not in (True, False, "deferred"):
+            raise ValueError("check_finite must be True, False or 'deferred'")
+        # True: the reference's guard (optim.py:362-366), raised by the bad step itself, one host sync
+        # per step; "deferred": no host sync -- the check predicates the step's state-writing kernels on
+        # the device and the NonFiniteGradientError of a skipped step is raised by the NEXT call
+        # (step / synchronize / state_tree / step_count), with the step counter rolled back
         self.check_finite = check_finite
+        self._pending_check = False
         self._t = 0
         # float32 parameters: directions travel (all-gather) and apply in float32 -- the update lands
         # in float32 anyway; half the gather-buffer bytes
@@ -151,7 +158,21 @@ class Shampoo:
 
     @property
     def step_count(self) -> int:
+        self.synchronize()
         return self._t
+
+    def synchronize(self) -> None:
+        """Resolve a deferred non-finite check: raises NonFiniteGradientError if the last step was
+        skipped on the device (its step count is rolled back first)."""
+        if not self._pending_check:
+            return
+        self._pending_check = False
+        aborted = C.c_int32()
+        rc = N.lib().shampoo_check_finite_resolve(self._ctx, C.byref(aborted))
+        if aborted.value:
+            self._t -= 1
+            raise NonFiniteGradientError("gradient contains non-finite entries; step aborted (deferred check)")
+        N.check(rc, "check_finite_resolve")
 
     def advance_step(self) -> None:
         self._t += 1
@@ -217,21 +238,28 @@ class Shampoo:
     def step(self, grads, lr: Optional[float] = None) -> None:
         """One full optimizer step (optim.py:356-383); raises before any mutation on bad input.
         ``lr``: overrides lr_at(config, t) for this step (torch LR schedulers through the facade)."""
+        self.synchronize()
         grads = self._as_grads(grads)
         if self._params:
             dt = {p.dtype for p in self._params}
             if len(dt) != 1:
                 raise TypeError("all parameters must share one dtype")
-        if self.check_finite and grads:
-            gp = N.ptr_array([g.data_ptr() for g in grads])
-            rc = N.lib().shampoo_check_finite(self._ctx, gp, _dtype_code(grads[0]), self._stream())
-            if rc == N.ERR_NONFINITE_GRAD:
-                raise NonFiniteGradientError("gradient contains non-finite entries; step aborted")
-            N.check(rc, "check_finite")
         t = self._t
         lr_at(self.config, t)  # OutOfRangeError before any mutation
         if lr is not None and not (float(lr) >= 0.0):
             raise ValueError("lr must be non-negative")
+        if self.check_finite and grads:
+            gp = N.ptr_array([g.data_ptr() for g in grads])
+            if self.check_finite == "deferred":
+                deferred = C.c_int32()
+                rc = N.lib().shampoo_check_finite_deferred(self._ctx, gp, _dtype_code(grads[0]), t,
+                                                           C.byref(deferred), self._stream())
+                self._pending_check = rc == N.OK and bool(deferred.value)
+            else:
+                rc = N.lib().shampoo_check_finite(self._ctx, gp, _dtype_code(grads[0]), self._stream())
+            if rc == N.ERR_NONFINITE_GRAD:
+                raise NonFiniteGradientError("gradient contains non-finite entries; step aborted")
+            N.check(rc, "check_finite")
         self.compute_directions(grads, t)
         if self.exchange is not None and self.group_size > 1:
             self.exchange(self.gather_buffer, self.group_rank, self.max_payload)
@@ -264,6 +292,7 @@ class Shampoo:
         reduce-scatter): only this rank's owned blocks are read, scaled by ``scale``.  Raises
         NonFiniteGradientError before any mutation if an owned block holds a non-finite entry;
         ``flag``: the ``nonfinite_flag()`` already max-reduced across ranks (distributed)."""
+        self.synchronize()
         if flag is None:
             flag = self.nonfinite_flag()
         if self.check_finite and int(flag.item()):
@@ -300,6 +329,7 @@ class Shampoo:
         """Step from this rank's LOCAL gradients: reduce-scatter them to the block owners (+ all-reduce
         across replica groups) instead of a full DDP all-reduce, then the usual step.  ``average``
         divides by the world size (DDP mean).  Single process: identical to ``step(grads)``."""
+        self.synchronize()
         buf = self.pack_local_gradients(grads)
         ex = self.exchange
         distributed = ex is not None and self.world_size > 1
@@ -331,6 +361,7 @@ class Shampoo:
 
     def state_tree(self) -> dict:
         """Nested state param -> block -> name -> payload (copies, float64 numpy)."""
+        self.synchronize()
         torch.cuda.synchronize(self.device)
         lib = N.lib()
         gstep = C.c_int64()
@@ -414,6 +445,7 @@ class Shampoo:
         """Write this optimizer's parameters and state as a reference-format JSON checkpoint (one
         file; a sharded optimizer writes only its owned blocks -- see DistributedShampoo for the
         union)."""
+        self.synchronize()
         from .checkpoint import save_checkpoint
         tree = self.state_tree()
         save_checkpoint(path, self._t, [p.detach().cpu().numpy() for p in self._params], tree)
