@@ -338,6 +338,12 @@ int build_engine(shampoo_ctx* c) {
       const int rc = b.set_slices(ps);
       if (rc) return rc;
     }
+    // statistics slices (SHAMPOO_STATS_SLICES overrides the FP64-class default)
+    const char* es = std::getenv("SHAMPOO_STATS_SLICES");
+    if (es) {
+      const int rc = e->stats.set_slices(std::atoi(es));
+      if (rc) return rc;
+    }
   }
   for (size_t l = 0; l < c->owned.size(); ++l) {
     const BlockPlan& b = c->plan.blocks[c->owned[l]];

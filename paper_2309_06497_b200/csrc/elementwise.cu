@@ -27,6 +27,40 @@ __device__ __forceinline__ bool graft_normalized(int32_t g) {
   return g >= SHAMPOO_GRAFT_NORMALIZED_ADAGRAD;
 }
 
+// Two consecutive elements per access (8- or 16-byte vectors) on the contiguous-block fast paths.
+template <typename T> struct Pair;
+template <> struct Pair<double> { using V = double2; };
+template <> struct Pair<float> { using V = float2; };
+template <typename T>
+__device__ __forceinline__ void ld2(const T* p, T& a, T& b) {
+  const typename Pair<T>::V v = *reinterpret_cast<const typename Pair<T>::V*>(p);
+  a = v.x;
+  b = v.y;
+}
+template <typename T>
+__device__ __forceinline__ void st2(T* p, T a, T b) {
+  typename Pair<T>::V v;
+  v.x = a;
+  v.y = b;
+  *reinterpret_cast<typename Pair<T>::V*>(p) = v;
+}
+template <typename T>
+__device__ __forceinline__ void ld2_as(const void* p, int64_t i, int32_t dtype, T& a, T& b) {
+  if (dtype == SHAMPOO_DTYPE_F32) {
+    float x, y;
+    ld2<float>(static_cast<const float*>(p) + i, x, y);
+    a = T(x);
+    b = T(y);
+  } else {
+    double x, y;
+    ld2<double>(static_cast<const double*>(p) + i, x, y);
+    a = T(x);
+    b = T(y);
+  }
+}
+__device__ __forceinline__ bool al(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) & (bytes - 1)) == 0; }
+__device__ __forceinline__ int dsize(int32_t dtype) { return dtype == SHAMPOO_DTYPE_F32 ? 4 : 8; }
+
 __global__ void __launch_bounds__(NT) k_finite(const Chunk* __restrict__ chunks,
                                                const DevBlock* __restrict__ params,
                                                const void* const* __restrict__ grads, int32_t dtype,
@@ -64,68 +98,129 @@ __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restric
   T* GA = static_cast<T*>(ar.GA) + B.vofs;
   const void* gp = grads[B.param];
   const void* wp = params[B.param];
+  const T* gb = sc.gbuf ? static_cast<const T*>(ar.GBUF) + B.gofs : nullptr;  // reduced gradients
   const bool normalized = graft_normalized(sc.graft);
+  const bool fresh = pass == 0 || !normalized;  // g from the caller (else the pass-0 copy in G)
+  const bool graft = pass != 0 && sc.graft != SHAMPOO_GRAFT_SGD;
+  const bool filt = pass != 0 && sc.use_filter;
   double inv_norm = 1.0;
   if (pass == 1 && normalized) {
     const double n2 = ar.gnorm2[B.local];
     inv_norm = n2 > 0.0 ? 1.0 / sqrt(n2) : 1.0;
   }
-  double acc = 0.0;
-  // U elements per thread per iteration: every load of the batch is issued before the first store
-  // (the state arrays may alias the caller's pointers as far as the compiler knows), same element
-  // order as a plain strided loop, so the partial sums are unchanged
-  constexpr int U = 4;
-  for (int64_t e0 = threadIdx.x; e0 < c.count; e0 += U * NT) {
-    T gq[U], aq[U], fq[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + (int64_t)u * NT;
-      gq[u] = aq[u] = fq[u] = T(0);
-      if (e >= c.count) continue;
-      const int64_t j = c.start + e;
-      if (pass == 0 || !normalized) {
-        if (sc.gbuf) {  // reduced gradient: this block's slice of the gather-layout buffer
-          gq[u] = T(sc.gscale * (double)static_cast<const T*>(ar.GBUF)[B.gofs + j]);
-          if (sc.l2) gq[u] += T(sc.weight_decay) * load_as<T>(wp, block_to_param_offset(B, j), sc.pdtype);
-        } else {
-          const int64_t po = block_to_param_offset(B, j);
-          gq[u] = load_as<T>(gp, po, sc.pdtype);
-          if (sc.l2) gq[u] += T(sc.weight_decay) * load_as<T>(wp, po, sc.pdtype);
-        }
-      } else {
-        gq[u] = G[j];
+  // Elements in pairs (2q, 2q+1), pair q on thread q % NT: one summation order whichever way the
+  // pair is loaded -- 8/16-byte vectors when the block is one contiguous run and every array is
+  // pair-aligned, else two scalar accesses -- so reduced-buffer and caller-gradient steps agree bitwise.
+  const int64_t j0 = c.start;
+  const bool contig = B.cbase >= 0;
+  const int64_t p0 = contig ? B.cbase + c.start : 0;
+  const int es = dsize(sc.pdtype);
+  const bool vec = contig && al(G + j0, 2 * sizeof(T)) &&
+                   (!fresh || (sc.gbuf ? al(gb + j0, 2 * sizeof(T)) : al(static_cast<const char*>(gp) + p0 * es, 2 * es))) &&
+                   (!fresh || !sc.l2 || al(static_cast<const char*>(wp) + p0 * es, 2 * es)) &&
+                   (!graft || al(GA + j0, 2 * sizeof(T))) && (!filt || (al(F + j0, 2 * sizeof(T)) && al(GE + j0, 2 * sizeof(T))));
+  auto param_off = [&](int64_t j) { return contig ? B.cbase + j : block_to_param_offset(B, j); };
+  // gradient of elements j, j + 1 (n = 2) or j (n = 1)
+  auto load_g = [&](int64_t j, int n, T& g0, T& g1) {
+    g1 = T(0);
+    if (!fresh) {
+      if (n == 2 && vec) ld2<T>(G + j, g0, g1);
+      else {
+        g0 = G[j];
+        if (n == 2) g1 = G[j + 1];
       }
-      if (pass != 0 && sc.graft != SHAMPOO_GRAFT_SGD) aq[u] = GA[j];
-      if (pass != 0 && sc.use_filter) fq[u] = F[j];
+      return;
+    }
+    if (sc.gbuf) {
+      if (n == 2 && vec) ld2<T>(gb + j, g0, g1);
+      else {
+        g0 = gb[j];
+        if (n == 2) g1 = gb[j + 1];
+      }
+      g0 = T(sc.gscale * (double)g0);
+      g1 = T(sc.gscale * (double)g1);
+    } else if (n == 2 && vec) {
+      ld2_as<T>(gp, p0 + (j - j0), sc.pdtype, g0, g1);
+    } else {
+      g0 = load_as<T>(gp, param_off(j), sc.pdtype);
+      if (n == 2) g1 = load_as<T>(gp, param_off(j + 1), sc.pdtype);
+    }
+    if (sc.l2) {
+      T w0, w1 = T(0);
+      if (n == 2 && vec) ld2_as<T>(wp, p0 + (j - j0), sc.pdtype, w0, w1);
+      else {
+        w0 = load_as<T>(wp, param_off(j), sc.pdtype);
+        if (n == 2) w1 = load_as<T>(wp, param_off(j + 1), sc.pdtype);
+      }
+      g0 += T(sc.weight_decay) * w0;
+      g1 += T(sc.weight_decay) * w1;
+    }
+  };
+  auto ldp = [&](const T* a, int64_t j, int n, T& x0, T& x1) {
+    if (n == 2 && vec) ld2<T>(a + j, x0, x1);
+    else {
+      x0 = a[j];
+      x1 = n == 2 ? a[j + 1] : T(0);
+    }
+  };
+  auto stp = [&](T* a, int64_t j, int n, T x0, T x1) {
+    if (n == 2 && vec) st2<T>(a + j, x0, x1);
+    else {
+      a[j] = x0;
+      if (n == 2) a[j + 1] = x1;
+    }
+  };
+  double acc = 0.0;
+  const int64_t npair = (c.count + 1) >> 1;
+  constexpr int U2 = 2;  // pairs per thread per iteration: all loads of the batch before its stores
+  for (int64_t q0 = threadIdx.x; q0 < npair; q0 += U2 * NT) {
+    T g[U2][2], a[U2][2], f[U2][2];
+#pragma unroll
+    for (int u = 0; u < U2; ++u) {
+      const int64_t q = q0 + (int64_t)u * NT;
+      g[u][0] = g[u][1] = a[u][0] = a[u][1] = f[u][0] = f[u][1] = T(0);
+      if (q >= npair) continue;
+      const int64_t j = j0 + 2 * q;
+      const int n = (2 * q + 1 < c.count) ? 2 : 1;
+      load_g(j, n, g[u][0], g[u][1]);
+      if (graft) ldp(GA, j, n, a[u][0], a[u][1]);
+      if (filt) ldp(F, j, n, f[u][0], f[u][1]);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + (int64_t)u * NT;
-      if (e >= c.count) continue;
-      const int64_t j = c.start + e;
-      const T g = gq[u];
-      if (pass == 0 || !normalized) G[j] = g;
+    for (int u = 0; u < U2; ++u) {
+      const int64_t q = q0 + (int64_t)u * NT;
+      if (q >= npair) continue;
+      const int64_t j = j0 + 2 * q;
+      const int n = (2 * q + 1 < c.count) ? 2 : 1;
+      if (fresh) stp(G, j, n, g[u][0], g[u][1]);
       if (pass == 0) {
-        acc += (double)g * (double)g;
+        acc += (double)g[u][0] * (double)g[u][0];
+        if (n == 2) acc += (double)g[u][1] * (double)g[u][1];
         continue;
       }
-      T a = T(0);
-      if (sc.graft != SHAMPOO_GRAFT_SGD) {
-        const T gg = normalized ? T((double)g * inv_norm) : g;
-        const T sq = gg * gg;
-        a = aq[u];
-        a = graft_summed(sc.graft) ? a + sq : T(sc.beta2g) * a + T(sc.one_minus_beta2g) * sq;
-        GA[j] = a;
+      T ge[2] = {g[u][0], g[u][1]};
+      if (graft) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const T gg = normalized ? T((double)g[u][h] * inv_norm) : g[u][h];
+          const T sq = gg * gg;
+          a[u][h] = graft_summed(sc.graft) ? a[u][h] + sq : T(sc.beta2g) * a[u][h] + T(sc.one_minus_beta2g) * sq;
+        }
+        stp(GA, j, n, a[u][0], a[u][1]);
       }
-      T ge = g;
-      if (sc.use_filter) {
-        const T f = T(sc.beta1) * fq[u] + T(sc.one_minus_beta1) * g;
-        F[j] = f;
-        ge = f * T(sc.inv_bc1);
-        GE[j] = ge;
+      if (filt) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          f[u][h] = T(sc.beta1) * f[u][h] + T(sc.one_minus_beta1) * g[u][h];
+          ge[h] = f[u][h] * T(sc.inv_bc1);
+        }
+        stp(F, j, n, f[u][0], f[u][1]);
+        stp(GE, j, n, ge[0], ge[1]);
       }
-      const T pg = graft_dir<T>(sc.graft, ge, a, sc.inv_bc2g, sc.graft_eps);
-      acc += (double)pg * (double)pg;
+      for (int h = 0; h < n; ++h) {
+        const T pg = graft_dir<T>(sc.graft, ge[h], a[u][h], sc.inv_bc2g, sc.graft_eps);
+        acc += (double)pg * (double)pg;
+      }
     }
   }
   acc = block_sum<double, NT>(acc, red);
@@ -180,6 +275,68 @@ __global__ void __launch_bounds__(NT) k_final(const Chunk* __restrict__ chunks,
     ps_zero = (n2 == 0.0);
     if (!ps_zero) ratio = sqrt(ar.pg2[B.local]) / sqrt(n2);  // grafting.py:95-110
   }
+  const bool from_ps = use_ps && !ps_zero;
+  if (B.cbase >= 0) {  // contiguous block: two elements per access when every array is pair-aligned
+    const int64_t j0 = c.start, p0 = B.cbase + c.start;
+    const int pb = 2 * dsize(sc.pdtype);
+    const bool graft = !from_ps && sc.graft != SHAMPOO_GRAFT_SGD;
+    if (al(out + j0, 2 * sizeof(BT)) && (from_ps ? al(PS + j0, 2 * sizeof(T)) : al(G + j0, 2 * sizeof(T))) &&
+        (!graft || al(GA + j0, 2 * sizeof(T))) && (sc.momentum <= 0.0 || al(M + j0, 2 * sizeof(T))) &&
+        (!sc.decoupled || al(static_cast<const char*>(wp) + p0 * dsize(sc.pdtype), pb))) {
+      const int64_t np2 = c.count >> 1;
+      constexpr int U2 = 2;
+      for (int64_t q0 = threadIdx.x; q0 < np2; q0 += U2 * NT) {
+        T pv[U2][2], av[U2][2], wv[U2][2], mv[U2][2];
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          const int64_t q = q0 + (int64_t)u * NT;
+          pv[u][0] = pv[u][1] = av[u][0] = av[u][1] = wv[u][0] = wv[u][1] = mv[u][0] = mv[u][1] = T(0);
+          if (q >= np2) continue;
+          const int64_t j = j0 + 2 * q;
+          if (from_ps) {
+            ld2<T>(PS + j, pv[u][0], pv[u][1]);
+          } else {
+            ld2<T>(G + j, pv[u][0], pv[u][1]);
+            if (graft) ld2<T>(GA + j, av[u][0], av[u][1]);
+          }
+          if (sc.decoupled) ld2_as<T>(wp, p0 + 2 * q, sc.pdtype, wv[u][0], wv[u][1]);
+          if (sc.momentum > 0.0) ld2<T>(M + j, mv[u][0], mv[u][1]);
+        }
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          const int64_t q = q0 + (int64_t)u * NT;
+          if (q >= np2) continue;
+          const int64_t j = j0 + 2 * q;
+          T r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            T p = from_ps ? T(ratio * (double)pv[u][h]) : graft_dir<T>(sc.graft, pv[u][h], av[u][h], sc.inv_bc2g, sc.graft_eps);
+            if (sc.decoupled) p += T(sc.weight_decay) * wv[u][h];
+            if (sc.momentum > 0.0) {
+              const T m = T(sc.momentum) * mv[u][h] + p;
+              mv[u][h] = m;
+              p = sc.nesterov ? T(sc.momentum) * m + p : m;
+            }
+            r[h] = p;
+          }
+          if (sc.momentum > 0.0) st2<T>(M + j, mv[u][0], mv[u][1]);
+          st2<BT>(out + j, BT(r[0]), BT(r[1]));
+        }
+      }
+      if (!(c.count & 1) || threadIdx.x != 0) return;
+      // odd tail: the last element through the scalar loop below (thread 0 only)
+      const int64_t j = j0 + c.count - 1;
+      T p = from_ps ? T(ratio * (double)PS[j]) : graft_dir<T>(sc.graft, G[j], graft ? GA[j] : T(0), sc.inv_bc2g, sc.graft_eps);
+      if (sc.decoupled) p += T(sc.weight_decay) * load_as<T>(wp, p0 + c.count - 1, sc.pdtype);
+      if (sc.momentum > 0.0) {
+        const T m = T(sc.momentum) * M[j] + p;
+        M[j] = m;
+        p = sc.nesterov ? T(sc.momentum) * m + p : m;
+      }
+      out[j] = BT(p);
+      return;
+    }
+  }
   constexpr int U = 4;  // loads of U elements before their stores (see k_prepare)
   for (int64_t e0 = threadIdx.x; e0 < c.count; e0 += U * NT) {
     T pq[U], aq[U], wq[U], mq[U];
@@ -226,6 +383,42 @@ __global__ void __launch_bounds__(NT) k_apply(const Chunk* __restrict__ chunks,
   const DevBlock& B = blocks[c.block];
   const BT* p = buf + B.gofs;
   void* wp = params[B.param];
+  if (B.cbase >= 0) {  // contiguous block: two elements per access when pair-aligned
+    const int64_t j0 = c.start, p0 = B.cbase + c.start;
+    const int es = dsize(pdtype);
+    if (al(p + j0, 2 * sizeof(BT)) && al(static_cast<char*>(wp) + p0 * es, 2 * es)) {
+      const int64_t np2 = c.count >> 1;
+#pragma unroll 4
+      for (int64_t q = threadIdx.x; q < np2; q += NT) {
+        BT d0, d1;
+        ld2<BT>(p + j0 + 2 * q, d0, d1);
+        const double s0 = __dmul_rn(lr, (double)d0), s1 = __dmul_rn(lr, (double)d1);
+        if (pdtype == SHAMPOO_DTYPE_F32) {
+          float* w = static_cast<float*>(wp) + p0 + 2 * q;
+          float w0, w1;
+          ld2<float>(w, w0, w1);
+          st2<float>(w, (float)__dsub_rn((double)w0, s0), (float)__dsub_rn((double)w1, s1));
+        } else {
+          double* w = static_cast<double*>(wp) + p0 + 2 * q;
+          double w0, w1;
+          ld2<double>(w, w0, w1);
+          st2<double>(w, __dsub_rn(w0, s0), __dsub_rn(w1, s1));
+        }
+      }
+      if ((c.count & 1) && threadIdx.x == 0) {
+        const int64_t j = j0 + c.count - 1, po = p0 + c.count - 1;
+        const double step = __dmul_rn(lr, (double)p[j]);
+        if (pdtype == SHAMPOO_DTYPE_F32) {
+          float* w = static_cast<float*>(wp);
+          w[po] = (float)__dsub_rn((double)w[po], step);
+        } else {
+          double* w = static_cast<double*>(wp);
+          w[po] = __dsub_rn(w[po], step);
+        }
+      }
+      return;
+    }
+  }
   for (int64_t e = threadIdx.x; e < c.count; e += NT) {
     const int64_t j = c.start + e;
     const int64_t po = block_to_param_offset(B, j);

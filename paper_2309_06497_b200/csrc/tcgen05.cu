@@ -289,6 +289,34 @@ __device__ __forceinline__ void ozaki_pack4(const double (&x)[4], int e, uint32_
   }
 }
 
+// 16 consecutive elements of one operand row (k0 .. k0+15, `valid` of them inside the row) as doubles:
+// 16-byte vector loads when the run is complete and aligned (the common case), else scalar.
+template <typename T>
+__device__ __forceinline__ void load_run16(const T* __restrict__ rp, int valid, double (&xv)[16]) {
+  if (valid >= 16 && (reinterpret_cast<uintptr_t>(rp) & 15u) == 0) {
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(rp) + i);
+        xv[2 * i] = v.x;
+        xv[2 * i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(rp) + i);
+        xv[4 * i] = v.x;
+        xv[4 * i + 1] = v.y;
+        xv[4 * i + 2] = v.z;
+        xv[4 * i + 3] = v.w;
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xv[i] = i < valid ? (double)rp[i] : 0.0;
+}
+
 // Operands -> int8 slice planes, slice-major per stage: byte offset
 // ((stage * S + s) * rc + core) * 256 + kc * 128 + r8 * 16 holds row 8 core + r8,
 // k = 32 stage + 16 kc .. +15 of slice s.  Unit u = ((stage * rc + core) * 2 + kc) * 8 + r8.
@@ -318,7 +346,9 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
     const int e = max(exps[J.exp + row], kExpFloor);
     const Idx2 kx = J.k;
     double xv[16];
-    if (kx.div == 0x7fffffff) {  // one stride along k (the common case): no per-element index map
+    if (kx.div == 0x7fffffff && kx.lo == 1) {  // contiguous k: one 128-byte run
+      load_run16<T>(src + rb + k0, J.K - k0, xv);
+    } else if (kx.div == 0x7fffffff) {  // one stride along k: no per-element index map
       const T* rp = src + rb + (int64_t)k0 * kx.lo;
 #pragma unroll
       for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)rp[(int64_t)i * kx.lo] : 0.0;
@@ -428,7 +458,9 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
       const int e = rexp[cl * 8 + r8];
       const Idx2 kx = J.k;
       double xv[16];
-      if (kx.div == 0x7fffffff) {
+      if (kx.div == 0x7fffffff && kx.lo == 1) {
+        load_run16<T>(src + rb + k0, J.K - k0, xv);
+      } else if (kx.div == 0x7fffffff) {
         const T* rp = src + rb + (int64_t)k0 * kx.lo;
 #pragma unroll
         for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)rp[(int64_t)i * kx.lo] : 0.0;
