@@ -13,10 +13,12 @@ namespace shampoo {
 
 namespace {
 
-constexpr int TM = 128, TN = 32, TKB = 32;    // CTA tile; 32 int8 (= one MMA K) per pipeline stage
+// CTA tile TM x TN, 32 int8 (= one MMA K) per pipeline stage.  TN = 64: the kernel is bound by the
+// operand bytes each SM takes in per MMA (measured 49 GB/s per SM at TN = 32 for both S = 6 and 8);
+// an A slice feeds twice the output columns per byte at TN = 64
+constexpr int TM = 128, TN = 64, TKB = 32;
 constexpr int SL_PER_MMA = 256 / TN;          // B slices stacked along N in one MMA (N <= 256)
-constexpr int GEMM_THREADS = 192;             // warp 0 bulk copies, warp 1 MMA, warps 2-5 epilogue
-constexpr int GEMM_THREADS_P = 320;           // persistent variant: 8 epilogue warps
+constexpr int GEMM_THREADS_P = 320;           // warp 0 bulk copies, warp 1 MMA, warps 2-9 epilogue
 constexpr int64_t kOzSplitStages = 256;       // 8192 k per split: int32 sums stay exact (< 2^31)
 constexpr int PACK_UNITS = 256;               // pack threads per CTA (one unit = 16 k of one row)
 constexpr int EXP_CHUNK = 64;                 // k per rowexp thread (strided rows)
@@ -33,10 +35,6 @@ struct OzCfg {
   static constexpr int A_BYTES = (TM / 8) * S * 256;     // one stage of a 128-row tile, all slices
   static constexpr int B_BYTES = (TN / 8) * S * 256;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  // two CTAs per SM (one's FP64 epilogue overlaps the other's MMAs): <= ~100 KB of stages each
-  static constexpr int STAGES = (100 * 1024) / STAGE < 6 ? (100 * 1024) / STAGE : 6;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;
-  static constexpr uint32_t TMEM_COLS = 256;             // S * TN <= 256: two CTAs share the 512 columns
   // kind::i8: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1), K-major, M = 128; N (bits 17-22)
   // is set per instruction
   static constexpr uint32_t IDESC_BASE = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TM >> 4) << 24);
@@ -492,232 +490,14 @@ __device__ __forceinline__ double pow2i(int e) {
 
 constexpr int LDE = TN + 1;  // staged epilogue tile leading dim (doubles)
 
-template <typename T, int S>
-__global__ void __launch_bounds__(GEMM_THREADS, 2) k_oz_gemm(const GemmProblem* __restrict__ probs,
-                                                            const OzProb* __restrict__ tps,
-                                                            const int64_t* __restrict__ begin, int nprob,
-                                                            const int32_t* __restrict__ mask,
-                                                            const int8_t* __restrict__ arena,
-                                                            const int32_t* __restrict__ exps, double* __restrict__ ws,
-                                                            const CUtensorMap* __restrict__ tmaps) {
-  using Cfg = OzCfg<S>;
-  extern __shared__ __align__(1024) uint8_t oz_smem[];
-  // per stage two "full" barriers: [0] all B slices + the first half of the A slices, [1] the rest of
-  // A, so the MMAs of the first A slices overlap the tail of the stage's copies
-  __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES][2], empty_bar[Cfg::STAGES], done_bar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ double col_scale[TN];
-  __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
-  const int pi = find64<GemmProblem>(begin, nprob, blockIdx.x);
-  const GemmProblem& P = probs[pi];
-  if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
-  const OzProb& T_ = tps[pi];
-  const int64_t l = blockIdx.x - begin[pi];
-  const int split = (int)(l % T_.ksplit);
-  const int64_t tile = l / T_.ksplit;
-  int tm, tn;
-  if (P.flags & kGemmSym) sym_decode(tile, T_.nt, tm, tn);
-  else {
-    tm = (int)(tile / T_.nt);
-    tn = (int)(tile % T_.nt);
-  }
-  const int s0 = split * T_.kst;
-  const int nk = min(T_.ks, s0 + T_.kst) - s0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
-  // row cores present in this tile (rows beyond M / N are never stored: their smem stays stale)
-  const int a_cores = min(TM / 8, T_.a_rc - tm * (TM / 8));
-  const int b_cores = min(TN / 8, T_.b_rc - tn * (TN / 8));
-
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i][0], 1);
-      mbar_init(&full_bar[i][1], 1);
-      mbar_init(&empty_bar[i], 1);
-    }
-    mbar_init(&done_bar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "n"(Cfg::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {  // producer: per stage and slice, the tile's row cores (contiguous) of A and B
-      const int64_t a_plane = (int64_t)T_.a_rc * 256, b_plane = (int64_t)T_.b_rc * 256;
-      const int8_t* a_src = arena + T_.a_pack + (int64_t)s0 * S * a_plane + (int64_t)tm * (TM / 8) * 256;
-      const int8_t* b_src = arena + T_.b_pack + (int64_t)s0 * S * b_plane + (int64_t)tn * (TN / 8) * 256;
-      const uint32_t a_bytes = (uint32_t)a_cores * 256, b_bytes = (uint32_t)b_cores * 256;
-      for (int it = 0; it < nk; ++it) {
-        const int st = it % Cfg::STAGES;
-        const uint32_t use = (uint32_t)(it / Cfg::STAGES);
-        if (it >= Cfg::STAGES) mbar_wait(&empty_bar[st], (use & 1u) ^ 1u);
-        uint8_t* sb = sbase + (size_t)st * Cfg::STAGE;
-        constexpr int SH = (S + 1) / 2;  // A slices in the first half
-        const int8_t* as = a_src + (int64_t)it * S * a_plane;
-        const int8_t* bs = b_src + (int64_t)it * S * b_plane;
-        if (tmaps) {
-          // three TMA boxes per stage: B (4 cores x S slices), A slices [0, SH) and [SH, S) (16 cores
-          // each); cores past the operand's end arrive zero-filled, so the byte counts are fixed
-          const CUtensorMap* tm3 = tmaps + 3 * pi;
-          const int z = (s0 + it) * S;
-          mbar_expect_tx(&full_bar[st][0], (uint32_t)(S * (TN / 8) * 256 + SH * (TM / 8) * 256));
-          mbar_expect_tx(&full_bar[st][1], (uint32_t)((S - SH) * (TM / 8) * 256));
-          tma_load_3d(sb + Cfg::A_BYTES, tm3 + 2, 0, tn * (TN / 8), z, &full_bar[st][0]);
-          tma_load_3d(sb, tm3 + 0, 0, tm * (TM / 8), z, &full_bar[st][0]);
-          tma_load_3d(sb + SH * (TM / 8) * 256, tm3 + 1, 0, tm * (TM / 8), z + SH, &full_bar[st][1]);
-          continue;
-        }
-        mbar_expect_tx(&full_bar[st][0], (uint32_t)S * b_bytes + (uint32_t)SH * a_bytes);
-        mbar_expect_tx(&full_bar[st][1], (uint32_t)(S - SH) * a_bytes);
-#pragma unroll
-        for (int q = 0; q < S; ++q) {
-          bulk_g2s(sb + Cfg::A_BYTES + q * (TN / 8) * 256, bs + q * b_plane, b_bytes, &full_bar[st][0]);
-          if (q < SH) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][0]);
-        }
-#pragma unroll
-        for (int q = SH; q < S; ++q) bulk_g2s(sb + q * (TM / 8) * 256, as + q * a_plane, a_bytes, &full_bar[st][1]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // MMA issuer.  A slice sa times the B slices sb = 0 .. S-1-sa stacked along N (slice-major in
-      // smem): output column block sb lands at TMEM column (sa + sb) * TN = accumulator of diagonal
-      // d = sa + sb.  N <= 256 per instruction (one MMA per A slice for TN = 32).
-      for (int it = 0; it < nk; ++it) {
-        const int st = it % Cfg::STAGES;
-        const uint32_t par = (uint32_t)(it / Cfg::STAGES) & 1u;
-        mbar_wait(&full_bar[st][0], par);
-        tc_fence_after();
-        const uint32_t sa_base = smem_u32(sbase + (size_t)st * Cfg::STAGE);
-        const uint32_t sb_base = sa_base + Cfg::A_BYTES;
-#pragma unroll
-        for (int sa = 0; sa < S; ++sa) {
-          if (sa == (S + 1) / 2) {
-            mbar_wait(&full_bar[st][1], par);
-            tc_fence_after();
-          }
-          const uint64_t ad = sdesc(sa_base + sa * (TM / 8) * 256, 128, 256);
-#pragma unroll
-          for (int sb0 = 0; sb0 < S - sa; sb0 += SL_PER_MMA) {
-            const int nsl = min(SL_PER_MMA, S - sa - sb0);
-            const uint64_t bd = sdesc(sb_base + sb0 * (TN / 8) * 256, 128, 256);
-            const uint32_t idesc = Cfg::IDESC_BASE | ((uint32_t)(nsl * TN >> 3) << 17);
-            tc_mma_i8(tmem + (uint32_t)((sa + sb0) * TN), ad, bd, idesc, (it > 0 || sa > 0) ? 1u : 0u);
-          }
-        }
-        tc_commit(&empty_bar[st]);  // frees the stage once these MMAs have read it
-      }
-      tc_commit(&done_bar);
-      atomicAdd(&g_oz_mma_units, (unsigned long long)nk * (S * (S + 1) / 2));
-    }
-  } else {
-    // epilogue (128 threads): TMEM -> FP64 diagonal combination -> smem tile -> coalesced stores
-    const int et = threadIdx.x - 64;
-    const int lg = warp & 3;
-    const int rl = lg * 32 + lane;
-    double* tileS = reinterpret_cast<double*>(sbase);  // pipeline smem is free once done_bar fires
-    if (et < TN) {
-      const int gj = tn * TN + et;
-      col_scale[et] = pow2i(exps[T_.b_exp + min(gj, T_.b_rc * 8 - 1)]);
-      col_off[et] = evx(P.c_c, gj);
-      mrow_off[et] = evx(P.c_r, gj);
-    }
-    {
-      const int gi = tm * TM + et;
-      row_off[et] = evx(P.c_r, gi);
-      mcol_off[et] = evx(P.c_c, gi);
-    }
-    mbar_wait_sleep(&done_bar, 0);
-    tc_fence_after();
-    const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
-    // diagonals combined exactly in two int64 fixed-point halves (|acc_d| < 2^31, so each half
-    // stays below 2^53 and converts to double exactly): one rounding per output
-    constexpr int H = (S + 1) / 2;
-    int32_t v[16];
-    for (int c0 = 0; c0 < TN; c0 += 16) {
-      long long hi[16], lo[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0;
-      if (nk > 0) {
-#pragma unroll
-        for (int d = 0; d < S; ++d) {
-          tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * TN + c0), v);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            if (d < H) hi[q] += (long long)v[q] << (7 * (H - 1 - d));
-            else lo[q] += (long long)v[q] << (7 * (S - 1 - d));
-          }
-        }
-      }
-      const double whi = pow2i(-7 * (H + 1)), wlo = pow2i(-7 * (S + 1));
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        tileS[rl * LDE + c0 + q] = fma((double)hi[q], whi, (double)lo[q] * wlo) * rscale;
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const bool sym = (P.flags & kGemmSym) != 0;
-    if (T_.ksplit == 1) {
-      T* __restrict__ C = static_cast<T*>(P.C);
-      const bool readc = (P.flags & kGemmReadC) != 0;
-      for (int e0 = et; e0 < TM * TN; e0 += 8 * 128) {  // row-major over the tile: coalesced along columns
-        double cv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {  // independent loads first (8 in flight per thread)
-          const int e = e0 + u * 128, r = e / TN, c = e % TN;
-          const int gi = tm * TM + r, gj = tn * TN + c;
-          const bool live = gi < P.M && gj < P.N && !(sym && gi < gj);
-          cv[u] = (readc && live) ? (double)C[row_off[r] + col_off[c]] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int e = e0 + u * 128, r = e / TN, c = e % TN;
-          const int gi = tm * TM + r, gj = tn * TN + c;
-          if (gi >= P.M || gj >= P.N || (sym && gi < gj)) continue;
-          double val = P.alpha * (tileS[r * LDE + c] * col_scale[c]);
-          if (readc) val = fma(P.beta, cv[u], val);
-          tileS[r * LDE + c] = val;
-          C[row_off[r] + col_off[c]] = (T)val;
-        }
-      }
-      if (sym) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int e = et; e < TM * TN; e += 128) {  // mirror: coalesced along the tile's rows
-          const int c = e / TM, r = e % TM;
-          const int gi = tm * TM + r, gj = tn * TN + c;
-          if (gi >= P.M || gj >= P.N || gi <= gj) continue;
-          C[mrow_off[c] + mcol_off[r]] = (T)tileS[r * LDE + c];
-        }
-      }
-    } else {
-      double* dst = ws + T_.ws_off + (tile * T_.ksplit + split) * (int64_t)(TM * TN);
-      for (int e = et; e < TM * TN; e += 128) {
-        const int r = e / TN, c = e % TN;
-        dst[e] = tileS[r * LDE + c] * col_scale[c];
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS) : "memory");
-  }
-}
-
-// Persistent variant: one CTA per SM walks the tile list with a static stride; the stage ring runs
-// across tiles (the producer prefetches the next tile's k-steps while the current one computes) and
-// the TMEM accumulators are double-buffered (2 x 256 columns), so the FP64 epilogue of tile i
-// overlaps the MMAs of tile i + 1.  Same math, layout and epilogue semantics as k_oz_gemm.
 template <int S>
 struct OzPCfg {
+  // TMEM: one accumulator set = S diagonals x TN columns; two sets (epilogue of tile i overlaps the
+  // MMAs of tile i+1) when they fit the 512 columns, else one (the epilogue drains it first thing)
+  static constexpr uint32_t ACC_COLS = S * TN;
+  static constexpr int NBUF = 2 * ACC_COLS <= 512 ? 2 : 1;
+  static constexpr uint32_t ALLOC = NBUF * ACC_COLS <= 256 ? 256 : 512;
+  static_assert(ACC_COLS <= 512, "S x TN accumulator columns exceed TMEM");
   static constexpr int STAGE = OzCfg<S>::STAGE;
   static constexpr size_t TILE_BYTES = (size_t)TM * LDE * sizeof(double);
   static constexpr int STAGES_RAW = (int)((226 * 1024 - TILE_BYTES - 1024) / STAGE);
@@ -761,7 +541,8 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
   using Cfg = OzCfg<S>;
   using PC = OzPCfg<S>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
-  __shared__ __align__(8) uint64_t full_bar[PC::STAGES][2], empty_bar[PC::STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full_bar[PC::STAGES][2], empty_bar[PC::STAGES], tfull[PC::NBUF],
+      tempty[PC::NBUF];
   __shared__ uint32_t tmem_slot;
   __shared__ double col_scale[TN];
   __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
@@ -775,7 +556,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
       mbar_init(&full_bar[i][1], 1);
       mbar_init(&empty_bar[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < PC::NBUF; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 1);
     }
@@ -783,7 +564,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "n"(2 * Cfg::TMEM_COLS)
+                 "n"(PC::ALLOC)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -841,10 +622,10 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
       OzItem it;
       for (int64_t item = blockIdx.x; item < total_items; item += gridDim.x) {
         if (!oz_decode(probs, tps, begin, nprob, mask, item, it)) continue;
-        const uint32_t b = tcount & 1u;
-        mbar_wait(&tempty[b], ((tcount >> 1) & 1u) ^ 1u);  // the epilogue drained this buffer
+        const uint32_t b = tcount % PC::NBUF;
+        mbar_wait(&tempty[b], ((tcount / PC::NBUF) & 1u) ^ 1u);  // the epilogue drained this buffer
         tc_fence_after();
-        const uint32_t acc = tmem + b * Cfg::TMEM_COLS;
+        const uint32_t acc = tmem + b * PC::ACC_COLS;
         for (int k = 0; k < it.nk; ++k, ++g) {
           const int st = (int)(g % PC::STAGES);
           const uint32_t par = (g / PC::STAGES) & 1u;
@@ -899,10 +680,10 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
         row_off[et] = evx(P.c_r, gi);
         mcol_off[et] = evx(P.c_c, gi);
       }
-      const uint32_t b = tcount & 1u;
-      mbar_wait_sleep(&tfull[b], (tcount >> 1) & 1u);
+      const uint32_t b = tcount % PC::NBUF;
+      mbar_wait_sleep(&tfull[b], (tcount / PC::NBUF) & 1u);
       tc_fence_after();
-      const uint32_t acc = tmem + b * Cfg::TMEM_COLS;
+      const uint32_t acc = tmem + b * PC::ACC_COLS;
       const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
       constexpr int H = (S + 1) / 2;
       int32_t v[16];
@@ -976,7 +757,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * Cfg::TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(PC::ALLOC) : "memory");
   }
 }
 
@@ -1040,11 +821,8 @@ int OzakiGemmBatch<T>::set_slices(int s) {
 template <typename T, int S>
 static cudaError_t oz_set_smem_attrs() {
   static const cudaError_t e = [] {
-    cudaError_t a = cudaFuncSetAttribute(k_oz_gemm<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OzCfg<S>::SMEM);
-    cudaError_t b = cudaFuncSetAttribute(k_oz_gemm_p<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)OzPCfg<S>::SMEM);
-    return a != cudaSuccess ? a : b;
+    return cudaFuncSetAttribute(k_oz_gemm_p<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)OzPCfg<S>::SMEM);
   }();  // once per instantiation, thread-safe
   return e;
 }
@@ -1281,20 +1059,10 @@ int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
     cached_valid_ = true;
   }
   if ((rc = launch_pack(sets_[0], s, mask))) return rc;
-  static const bool persist = [] {
-    const char* e = std::getenv("SHAMPOO_OZ_PERSIST");
-    return e ? std::atoi(e) != 0 : true;  // 1.5% faster on the bench step (SHAMPOO_OZ_PERSIST=0: 2 CTAs/SM)
-  }();
-  if (persist) {
-    const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
-    OZ_DISPATCH(S_, k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(
-                        d_prob_, d_tp_, d_begin_, (int)host.size(), total_items_, mask, arena_, exps_, ws_,
-                        static_cast<const CUtensorMap*>(d_tmaps_)));
-  } else {
-    OZ_DISPATCH(S_, k_oz_gemm<T, S><<<(unsigned)total_items_, GEMM_THREADS, OzCfg<S>::SMEM, s>>>(
-                        d_prob_, d_tp_, d_begin_, (int)host.size(), mask, arena_, exps_, ws_,
-                        static_cast<const CUtensorMap*>(d_tmaps_)));
-  }
+  const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
+  OZ_DISPATCH(S_, k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(
+                      d_prob_, d_tp_, d_begin_, (int)host.size(), total_items_, mask, arena_, exps_, ws_,
+                      static_cast<const CUtensorMap*>(d_tmaps_)));
   SH_LAUNCH_CHECK();
   if (total_red_ > 0) {
     k_oz_reduce<T><<<(unsigned)total_red_, 256, 0, s>>>(d_prob_, d_tp_, d_rbegin_, d_rprob_, nred_, mask, ws_);
