@@ -120,106 +120,169 @@ __global__ void __launch_bounds__(NT) k_prepare(int pass, const Chunk* __restric
                    (!fresh || !sc.l2 || al(static_cast<const char*>(wp) + p0 * es, 2 * es)) &&
                    (!graft || al(GA + j0, 2 * sizeof(T))) && (!filt || (al(F + j0, 2 * sizeof(T)) && al(GE + j0, 2 * sizeof(T))));
   auto param_off = [&](int64_t j) { return contig ? B.cbase + j : block_to_param_offset(B, j); };
-  // gradient of elements j, j + 1 (n = 2) or j (n = 1)
+  // gradient of elements j, j + 1 (n = 2) or j (n = 1), scalar accesses
   auto load_g = [&](int64_t j, int n, T& g0, T& g1) {
     g1 = T(0);
     if (!fresh) {
-      if (n == 2 && vec) ld2<T>(G + j, g0, g1);
-      else {
-        g0 = G[j];
-        if (n == 2) g1 = G[j + 1];
-      }
+      g0 = G[j];
+      if (n == 2) g1 = G[j + 1];
       return;
     }
     if (sc.gbuf) {
-      if (n == 2 && vec) ld2<T>(gb + j, g0, g1);
-      else {
-        g0 = gb[j];
-        if (n == 2) g1 = gb[j + 1];
-      }
-      g0 = T(sc.gscale * (double)g0);
-      g1 = T(sc.gscale * (double)g1);
-    } else if (n == 2 && vec) {
-      ld2_as<T>(gp, p0 + (j - j0), sc.pdtype, g0, g1);
+      g0 = T(sc.gscale * (double)gb[j]);
+      if (n == 2) g1 = T(sc.gscale * (double)gb[j + 1]);
     } else {
       g0 = load_as<T>(gp, param_off(j), sc.pdtype);
       if (n == 2) g1 = load_as<T>(gp, param_off(j + 1), sc.pdtype);
     }
     if (sc.l2) {
-      T w0, w1 = T(0);
-      if (n == 2 && vec) ld2_as<T>(wp, p0 + (j - j0), sc.pdtype, w0, w1);
-      else {
-        w0 = load_as<T>(wp, param_off(j), sc.pdtype);
-        if (n == 2) w1 = load_as<T>(wp, param_off(j + 1), sc.pdtype);
-      }
-      g0 += T(sc.weight_decay) * w0;
-      g1 += T(sc.weight_decay) * w1;
-    }
-  };
-  auto ldp = [&](const T* a, int64_t j, int n, T& x0, T& x1) {
-    if (n == 2 && vec) ld2<T>(a + j, x0, x1);
-    else {
-      x0 = a[j];
-      x1 = n == 2 ? a[j + 1] : T(0);
-    }
-  };
-  auto stp = [&](T* a, int64_t j, int n, T x0, T x1) {
-    if (n == 2 && vec) st2<T>(a + j, x0, x1);
-    else {
-      a[j] = x0;
-      if (n == 2) a[j + 1] = x1;
+      g0 += T(sc.weight_decay) * load_as<T>(wp, param_off(j), sc.pdtype);
+      if (n == 2) g1 += T(sc.weight_decay) * load_as<T>(wp, param_off(j + 1), sc.pdtype);
     }
   };
   double acc = 0.0;
+  // the math of one pair (n = 2) or of the odd tail (n = 1), in element order
+  auto pair_math = [&](int64_t j, int n, T (&g)[2], T (&a)[2], T (&f)[2], bool vstore) {
+    auto stp = [&](T* arr, T x0, T x1) {
+      if (vstore) st2<T>(arr + j, x0, x1);
+      else {
+        arr[j] = x0;
+        if (n == 2) arr[j + 1] = x1;
+      }
+    };
+    if (fresh) stp(G, g[0], g[1]);
+    if (pass == 0) {
+      for (int h = 0; h < n; ++h) acc += (double)g[h] * (double)g[h];
+      return;
+    }
+    T ge[2] = {g[0], g[1]};
+    if (graft) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const T gg = normalized ? T((double)g[h] * inv_norm) : g[h];
+        const T sq = gg * gg;
+        a[h] = graft_summed(sc.graft) ? a[h] + sq : T(sc.beta2g) * a[h] + T(sc.one_minus_beta2g) * sq;
+      }
+      stp(GA, a[0], a[1]);
+    }
+    if (filt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        f[h] = T(sc.beta1) * f[h] + T(sc.one_minus_beta1) * g[h];
+        ge[h] = f[h] * T(sc.inv_bc1);
+      }
+      stp(F, f[0], f[1]);
+      stp(GE, ge[0], ge[1]);
+    }
+    for (int h = 0; h < n; ++h) {
+      const T pg = graft_dir<T>(sc.graft, ge[h], a[h], sc.inv_bc2g, sc.graft_eps);
+      acc += (double)pg * (double)pg;
+    }
+  };
   const int64_t npair = (c.count + 1) >> 1;
   constexpr int U2 = 2;  // pairs per thread per iteration: all loads of the batch before its stores
-  for (int64_t q0 = threadIdx.x; q0 < npair; q0 += U2 * NT) {
-    T g[U2][2], a[U2][2], f[U2][2];
+  if (vec) {
+    const int64_t nfull = c.count >> 1;
+    for (int64_t q0 = threadIdx.x; q0 < nfull; q0 += U2 * NT) {
+      T g[U2][2], a[U2][2], f[U2][2];
 #pragma unroll
-    for (int u = 0; u < U2; ++u) {
-      const int64_t q = q0 + (int64_t)u * NT;
-      g[u][0] = g[u][1] = a[u][0] = a[u][1] = f[u][0] = f[u][1] = T(0);
-      if (q >= npair) continue;
-      const int64_t j = j0 + 2 * q;
-      const int n = (2 * q + 1 < c.count) ? 2 : 1;
-      load_g(j, n, g[u][0], g[u][1]);
-      if (graft) ldp(GA, j, n, a[u][0], a[u][1]);
-      if (filt) ldp(F, j, n, f[u][0], f[u][1]);
+      for (int u = 0; u < U2; ++u) {
+        const int64_t q = q0 + (int64_t)u * NT;
+        g[u][0] = g[u][1] = a[u][0] = a[u][1] = f[u][0] = f[u][1] = T(0);
+        if (q >= nfull) continue;
+        const int64_t j = j0 + 2 * q;
+        if (!fresh) {
+          ld2<T>(G + j, g[u][0], g[u][1]);
+        } else {
+          if (sc.gbuf) {
+            ld2<T>(gb + j, g[u][0], g[u][1]);
+            g[u][0] = T(sc.gscale * (double)g[u][0]);
+            g[u][1] = T(sc.gscale * (double)g[u][1]);
+          } else {
+            ld2_as<T>(gp, p0 + 2 * q, sc.pdtype, g[u][0], g[u][1]);
+          }
+          if (sc.l2) {
+            T w0, w1;
+            ld2_as<T>(wp, p0 + 2 * q, sc.pdtype, w0, w1);
+            g[u][0] += T(sc.weight_decay) * w0;
+            g[u][1] += T(sc.weight_decay) * w1;
+          }
+        }
+        if (graft) ld2<T>(GA + j, a[u][0], a[u][1]);
+        if (filt) ld2<T>(F + j, f[u][0], f[u][1]);
+      }
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {  // pair_math inlined by hand (16-byte stores)
+        const int64_t q = q0 + (int64_t)u * NT;
+        if (q >= nfull) continue;
+        const int64_t j = j0 + 2 * q;
+        if (fresh) st2<T>(G + j, g[u][0], g[u][1]);
+        if (pass == 0) {
+          acc += (double)g[u][0] * (double)g[u][0];
+          acc += (double)g[u][1] * (double)g[u][1];
+          continue;
+        }
+        T ge0 = g[u][0], ge1 = g[u][1];
+        if (graft) {
+          const T g0 = normalized ? T((double)g[u][0] * inv_norm) : g[u][0];
+          const T g1 = normalized ? T((double)g[u][1] * inv_norm) : g[u][1];
+          const T s0 = g0 * g0, s1 = g1 * g1;
+          if (graft_summed(sc.graft)) {
+            a[u][0] += s0;
+            a[u][1] += s1;
+          } else {
+            a[u][0] = T(sc.beta2g) * a[u][0] + T(sc.one_minus_beta2g) * s0;
+            a[u][1] = T(sc.beta2g) * a[u][1] + T(sc.one_minus_beta2g) * s1;
+          }
+          st2<T>(GA + j, a[u][0], a[u][1]);
+        }
+        if (filt) {
+          f[u][0] = T(sc.beta1) * f[u][0] + T(sc.one_minus_beta1) * g[u][0];
+          f[u][1] = T(sc.beta1) * f[u][1] + T(sc.one_minus_beta1) * g[u][1];
+          ge0 = f[u][0] * T(sc.inv_bc1);
+          ge1 = f[u][1] * T(sc.inv_bc1);
+          st2<T>(F + j, f[u][0], f[u][1]);
+          st2<T>(GE + j, ge0, ge1);
+        }
+        const T pg0 = graft_dir<T>(sc.graft, ge0, a[u][0], sc.inv_bc2g, sc.graft_eps);
+        const T pg1 = graft_dir<T>(sc.graft, ge1, a[u][1], sc.inv_bc2g, sc.graft_eps);
+        acc += (double)pg0 * (double)pg0;
+        acc += (double)pg1 * (double)pg1;
+      }
     }
+    // the odd tail is pair npair - 1: its thread's last pair, as in the scalar order below
+    if ((c.count & 1) && threadIdx.x == (int)((npair - 1) % NT)) {
+      const int64_t j = j0 + c.count - 1;
+      T g[2], a[2] = {T(0), T(0)}, f[2] = {T(0), T(0)};
+      load_g(j, 1, g[0], g[1]);
+      if (graft) a[0] = GA[j];
+      if (filt) f[0] = F[j];
+      pair_math(j, 1, g, a, f, false);
+    }
+  } else {
+    for (int64_t q0 = threadIdx.x; q0 < npair; q0 += U2 * NT) {
+      T g[U2][2], a[U2][2], f[U2][2];
 #pragma unroll
-    for (int u = 0; u < U2; ++u) {
-      const int64_t q = q0 + (int64_t)u * NT;
-      if (q >= npair) continue;
-      const int64_t j = j0 + 2 * q;
-      const int n = (2 * q + 1 < c.count) ? 2 : 1;
-      if (fresh) stp(G, j, n, g[u][0], g[u][1]);
-      if (pass == 0) {
-        acc += (double)g[u][0] * (double)g[u][0];
-        if (n == 2) acc += (double)g[u][1] * (double)g[u][1];
-        continue;
-      }
-      T ge[2] = {g[u][0], g[u][1]};
-      if (graft) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const T gg = normalized ? T((double)g[u][h] * inv_norm) : g[u][h];
-          const T sq = gg * gg;
-          a[u][h] = graft_summed(sc.graft) ? a[u][h] + sq : T(sc.beta2g) * a[u][h] + T(sc.one_minus_beta2g) * sq;
+      for (int u = 0; u < U2; ++u) {
+        const int64_t q = q0 + (int64_t)u * NT;
+        g[u][0] = g[u][1] = a[u][0] = a[u][1] = f[u][0] = f[u][1] = T(0);
+        if (q >= npair) continue;
+        const int64_t j = j0 + 2 * q;
+        const int n = (2 * q + 1 < c.count) ? 2 : 1;
+        load_g(j, n, g[u][0], g[u][1]);
+        if (graft) {
+          a[u][0] = GA[j];
+          if (n == 2) a[u][1] = GA[j + 1];
         }
-        stp(GA, j, n, a[u][0], a[u][1]);
-      }
-      if (filt) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          f[u][h] = T(sc.beta1) * f[u][h] + T(sc.one_minus_beta1) * g[u][h];
-          ge[h] = f[u][h] * T(sc.inv_bc1);
+        if (filt) {
+          f[u][0] = F[j];
+          if (n == 2) f[u][1] = F[j + 1];
         }
-        stp(F, j, n, f[u][0], f[u][1]);
-        stp(GE, j, n, ge[0], ge[1]);
       }
-      for (int h = 0; h < n; ++h) {
-        const T pg = graft_dir<T>(sc.graft, ge[h], a[u][h], sc.inv_bc2g, sc.graft_eps);
-        acc += (double)pg * (double)pg;
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int64_t q = q0 + (int64_t)u * NT;
+        if (q < npair) pair_math(j0 + 2 * q, (2 * q + 1 < c.count) ? 2 : 1, g[u], a[u], f[u], false);
       }
     }
   }

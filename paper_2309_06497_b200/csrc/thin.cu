@@ -151,67 +151,84 @@ __global__ void __launch_bounds__(256) k_thin_rank1(const GemmProblem* __restric
   }
 }
 
-// Small M and N (<= 8), any K: CTA per (problem, 4096-wide k chunk) -> FP64 partials.
-template <typename T>
+// Small M and N (<= TB <= 8), any K: CTA per (problem, 4096-wide k chunk) -> FP64 partials (layout
+// TMAX x TMAX per chunk).  TB = 4 for the 3 x 3 kernel modes: 16 accumulators instead of 64 (the
+// 8 x 8 variant ran at one CTA per SM on its 187 registers).
+template <typename T, int TB>
 __global__ void __launch_bounds__(256) k_thin_kred(const GemmProblem* __restrict__ probs,
                                                    const int64_t* __restrict__ begin, int nprob,
                                                    const int32_t* __restrict__ mask, const int64_t* __restrict__ woff,
                                                    double* __restrict__ ws) {
-  __shared__ double red[TMAX * TMAX][8];
+  __shared__ double red[TB * TB][8];
   const int p = find64(begin, nprob, blockIdx.x);
   const GemmProblem& P = probs[p];
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   const int chunk = (int)(blockIdx.x - begin[p]);
   const T* __restrict__ A = static_cast<const T*>(P.A);
   const T* __restrict__ B = static_cast<const T*>(P.B);
-  double acc[TMAX][TMAX];
+  double acc[TB][TB];
 #pragma unroll
-  for (int i = 0; i < TMAX; ++i)
+  for (int i = 0; i < TB; ++i)
 #pragma unroll
-    for (int j = 0; j < TMAX; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < TB; ++j) acc[i][j] = 0.0;
   const int k0 = chunk * KRED_CHUNK, k1 = min(P.K, k0 + KRED_CHUNK);
+  int64_t ar[TB], br[TB];
+#pragma unroll
+  for (int i = 0; i < TB; ++i) {
+    ar[i] = i < P.M ? ev(P.a_r, i) : 0;
+    br[i] = i < P.N ? ev(P.b_r, i) : 0;
+  }
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-    double a[TMAX], b[TMAX];
+    double a[TB], b[TB];
     const int64_t ak = ev(P.a_k, k), bk = ev(P.b_k, k);
 #pragma unroll
-    for (int i = 0; i < TMAX; ++i) {
-      a[i] = i < P.M ? (double)A[ev(P.a_r, i) + ak] : 0.0;
-      b[i] = i < P.N ? (double)B[ev(P.b_r, i) + bk] : 0.0;
+    for (int i = 0; i < TB; ++i) {
+      a[i] = i < P.M ? (double)A[ar[i] + ak] : 0.0;
+      b[i] = i < P.N ? (double)B[br[i] + bk] : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < TMAX; ++i)
+    for (int i = 0; i < TB; ++i)
 #pragma unroll
-      for (int j = 0; j < TMAX; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int j = 0; j < TB; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
   }
   const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
 #pragma unroll
-  for (int i = 0; i < TMAX; ++i)
+  for (int i = 0; i < TB; ++i)
 #pragma unroll
-    for (int j = 0; j < TMAX; ++j) {
+    for (int j = 0; j < TB; ++j) {
       const double v = warp_sum(acc[i][j]);
-      if (ln == 0) red[i * TMAX + j][w] = v;
+      if (ln == 0) red[i * TB + j][w] = v;
     }
   __syncthreads();
   if (threadIdx.x < TMAX * TMAX) {
+    const int i = threadIdx.x / TMAX, j = threadIdx.x % TMAX;
     double v = 0.0;
-    for (int q = 0; q < 8; ++q) v += red[threadIdx.x][q];
+    if (i < TB && j < TB)
+      for (int q = 0; q < 8; ++q) v += red[i * TB + j][q];
     ws[woff[p] + (int64_t)chunk * TMAX * TMAX + threadIdx.x] = v;
   }
 }
 
+// Chunk partials -> C: a warp per output element, lanes over the chunks (fixed order), then a
+// fixed-shape warp tree (deterministic).
 template <typename T>
-__global__ void k_thin_kred_final(const GemmProblem* __restrict__ probs, int nprob, const int32_t* __restrict__ mask,
-                                  const int64_t* __restrict__ woff, const int32_t* __restrict__ nchunks,
-                                  const double* __restrict__ ws) {
+__global__ void __launch_bounds__(256) k_thin_kred_final(const GemmProblem* __restrict__ probs, int nprob,
+                                                         const int32_t* __restrict__ mask,
+                                                         const int64_t* __restrict__ woff,
+                                                         const int32_t* __restrict__ nchunks,
+                                                         const double* __restrict__ ws) {
   const int p = blockIdx.x;
   const GemmProblem& P = probs[p];
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
-  const int e = threadIdx.x;
-  const int i = e / TMAX, j = e % TMAX;
-  if (i >= P.M || j >= P.N) return;
-  double acc = 0.0;
-  for (int c = 0; c < nchunks[p]; ++c) acc += ws[woff[p] + (int64_t)c * TMAX * TMAX + e];
-  thin_store<T>(P, i, j, acc);
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int e = w; e < TMAX * TMAX; e += 8) {
+    const int i = e / TMAX, j = e % TMAX;
+    if (i >= P.M || j >= P.N) continue;
+    double acc = 0.0;
+    for (int c = ln; c < nchunks[p]; c += 32) acc += ws[woff[p] + (int64_t)c * TMAX * TMAX + e];
+    acc = warp_sum(acc);
+    if (ln == 0) thin_store<T>(P, i, j, acc);
+  }
 }
 
 }  // namespace
@@ -232,6 +249,7 @@ ThinGemmBatch<T>::~ThinGemmBatch() {
   dev_free(d_obegin_);
   dev_free(d_red_);
   dev_free(d_rbegin_);
+  dev_free(d_rbegin8_);
   dev_free(d_woff_);
   dev_free(d_nch_);
   dev_free(ws_);
@@ -240,7 +258,15 @@ ThinGemmBatch<T>::~ThinGemmBatch() {
 template <typename T>
 int ThinGemmBatch<T>::upload() {
   std::vector<GemmProblem> outp, redp, r1p;
-  for (const auto& p : host) (is_rank1(p) ? r1p : p.K <= 32 ? outp : redp).push_back(p);
+  std::vector<GemmProblem> red8;
+  for (const auto& p : host) {
+    if (is_rank1(p)) r1p.push_back(p);
+    else if (p.K <= 32) outp.push_back(p);
+    else if (p.M <= 4 && p.N <= 4) redp.push_back(p);
+    else red8.push_back(p);
+  }
+  n_red4_ = (int)redp.size();
+  redp.insert(redp.end(), red8.begin(), red8.end());
   std::vector<int64_t> r1b;
   n_r1_ctas_ = 0;
   for (const auto& p : r1p) {
@@ -264,15 +290,19 @@ int ThinGemmBatch<T>::upload() {
     n_out_items_ += (int64_t)((p.M + R - 1) / R) * nchunk;
   }
   n_red_ctas_ = 0;
+  n_red4_ctas_ = 0;
   int64_t wsz = 0;
-  for (const auto& p : redp) {
+  for (size_t q = 0; q < redp.size(); ++q) {
+    const GemmProblem& p = redp[q];
     const int c = std::max(1, (p.K + KRED_CHUNK - 1) / KRED_CHUNK);
+    if ((int)q == n_red4_) n_red4_ctas_ = n_red_ctas_;
     rb.push_back(n_red_ctas_);
     wo.push_back(wsz);
     nch.push_back(c);
     n_red_ctas_ += c;
     wsz += (int64_t)c * TMAX * TMAX;
   }
+  if (n_red4_ == (int)redp.size()) n_red4_ctas_ = n_red_ctas_;
   n_out_ = (int)outp.size();
   n_red_ = (int)redp.size();
   if (n_out_) {
@@ -289,6 +319,12 @@ int ThinGemmBatch<T>::upload() {
     SH_CUDA_CHECK(dev_malloc(&ws_, wsz * sizeof(double)));
     SH_CUDA_CHECK(cudaMemcpy(d_red_, redp.data(), redp.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_rbegin_, rb.data(), rb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (n_red_ > n_red4_) {  // CTA prefix of the M/N <= 8 problems, relative to their own launch
+      std::vector<int64_t> rb8(rb.begin() + n_red4_, rb.end());
+      for (auto& x : rb8) x -= n_red4_ctas_;
+      SH_CUDA_CHECK(dev_malloc(&d_rbegin8_, rb8.size() * sizeof(int64_t)));
+      SH_CUDA_CHECK(cudaMemcpy(d_rbegin8_, rb8.data(), rb8.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
     SH_CUDA_CHECK(cudaMemcpy(d_woff_, wo.data(), wo.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(cudaMemcpy(d_nch_, nch.data(), nch.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
@@ -306,9 +342,17 @@ int ThinGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
     SH_LAUNCH_CHECK();
   }
   if (n_red_) {
-    k_thin_kred<T><<<(unsigned)n_red_ctas_, 256, 0, s>>>(d_red_, d_rbegin_, n_red_, mask, d_woff_, ws_);
-    SH_LAUNCH_CHECK();
-    k_thin_kred_final<T><<<n_red_, TMAX * TMAX, 0, s>>>(d_red_, n_red_, mask, d_woff_, d_nch_, ws_);
+    // problems [0, n_red4_) have M, N <= 4 (CTAs [0, n_red4_ctas_)); the rest up to 8
+    if (n_red4_) {
+      k_thin_kred<T, 4><<<(unsigned)n_red4_ctas_, 256, 0, s>>>(d_red_, d_rbegin_, n_red4_, mask, d_woff_, ws_);
+      SH_LAUNCH_CHECK();
+    }
+    if (n_red_ > n_red4_) {
+      k_thin_kred<T, TMAX><<<(unsigned)(n_red_ctas_ - n_red4_ctas_), 256, 0, s>>>(
+          d_red_ + n_red4_, d_rbegin8_, n_red_ - n_red4_, mask, d_woff_ + n_red4_, ws_);
+      SH_LAUNCH_CHECK();
+    }
+    k_thin_kred_final<T><<<n_red_, 256, 0, s>>>(d_red_, n_red_, mask, d_woff_, d_nch_, ws_);
     SH_LAUNCH_CHECK();
   }
   return SHAMPOO_OK;

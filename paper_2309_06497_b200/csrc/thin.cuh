@@ -37,11 +37,13 @@ class ThinGemmBatch {
   int64_t* d_obegin_ = nullptr;
   GemmProblem* d_red_ = nullptr;
   int64_t* d_rbegin_ = nullptr;
+  int64_t* d_rbegin8_ = nullptr;  // CTA prefix of the M, N <= 8 reduction problems (after the <= 4 ones)
   int64_t* d_woff_ = nullptr;
   int32_t* d_nch_ = nullptr;
   double* ws_ = nullptr;
   int64_t n_out_items_ = 0, n_red_ctas_ = 0;
-  int n_out_ = 0, n_red_ = 0;
+  int n_out_ = 0, n_red_ = 0, n_red4_ = 0;
+  int64_t n_red4_ctas_ = 0;
 };
 
 }  // namespace shampoo
