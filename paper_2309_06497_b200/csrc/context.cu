@@ -45,6 +45,11 @@ template <typename T>
 struct Engine : EngineBase {
   // tcgen05 int8 tensor cores, Ozaki split (exact accumulation; 8 slices for double, 5 for single)
   OzakiGemmBatch<T> stats;             // factor EMA updates, all owned blocks x modes
+  // plain steps: the statistics and the first mode product in ONE launch -- for order-2 blocks the
+  // Gram of G's columns and the product L^(-1/4) G read the same operand, packed once.  Mask word 0
+  // = the step's go word (statistics), 1 + l = inverse of owned block l present (mode product)
+  OzakiGemmBatch<T> stats_prec;
+  bool merged = false;
   OzakiGemmBatch<T> prec[kMaxOrder];   // mode-k products, k = 0..order-1 (order >= 2)
   // problems too thin for a 128 x 64 tensor-core tile (rank-1 factor updates of vector blocks,
   // 3 x 3 / 7 x 7 kernel modes): HBM-bound CUDA-core kernels, exact products, FP64 sums
@@ -53,6 +58,7 @@ struct Engine : EngineBase {
   GemvBatch<T> prec1;                  // order-1 blocks: P = X g
   void inverses_changed() override {
     for (auto& b : prec) b.invalidate_cached();
+    stats_prec.invalidate_cached();
   }
 };
 
@@ -141,7 +147,9 @@ struct shampoo_ctx {
   void *G = nullptr, *GE = nullptr, *FILT = nullptr, *GA = nullptr, *MOM = nullptr, *PS = nullptr;
   void *T1 = nullptr, *T2 = nullptr, *FACT = nullptr, *INV = nullptr, *BUF = nullptr;
   double *part = nullptr, *gnorm2 = nullptr, *pg2 = nullptr, *ps2 = nullptr;
-  int32_t* d_ready = nullptr;
+  int32_t* d_ready = nullptr;      // = d_gomask + 1
+  int32_t* d_gomask = nullptr;     // [go word | ready per owned block]
+  bool prec0_done = false;         // this step's first mode products ran with the statistics
   int32_t *d_cb = nullptr, *d_cc = nullptr;
   // tables
   DevBlock* d_blocks = nullptr;
@@ -351,6 +359,7 @@ int build_engine(shampoo_ctx* c) {
       if (rc) return rc;
     }
   }
+  std::vector<GemmProblem> prec0;  // first mode products, for the merged plain-step launch
   for (size_t l = 0; l < c->owned.size(); ++l) {
     const BlockPlan& b = c->plan.blocks[c->owned[l]];
     if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
@@ -385,9 +394,24 @@ int build_engine(shampoo_ctx* c) {
         p.mask_index = (int32_t)l;
         if (thin(p)) e->prec_thin[m].add(p);
         else e->prec[m].add(p);
+        if (m == 0 && !thin(p)) {
+          p.mask_index = 1 + (int32_t)l;  // d_gomask layout
+          prec0.push_back(p);
+        }
       }
       off += d[m] * d[m];
     }
+  }
+  // merged plain-step launch: statistics first (their masks govern the shared packs: a skipped step
+  // skips them, and its mode products are discarded with it), then the first mode products
+  e->merged = !e->stats.empty() && !prec0.empty() && e->stats.slices() == e->prec[0].slices();
+  if (e->merged) {
+    for (const GemmProblem& g : e->stats.host) e->stats_prec.add(g);
+    for (const GemmProblem& g : prec0) e->stats_prec.add(g);
+    e->stats_prec.set_share_packs(true);
+    int rc = e->stats_prec.set_slices(e->stats.slices());
+    if (rc) return rc;
+    if ((rc = e->stats_prec.upload())) return rc;
   }
   int rc = e->stats.upload();
   if (rc) return rc;
@@ -405,9 +429,10 @@ int precondition_impl(shampoo_ctx* c, cudaStream_t s) {
   int rc;
   if ((rc = e.prec1.launch(s, c->d_ready))) return rc;
   for (int m = 0; m < kMaxOrder; ++m) {
-    if ((rc = e.prec[m].launch(s, c->d_ready))) return rc;
+    if (!(m == 0 && c->prec0_done) && (rc = e.prec[m].launch(s, c->d_ready))) return rc;
     if ((rc = e.prec_thin[m].launch(s, c->d_ready))) return rc;
   }
+  c->prec0_done = false;
   if ((rc = launch_sumsq<T>(c->d_owned_chunks, c->n_owned_chunks, c->d_blocks, c->PS, c->part, s))) return rc;
   return launch_block_reduce(c->d_cb, c->d_cc, (int)c->owned.size(), c->part, c->ps2, s);
 }
@@ -575,11 +600,10 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
       {(void**)&c->gnorm2, std::max<size_t>(no, 1) * 8},
       {(void**)&c->pg2, std::max<size_t>(no, 1) * 8},
       {(void**)&c->ps2, std::max<size_t>(no, 1) * 8},
-      {(void**)&c->d_ready, std::max<size_t>(no, 1) * 4},
+      {(void**)&c->d_gomask, (1 + std::max<size_t>(no, 1)) * 4},
       {(void**)&c->d_cb, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_cc, std::max<size_t>(no, 1) * 4},
       {(void**)&c->d_flag, 16},
-      {(void**)&c->d_go, 16},
       {&c->FB, (size_t)c->n_fb * es},
       {(void**)&c->dsum, (size_t)c->n_fb * 8},
       {(void**)&c->dscale, (size_t)c->n_fb * 8},
@@ -597,6 +621,12 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
   for (auto& s : slots) {
     *s.p = s.bytes ? (void*)(c->arena + at) : nullptr;
     at += align_up(s.bytes);
+  }
+  c->d_go = c->d_gomask;  // 1 outside a predicated step (the merged statistics launch reads it)
+  c->d_ready = c->d_gomask + 1;
+  {
+    const int32_t one = 1;
+    SH_CUDA_CHECK(cudaMemcpy(c->d_go, &one, sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   SH_CUDA_CHECK(cudaMalloc(&c->d_blocks, std::max(nb, 1) * sizeof(DevBlock)));
   SH_CUDA_CHECK(cudaMalloc(&c->d_params, std::max(c->nparams, 1) * sizeof(DevBlock)));
@@ -753,9 +783,13 @@ int shampoo_check_finite_resolve(shampoo_ctx* c, int32_t* aborted) {
   c->deferred_pending = false;
   SH_CUDA_CHECK(cudaEventSynchronize(c->ev_check));
   if (!*(volatile int32_t*)c->h_flag) return SHAMPOO_OK;
-  // the predicated step wrote no device state; undo its host-side counters
+  // the predicated step wrote no device state; undo its host-side counters and re-arm the go word
   c->graft_step = c->saved_graft_step;
   c->step = c->saved_step;
+  {
+    const int32_t one = 1;
+    SH_CUDA_CHECK(cudaMemcpy(c->d_go, &one, sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   if (aborted) *aborted = 1;
   set_error("gradient contains non-finite entries; step aborted (deferred check)");
   return SHAMPOO_ERR_NONFINITE_GRAD;
@@ -812,11 +846,19 @@ int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf
   }
   // statistics problems are masked on word 0 of the go pointer (deferred check; null: unconditional)
   const int32_t* go = c->go_armed ? c->d_go : nullptr;
-  rc = c->f32 ? c->eng<float>().stats.launch(ss, go) : c->eng<double>().stats.launch(ss, go);
+  const bool merged = c->f32 ? c->eng<float>().merged : c->eng<double>().merged;
+  c->prec0_done = merged && sc.precond && !refresh_step(c, t);
+  if (c->prec0_done) {
+    // plain step: statistics + first mode products in one launch on the caller's stream (shared packs)
+    rc = c->f32 ? c->eng<float>().stats_prec.launch(s, c->d_gomask) : c->eng<double>().stats_prec.launch(s, c->d_gomask);
+    ss = s;
+  } else {
+    rc = c->f32 ? c->eng<float>().stats.launch(ss, go) : c->eng<double>().stats.launch(ss, go);
+  }
   if (rc) return rc;
   rc = c->f32 ? c->eng<float>().stats_thin.launch(ss, go) : c->eng<double>().stats_thin.launch(ss, go);
   if (rc) return rc;
-  if (concurrent) {
+  if (concurrent && ss != s) {
     SH_CUDA_CHECK(cudaEventRecord(c->ev_stats, ss));
     c->stats_pending = true;
   }

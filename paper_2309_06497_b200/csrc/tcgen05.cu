@@ -4,6 +4,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <map>
+#include <tuple>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -865,8 +868,29 @@ int OzakiGemmBatch<T>::upload() {
   mma_count_ = 0;
   for (auto& ps : sets_) ps = PackSet{};
   // exponent offsets are relative to the set; fixed up once both sets are sized
+  // share_packs_: problems reading the same operand (same source, geometry, set) share one pack; the
+  // first registered problem's mask governs it (the caller orders the problems so that it does)
+  struct PackKey {
+    int set;
+    const void* src;
+    int64_t r0, r1, r2, k0, k1, k2;
+    int rows, K, ks;
+    bool operator<(const PackKey& o) const {
+      return std::tie(set, src, r0, r1, r2, k0, k1, k2, rows, K, ks) <
+             std::tie(o.set, o.src, o.r0, o.r1, o.r2, o.k0, o.k1, o.k2, o.rows, o.K, o.ks);
+    }
+  };
+  std::map<PackKey, std::tuple<int64_t, int32_t, int64_t>> packed;
   auto add_pack = [&](int set, const void* src, Idx2 r, Idx2 k, int rows, int K, int ks, int mask_index,
                       int64_t& off, int32_t& rc, int64_t& exp) {
+    const PackKey key{set, src, r.div, r.hi, r.lo, k.div, k.hi, k.lo, rows, K, ks};
+    if (share_packs_) {
+      const auto it = packed.find(key);
+      if (it != packed.end()) {
+        std::tie(off, rc, exp) = it->second;
+        return;
+      }
+    }
     rc = std::max(1, (rows + 7) / 8);
     off = arena;
     arena += (int64_t)ks * rc * S * 256;
@@ -896,6 +920,7 @@ int OzakiGemmBatch<T>::upload() {
     ps.core_ctas += (rc + PACK_CORES - 1) / PACK_CORES;
     if (!(k.div == 0x7fffffff && k.lo == 1)) ps.all_contig = false;
     jobs[set].push_back(J);
+    if (share_packs_) packed[key] = std::make_tuple(off, rc, exp);
   };
   for (size_t i = 0; i < host.size(); ++i) {
     GemmProblem& p = host[i];

@@ -93,6 +93,9 @@ class OzakiGemmBatch {
     ext_arena_ = p;
     ext_cap_ = cap;
   }
+  // before upload(): problems that read the same operand (source, geometry) share one pack; the
+  // first such problem's mask decides whether the pack runs
+  void set_share_packs(bool on) { share_packs_ = on; }
   double flops() const;      // algorithmic 2*M*N*K (SYM counted as full)
   double int8_ops() const;   // executed tensor-core int8 ops
 
@@ -125,6 +128,7 @@ class OzakiGemmBatch {
   int nred_ = 0;
   double mma_count_ = 0;
   int S_ = kDefaultSlices;
+  bool share_packs_ = false;
 };
 
 }  // namespace shampoo
