@@ -1295,7 +1295,6 @@ RootInverseBatch::~RootInverseBatch() {
   dev_free(d_newton_);
   dev_free(d_resbits_);
   dev_free(d_improved_);
-  dev_free(d_mask2_);
   dev_free(d_part_);
   dev_free(pack_arena_);
   dev_free(d_pair_begin_);
@@ -1378,7 +1377,8 @@ int RootInverseBatch::setup(const std::vector<int32_t>& n, const std::vector<int
   SH_CUDA_CHECK(dev_malloc(&d_item_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(dev_malloc(&d_elem_begin_, nj * sizeof(int32_t)));
   SH_CUDA_CHECK(dev_malloc(&d_col_begin_, nj * sizeof(int32_t)));
-  SH_CUDA_CHECK(dev_malloc(&d_count_, 4 * sizeof(int32_t) + nj * sizeof(int32_t)));
+  // [4 counters | mask (nj) | mask2 (nj)]: the Newton X-and-T^2 launch indexes both masks from one base
+  SH_CUDA_CHECK(dev_malloc(&d_count_, 4 * sizeof(int32_t) + 2 * (size_t)nj * sizeof(int32_t)));
   SH_CUDA_CHECK(dev_malloc(&d_stats_, 4 * sizeof(int64_t)));
   SH_CUDA_CHECK(cudaMemcpy(d_pair_begin_, pbeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
   SH_CUDA_CHECK(cudaMemcpy(d_item_begin_, ibeg.data(), nj * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1567,7 +1567,7 @@ int RootInverseBatch::build_newton() {
   SH_CUDA_CHECK(dev_malloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(cudaMemset(d_resbits_, 0, std::max(nj, 1) * sizeof(unsigned long long)));
   SH_CUDA_CHECK(dev_malloc(&d_improved_, std::max(nj, 1) * sizeof(int32_t)));
-  SH_CUDA_CHECK(dev_malloc(&d_mask2_, std::max(nj, 1) * sizeof(int32_t)));
+  d_mask2_ = d_count_ + 4 + nj;
   SH_CUDA_CHECK(dev_malloc(&d_part_, std::max(total_elem_chunks_, 1) * sizeof(double)));
   SH_CUDA_CHECK(cudaMemcpy(d_newton_, hn.data(), nj * sizeof(NewtonJob), cudaMemcpyHostToDevice));
   // GEMM sets for cur = 0/1: X_nxt = X_cur T ; T^p ; M_nxt = T^p M_cur (tcgen05 Ozaki, FP64 class)
@@ -1576,8 +1576,9 @@ int RootInverseBatch::build_newton() {
     int fb;
     nsteps = std::max(nsteps, power_plan(host_[j].root_p, &fb).size());
   }
+  // the first power step (T T) runs in the X <- X T launch: both read T, packed once (share_packs)
   newton_pow_.clear();
-  for (size_t q = 0; q < nsteps; ++q) {
+  for (size_t q = 1; q < nsteps; ++q) {
     newton_pow_.emplace_back(new OzakiGemmBatch<double>());
     newton_pow_.back()->set_external_arena(pack_arena_, pack_cap_);
   }
@@ -1601,12 +1602,20 @@ int RootInverseBatch::build_newton() {
       newton_x_[c].add(sym_gemm(buf(c), buf(kNT), buf(c ^ 1)));
       newton_m_[c].add(sym_gemm(buf(fb), buf(2 + c), buf(2 + (c ^ 1))));
     }
-    for (size_t q = 0; q < plan.size(); ++q)
-      newton_pow_[q]->add(sym_gemm(buf(plan[q].lhs), buf(plan[q].rhs), buf(plan[q].dst)));
+    for (size_t q = 0; q < plan.size(); ++q) {
+      GemmProblem g = sym_gemm(buf(plan[q].lhs), buf(plan[q].rhs), buf(plan[q].dst));
+      if (q == 0) {  // T T with the X update: mask2 sits nj words after mask
+        g.mask_index = nj + j;
+        for (int c = 0; c < 2; ++c) newton_x_[c].add(g);
+      } else {
+        newton_pow_[q - 1]->add(g);
+      }
+    }
     newton_sq_.add(sym_gemm(buf(2), buf(2), buf(kNT)));  // (A + eps I)^2 (SYRK: one shared pack)
   }
   int rc;
   for (int c = 0; c < 2; ++c) {
+    newton_x_[c].set_share_packs(true);  // X T's B operand and T T's A = B: one pack of T
     if ((rc = newton_x_[c].upload())) return rc;
     if ((rc = newton_m_[c].upload())) return rc;
   }
