@@ -244,29 +244,24 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
 // `top`, the rounded last digit is `last`, the sign `neg` (applied per byte after packing).
 template <int S>
 __device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& top, uint32_t& last, uint32_t& neg) {
+  // branch-free (the elements of a warp take different shift cases; branches serialised them):
+  // yg = m 2^sh with |x| < 2^e, so sh <= 7S + G - 53 -- a left shift exists only for S >= 7, and a
+  // right shift of 63 clears any 53-bit mantissa
   constexpr int G = 7;
   const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
   const int bexp = (int)((bits >> 52) & 0x7ff);
-  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
-  if (bexp) m |= 1ull << 52;
-  const int sh = (bexp ? bexp : 1) - 1075 - e + 7 * S + G;
-  unsigned long long yg;
-  bool sticky;
-  if (sh >= 0) {
-    yg = m << sh;
-    sticky = false;
-  } else if (sh > -64) {
-    yg = m >> (-sh);
-    sticky = (m & ((1ull << (-sh)) - 1ull)) != 0ull;
-  } else {
-    yg = 0ull;
-    sticky = m != 0ull;
-  }
+  const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | ((unsigned long long)(bexp != 0) << 52);
+  const int sh = max(bexp, 1) - 1075 - e + 7 * S + G;
+  const int rs = min(max(-sh, 0), 63);
+  unsigned long long ml = m;
+  if constexpr (7 * S + G > 53) ml = m << max(sh, 0);
+  const unsigned long long yg = ml >> rs;
+  const uint32_t sticky = (ml & ((1ull << rs) - 1ull)) != 0ull;
   top = yg >> G;
-  const unsigned frac = (unsigned)(yg & ((1u << G) - 1u)), half = 1u << (G - 1);
+  const uint32_t frac = (uint32_t)yg & ((1u << G) - 1u), half = 1u << (G - 1);
   uint32_t l = (uint32_t)(top & 127ull);
-  if (frac > half || (frac == half && (sticky || (l & 1u)))) ++l;
-  last = l > 127u ? 127u : l;
+  l += (uint32_t)(frac > half) | ((uint32_t)(frac == half) & (sticky | (l & 1u)));
+  last = min(l, 127u);
   neg = (uint32_t)(bits >> 63);
 }
 
