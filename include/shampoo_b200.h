@@ -235,6 +235,12 @@ SHAMPOO_API int64_t shampoo_launch_count(void);
 /* int8 tensor-core ops executed by the tcgen05 GEMM engine since load (or the last reset), counted
  * on the device per output tile (masked-out problems are not counted).  Synchronises the device. */
 SHAMPOO_API int shampoo_tc_counter(int32_t reset, double* int8_ops);
+/* Kernel-level timing of the tensor-core GEMM launches (bench evidence): with enable = 1 every
+ * k_oz_gemm_p launch is bracketed by CUDA events on its stream and its executed int8 ops are counted,
+ * both per step phase (the SHAMPOO_NUM_PHASES indices; slot 7 = outside a phase).  Each call returns
+ * (8 entries each, any may be null) the milliseconds, int8 ops and launches accumulated since the
+ * previous call, resets them, and sets the enable state. */
+SHAMPOO_API int shampoo_gemm_timing(int32_t enable, double* ms, double* int8_ops, int64_t* launches);
 
 /* ---- state export/import: device views into the context's arena.
  * name: "factor","inv_factor","graft_accumulator","filtered_grad","momentum",

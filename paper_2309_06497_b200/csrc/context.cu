@@ -94,13 +94,15 @@ struct PhaseScope {
   int phase;
   cudaStream_t s;
   cudaEvent_t a = nullptr;
-  PhaseScope(PhaseTimer* t_, int p, cudaStream_t s_) : t(t_), phase(p), s(s_) {
+  int prev_tag;
+  PhaseScope(PhaseTimer* t_, int p, cudaStream_t s_) : t(t_), phase(p), s(s_), prev_tag(oz_set_tag(p)) {
     if (t->on) {
       a = t->get();
       cudaEventRecord(a, s);
     }
   }
   ~PhaseScope() {
+    oz_set_tag(prev_tag);
     if (t->on) {
       cudaEvent_t b = t->get();
       cudaEventRecord(b, s);
@@ -961,6 +963,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   int grc[kRootGroups] = {};
   std::string gerr[kRootGroups];
   auto solve = [&](int g, cudaStream_t st) {
+    oz_set_tag(1);  // root-inverse phase (worker threads too)
     if (c->rinv[g].jobs() == 0) return;
     grc[g] = c->rinv[g].run(1.0 / corr, has_prev[g], k.exponent_multiplier, k.epsilon, k.solver, k.newton_tolerance,
                             st, gstats[g], nullptr, nullptr, /*allow_warm=*/true, &full_rank[g], &low_rank[g]);
@@ -980,6 +983,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   if (!lr_jobs.empty()) {
     SH_CUDA_CHECK(cudaStreamWaitEvent(c->lr_stream, c->ev_fork, 0));
     lr_thread = std::thread([&] {
+      oz_set_tag(1);
       lrc = low_rank_root_inverse(lr_jobs, 1.0 / corr, k.exponent_multiplier, k.epsilon, c->lr_stream, lstats);
       if (lrc) lerr = shampoo_last_error();
     });

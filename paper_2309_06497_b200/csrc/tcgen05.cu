@@ -4,7 +4,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <atomic>
 #include <map>
+#include <mutex>
 #include <tuple>
 
 #include <cuda.h>
@@ -32,6 +34,9 @@ constexpr int kExpFloor = -1100;              // exponent of an all-zero row (ld
 // masked on the device, e.g. the root-inverse Newton iterations): one unit = one 32-wide k stage of
 // one slice pair on a 128 x 32 tile, i.e. 2 * 128 * 32 * 32 int8 ops.  One atomic per tile.
 __device__ unsigned long long g_oz_mma_units = 0;
+// the same per step-phase tag (bench kernel-level roofline; slot kOzTags - 1 = untagged)
+constexpr int kOzTags = 8;
+__device__ unsigned long long g_oz_mma_units_tag[kOzTags] = {};
 
 template <int S>
 struct OzCfg {
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
                                                                int64_t total_items, const int32_t* __restrict__ mask,
                                                                const int8_t* __restrict__ arena,
                                                                const int32_t* __restrict__ exps, double* __restrict__ ws,
-                                                               const CUtensorMap* __restrict__ tmaps) {
+                                                               const CUtensorMap* __restrict__ tmaps, int tag) {
   using Cfg = OzCfg<S>;
   using PC = OzPCfg<S>;
   extern __shared__ __align__(1024) uint8_t oz_smem[];
@@ -650,6 +655,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
         }
         tc_commit(&tfull[b]);  // accumulators of this tile complete
         atomicAdd(&g_oz_mma_units, (unsigned long long)it.nk * (S * (S + 1) / 2));
+        atomicAdd(&g_oz_mma_units_tag[tag], (unsigned long long)it.nk * (S * (S + 1) / 2));
         ++tcount;
       }
     }
@@ -824,6 +830,37 @@ static cudaError_t oz_set_smem_attrs() {
   }();  // once per instantiation, thread-safe
   return e;
 }
+
+// Kernel-level timing of the GEMM launches (bench evidence): CUDA events around each k_oz_gemm_p
+// launch on its stream, bucketed by the calling thread's step-phase tag (oz_set_tag).
+thread_local int t_oz_tag = kOzTags - 1;
+struct OzGemmTimer {
+  std::atomic<bool> on{false};
+  std::mutex mu;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<cudaEvent_t> pool;
+  void begin(cudaStream_t s, cudaEvent_t* a, cudaEvent_t* b) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (cudaEvent_t* e : {a, b}) {
+        if (pool.empty()) {
+          cudaEventCreate(e);
+        } else {
+          *e = pool.back();
+          pool.pop_back();
+        }
+      }
+    }
+    cudaEventRecord(*a, s);
+  }
+  void end(cudaStream_t s, int tag, cudaEvent_t a, cudaEvent_t b) {
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(mu);
+    pending.emplace_back(tag, a, b);
+  }
+};
+OzGemmTimer g_oz_timer;
+int oz_tag() { return t_oz_tag; }
 
 template <typename T>
 OzakiGemmBatch<T>::~OzakiGemmBatch() {
@@ -1080,10 +1117,14 @@ int OzakiGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   }
   if ((rc = launch_pack(sets_[0], s, mask))) return rc;
   const unsigned grid = (unsigned)std::min<int64_t>(total_items_, kNumSMs);
+  const int tag = oz_tag();
+  cudaEvent_t ea = nullptr, eb = nullptr;
+  if (g_oz_timer.on.load(std::memory_order_relaxed)) g_oz_timer.begin(s, &ea, &eb);
   OZ_DISPATCH(S_, k_oz_gemm_p<T, S><<<grid, GEMM_THREADS_P, OzPCfg<S>::SMEM, s>>>(
                       d_prob_, d_tp_, d_begin_, (int)host.size(), total_items_, mask, arena_, exps_, ws_,
-                      static_cast<const CUtensorMap*>(d_tmaps_)));
+                      static_cast<const CUtensorMap*>(d_tmaps_), tag));
   SH_LAUNCH_CHECK();
+  if (ea) g_oz_timer.end(s, tag, ea, eb);
   if (total_red_ > 0) {
     k_oz_reduce<T><<<(unsigned)total_red_, 256, 0, s>>>(d_prob_, d_tp_, d_rbegin_, d_rprob_, nred_, mask, ws_);
     SH_LAUNCH_CHECK();
@@ -1109,6 +1150,45 @@ template class OzakiGemmBatch<double>;
 }  // namespace shampoo
 
 // ---------------------------------------------------------------- C ABI utility
+
+namespace shampoo {
+int oz_set_tag(int tag) {
+  const int prev = t_oz_tag;
+  t_oz_tag = (tag >= 0 && tag < kOzTags - 1) ? tag : kOzTags - 1;
+  return prev;
+}
+}  // namespace shampoo
+
+extern "C" int shampoo_gemm_timing(int32_t enable, double* ms, double* int8_ops, int64_t* launches) {
+  using namespace shampoo;
+  std::lock_guard<std::mutex> lk(g_oz_timer.mu);
+  if (ms || launches) {
+    for (int q = 0; q < kOzTags; ++q) {
+      if (ms) ms[q] = 0.0;
+      if (launches) launches[q] = 0;
+    }
+    for (auto& p : g_oz_timer.pending) {
+      float e = 0.f;
+      SH_CUDA_CHECK(cudaEventSynchronize(std::get<2>(p)));
+      SH_CUDA_CHECK(cudaEventElapsedTime(&e, std::get<1>(p), std::get<2>(p)));
+      if (ms) ms[std::get<0>(p)] += e;
+      if (launches) launches[std::get<0>(p)] += 1;
+    }
+  }
+  for (auto& p : g_oz_timer.pending) {
+    g_oz_timer.pool.push_back(std::get<1>(p));
+    g_oz_timer.pool.push_back(std::get<2>(p));
+  }
+  g_oz_timer.pending.clear();
+  unsigned long long units[kOzTags] = {};
+  SH_CUDA_CHECK(cudaMemcpyFromSymbol(units, g_oz_mma_units_tag, sizeof(units)));
+  if (int8_ops)
+    for (int q = 0; q < kOzTags; ++q) int8_ops[q] = (double)units[q] * 2.0 * TM * TN * TKB;
+  const unsigned long long zero[kOzTags] = {};
+  SH_CUDA_CHECK(cudaMemcpyToSymbol(g_oz_mma_units_tag, zero, sizeof(zero)));
+  g_oz_timer.on.store(enable != 0);
+  return SHAMPOO_OK;
+}
 
 extern "C" int shampoo_tc_counter(int32_t reset, double* int8_ops) {
   using namespace shampoo;

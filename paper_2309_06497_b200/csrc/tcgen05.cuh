@@ -66,6 +66,10 @@ struct OzPackJob {
   int64_t echunks;       // rowexp threads (contiguous rows: 32 per 2048-wide chunk; else 1 per 64)
 };
 
+// Step-phase tag of the calling host thread for the GEMM kernel timer / counters (returns the
+// previous tag; out-of-range = untagged).
+int oz_set_tag(int tag);
+
 template <typename T>
 class OzakiGemmBatch {
  public:
