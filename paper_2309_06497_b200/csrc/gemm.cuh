@@ -25,6 +25,8 @@ enum GemmFlags : int32_t {
   kGemmMasked = 4, // skip unless mask[mask_index] != 0
   kGemmConstA = 8,  // operand A changes rarely (an inverse factor): tensor-core packs are cached
   kGemmConstB = 16, // same for operand B
+  kGemmXformA = 32, // operand A packed as xa * A + xb * I with the fixed row exponent a_fexp (Ozaki path)
+  kGemmXformB = 64, // same for operand B (b_xa, b_xb, b_fexp)
 };
 
 struct Idx2 {
@@ -53,6 +55,10 @@ struct GemmProblem {
   void* C;
   Idx2 c_r, c_c;
   double alpha, beta;
+  // kGemmXform*: the operand entering the product is xa * X + xb * delta(row, k), sliced with the fixed
+  // exponent fexp (|entries| < 2^fexp guaranteed by the caller) -- no row-maximum pass
+  double a_xa, a_xb, b_xa, b_xb;
+  int32_t a_fexp, b_fexp;
 };
 
 struct GemvProblem {

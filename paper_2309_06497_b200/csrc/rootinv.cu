@@ -1081,6 +1081,7 @@ __global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ 
       X[e] *= sx;
     }
   }
+  if (N.tpack) return;  // T is packed straight from M by the X T / T T launch
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
     const bool d = (e / N.n == e % N.n);
     T[e] = ((d ? (double)(N.p + 1) : 0.0) - M[e]) / N.p;
@@ -1562,6 +1563,11 @@ int RootInverseBatch::build_newton() {
       // in 18 iterations at n = 4096 and misses the cap by one at 8192)
       if (host_[j].n > 2048) hn[j].cap += (int)std::ceil(std::log2(host_[j].n / 2048.0));
     }
+    // T enters only the first power step for p = 2, 4, 8 (T T, then squarings of the result): pack it
+    // straight from M with the affine map and a fixed exponent (|T_ij| <= ||T||_2 < (p+1)/p <= 1.5 < 2^1:
+    // the scaled spectrum of M stays inside (0, p + 1))
+    const int pj = host_[j].root_p;
+    hn[j].tpack = (pj == 2 || pj == 4 || pj == 8) ? 1 : 0;
   }
   SH_CUDA_CHECK(dev_malloc(&d_newton_, std::max(nj, 1) * sizeof(NewtonJob)));
   SH_CUDA_CHECK(dev_malloc(&d_resbits_, std::max(nj, 1) * sizeof(unsigned long long)));
@@ -1598,15 +1604,34 @@ int RootInverseBatch::build_newton() {
       g.mask_index = j;
       return g;
     };
+    const double xa = -1.0 / host_[j].root_p, xb = (double)(host_[j].root_p + 1) / host_[j].root_p;
     for (int c = 0; c < 2; ++c) {
-      newton_x_[c].add(sym_gemm(buf(c), buf(kNT), buf(c ^ 1)));
+      GemmProblem gx = sym_gemm(buf(c), buf(kNT), buf(c ^ 1));
+      if (hn[j].tpack) {  // B = T from M_c
+        gx.B = buf(2 + c);
+        gx.flags |= kGemmXformB;
+        gx.b_xa = xa;
+        gx.b_xb = xb;
+        gx.b_fexp = 1;
+      }
+      newton_x_[c].add(gx);
       newton_m_[c].add(sym_gemm(buf(fb), buf(2 + c), buf(2 + (c ^ 1))));
     }
     for (size_t q = 0; q < plan.size(); ++q) {
       GemmProblem g = sym_gemm(buf(plan[q].lhs), buf(plan[q].rhs), buf(plan[q].dst));
       if (q == 0) {  // T T with the X update: mask2 sits nj words after mask
         g.mask_index = nj + j;
-        for (int c = 0; c < 2; ++c) newton_x_[c].add(g);
+        for (int c = 0; c < 2; ++c) {
+          GemmProblem gc = g;
+          if (hn[j].tpack) {  // T T = SYRK of the affine pack of M_c (shares X T's B pack)
+            gc.A = gc.B = buf(2 + c);
+            gc.flags |= kGemmXformA | kGemmXformB;
+            gc.a_xa = gc.b_xa = xa;
+            gc.a_xb = gc.b_xb = xb;
+            gc.a_fexp = gc.b_fexp = 1;
+          }
+          newton_x_[c].add(gc);
+        }
       } else {
         newton_pow_[q - 1]->add(g);
       }

@@ -64,6 +64,8 @@ struct NewtonJob {
   int32_t iters, converged;
   int32_t cap;  // hybrid pre-pass: iteration cap (conditioning gate, kHybridNewtonKappa)
   int32_t fin;  // hybrid pre-pass: residual small enough that one more X <- X T is final
+  int32_t tpack;  // T = ((p+1) I - M) / p is packed straight from M (affine pack, fixed exponent): no FP64 T
+  int32_t pad_;
   double lam;   // hybrid pre-pass: power-iteration estimate of lambda_max(A) (scales X0, M0)
   double scale; // hybrid pre-pass: spectrum scaling applied at the start of the next iteration
   double vit;   // hybrid pre-pass: iterations counted for the conditioning gate (scaled ones count more)

@@ -203,6 +203,10 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
   const OzPackJob& J = jobs[j];
   if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
   const int64_t u = (int64_t)(blockIdx.x - ebegin[j]) * 256 + threadIdx.x;
+  if (J.fexp != kNoFixedExp) {  // fixed exponent: one thread per row writes it
+    if (u < J.rows) exps[J.exp + u] = J.fexp;
+    return;
+  }
   const T* __restrict__ src = static_cast<const T*>(J.src);
   double m = 0.0;
   int row;
@@ -357,6 +361,11 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
 #pragma unroll
       for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
     }
+    if (J.xa != 1.0 || J.xb != 0.0) {  // affine operand (e.g. Newton's T = ((p+1) I - M) / p)
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        xv[i] = (k0 + i < J.K) ? J.xa * xv[i] + (row == k0 + i ? J.xb : 0.0) : 0.0;
+    }
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const double x4[4] = {xv[4 * g], xv[4 * g + 1], xv[4 * g + 2], xv[4 * g + 3]};
@@ -394,7 +403,9 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const T* __restrict__ src = static_cast<const T*>(J.src);
   constexpr int R = PACK_CORES * 8;
-  if (k_contig(J)) {
+  if (J.fexp != kNoFixedExp) {
+    // fixed exponent (affine operands): no maxima pass
+  } else if (k_contig(J)) {
     for (int rr = warp; rr < R; rr += 8) {  // warp per row, lanes along k
       const int row = core0 * 8 + rr;
       double m = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
@@ -435,7 +446,8 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
   if (tid < ncores * 8) {
     const double m = rmax[0][tid];
     int e = kExpFloor;
-    if (m > 0.0) frexp(m, &e);
+    if (J.fexp != kNoFixedExp) e = J.fexp;
+    else if (m > 0.0) frexp(m, &e);
     rexp[tid] = e;
     exps[J.exp + core0 * 8 + tid] = e;
   }
@@ -468,6 +480,11 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
+      }
+      if (J.xa != 1.0 || J.xb != 0.0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          xv[i] = (k0 + i < J.K) ? J.xa * xv[i] + (row == k0 + i ? J.xb : 0.0) : 0.0;
       }
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -798,6 +815,8 @@ __global__ void __launch_bounds__(256) k_oz_reduce(const GemmProblem* __restrict
 namespace {
 bool same_idx(const Idx2& a, const Idx2& b) { return a.div == b.div && a.hi == b.hi && a.lo == b.lo; }
 bool same_operand(const GemmProblem& p) {
+  const bool xa = (p.flags & kGemmXformA) != 0, xb = (p.flags & kGemmXformB) != 0;
+  if (xa != xb || (xa && (p.a_xa != p.b_xa || p.a_xb != p.b_xb || p.a_fexp != p.b_fexp))) return false;
   return p.A == p.B && p.M == p.N && same_idx(p.a_r, p.b_r) && same_idx(p.a_k, p.b_k);
 }
 }  // namespace
@@ -907,15 +926,17 @@ int OzakiGemmBatch<T>::upload() {
     const void* src;
     int64_t r0, r1, r2, k0, k1, k2;
     int rows, K, ks;
+    double xa, xb;
+    int fexp;
     bool operator<(const PackKey& o) const {
-      return std::tie(set, src, r0, r1, r2, k0, k1, k2, rows, K, ks) <
-             std::tie(o.set, o.src, o.r0, o.r1, o.r2, o.k0, o.k1, o.k2, o.rows, o.K, o.ks);
+      return std::tie(set, src, r0, r1, r2, k0, k1, k2, rows, K, ks, xa, xb, fexp) <
+             std::tie(o.set, o.src, o.r0, o.r1, o.r2, o.k0, o.k1, o.k2, o.rows, o.K, o.ks, o.xa, o.xb, o.fexp);
     }
   };
   std::map<PackKey, std::tuple<int64_t, int32_t, int64_t>> packed;
   auto add_pack = [&](int set, const void* src, Idx2 r, Idx2 k, int rows, int K, int ks, int mask_index,
-                      int64_t& off, int32_t& rc, int64_t& exp) {
-    const PackKey key{set, src, r.div, r.hi, r.lo, k.div, k.hi, k.lo, rows, K, ks};
+                      int64_t& off, int32_t& rc, int64_t& exp, double xa, double xb, int fexp) {
+    const PackKey key{set, src, r.div, r.hi, r.lo, k.div, k.hi, k.lo, rows, K, ks, xa, xb, fexp};
     if (share_packs_) {
       const auto it = packed.find(key);
       if (it != packed.end()) {
@@ -940,6 +961,9 @@ int OzakiGemmBatch<T>::upload() {
     J.dst = off;
     J.exp = exp;
     J.units = (int64_t)ks * rc * 16;
+    J.xa = xa;
+    J.xb = xb;
+    J.fexp = fexp;
     J.echunks = (k.div == 0x7fffffff && k.lo == 1)
                     ? (int64_t)rows * ((K + EXP_WARP_CHUNK - 1) / EXP_WARP_CHUNK) * 32  // threads (warps x 32)
                     : (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
@@ -971,7 +995,9 @@ int OzakiGemmBatch<T>::upload() {
     else t.tiles = sym ? sym_tiles_before(t.mt, t.nt) : (int64_t)t.mt * t.nt;
     const int mi = (p.flags & kGemmMasked) ? p.mask_index : -1;
     const int aset = (p.flags & kGemmConstA) ? 1 : 0;
-    add_pack(aset, p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp);
+    const bool xfa = (p.flags & kGemmXformA) != 0, xfb = (p.flags & kGemmXformB) != 0;
+    add_pack(aset, p.A, p.a_r, p.a_k, p.M, p.K, t.ks, mi, t.a_pack, t.a_rc, t.a_exp, xfa ? p.a_xa : 1.0,
+             xfa ? p.a_xb : 0.0, xfa ? p.a_fexp : kNoFixedExp);
     a_set[i] = aset;
     if (share) {
       t.b_pack = t.a_pack;
@@ -979,7 +1005,8 @@ int OzakiGemmBatch<T>::upload() {
       t.b_exp = t.a_exp;
     } else {
       const int bset = (p.flags & kGemmConstB) ? 1 : 0;
-      add_pack(bset, p.B, p.b_r, p.b_k, p.N, p.K, t.ks, mi, t.b_pack, t.b_rc, t.b_exp);
+      add_pack(bset, p.B, p.b_r, p.b_k, p.N, p.K, t.ks, mi, t.b_pack, t.b_rc, t.b_exp, xfb ? p.b_xa : 1.0,
+               xfb ? p.b_xb : 0.0, xfb ? p.b_fexp : kNoFixedExp);
       b_set[i] = bset;
     }
     t.ws_off = 0;

@@ -64,7 +64,11 @@ struct OzPackJob {
   int64_t exp;           // row-exponent offset
   int64_t units;         // pack threads: rc * 8 * ks * 2 (row, stage, K core)
   int64_t echunks;       // rowexp threads (contiguous rows: 32 per 2048-wide chunk; else 1 per 64)
+  double xa, xb;         // packed value = xa * src + xb * (row == k); identity: 1, 0
+  int32_t fexp;          // kNoFixedExp, or the fixed row exponent (no row-maximum pass)
+  int32_t pad2;
 };
+constexpr int32_t kNoFixedExp = 0x7fffffff;
 
 // Step-phase tag of the calling host thread for the GEMM kernel timer / counters (returns the
 // previous tag; out-of-range = untagged).
