@@ -336,12 +336,16 @@ def run_ours(args):
         l0 = P.launch_count()
         h0 = time.perf_counter()
         ev[0].record(stream)
+        enq = []
         for k in range(args.steps):
             refresh.append(is_refresh(opt.step_count))
+            e0 = opt.host_enqueue_s
             opt.step(grads[k])
+            enq.append(opt.host_enqueue_s - e0)
             ev[k + 1].record(stream)
         torch.cuda.synchronize()
         host_s = time.perf_counter() - h0
+        window.enqueue_ms = [1e3 * x for x in enq]
         opt.exchange = exchange
         per = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
         return per, refresh, ev[0].elapsed_time(ev[-1]), host_s, P.launch_count() - l0
@@ -364,6 +368,8 @@ def run_ours(args):
     if prof:
         torch.cuda.cudart().cudaProfilerStop()
     value, plain_ms, refresh_ms = amortise(per, refr, f)
+    enq_plain = [m for m, r in zip(window.enqueue_ms, refr) if not r]
+    host_enqueue_ms = float(np.median(enq_plain)) if enq_plain else None
     value, plain_ms, refresh_ms, total_ms = max_over_ranks([value, plain_ms, refresh_ms, total_ms])
     window_ms = total_ms / args.steps
 
@@ -637,6 +643,7 @@ def run_ours(args):
                 "root_inverse_ms_per_block": round(per_call["root_inverse"] / max(nb, 1), 4),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "host_ms_per_step": round(1e3 * host_s / args.steps, 3),
+                "host_enqueue_ms_per_plain_step": round(host_enqueue_ms, 3) if host_enqueue_ms is not None else None,
                 "clocks": clk.summary(), "adam_fused_ms": round(adam_ms, 4) if adam_ms else None,
                 "iteration_overhead": overhead,
                 "device_state_gb": round(opt.device_bytes / 1e9, 3)}

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence, Union
 
@@ -122,6 +123,7 @@ class Shampoo:
         # (step / synchronize / state_tree / step_count), with the step counter rolled back
         self.check_finite = check_finite
         self._pending_check = False
+        self.host_enqueue_s = 0.0
         self._t = 0
         # float32 parameters: directions travel (all-gather) and apply in float32 -- the update lands
         # in float32 anyway; half the gather-buffer bytes
@@ -239,6 +241,7 @@ class Shampoo:
         """One full optimizer step (optim.py:356-383); raises before any mutation on bad input.
         ``lr``: overrides lr_at(config, t) for this step (torch LR schedulers through the facade)."""
         self.synchronize()
+        t_host = time.perf_counter()
         grads = self._as_grads(grads)
         if self._params:
             dt = {p.dtype for p in self._params}
@@ -265,6 +268,9 @@ class Shampoo:
             self.exchange(self.gather_buffer, self.group_rank, self.max_payload)
         self.apply_gathered(t, lr)
         self._t += 1
+        # host cost of enqueueing the step (validation, ctypes calls, launches), excluding the wait
+        # for the previous step's deferred check; refresh steps include their host-side solver syncs
+        self.host_enqueue_s += time.perf_counter() - t_host
 
     # -- gradient reduction to block owners
 
