@@ -361,11 +361,6 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
 #pragma unroll
       for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
     }
-    if (J.xa != 1.0 || J.xb != 0.0) {  // affine operand (e.g. Newton's T = ((p+1) I - M) / p)
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        xv[i] = (k0 + i < J.K) ? J.xa * xv[i] + (row == k0 + i ? J.xb : 0.0) : 0.0;
-    }
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const double x4[4] = {xv[4 * g], xv[4 * g + 1], xv[4 * g + 2], xv[4 * g + 3]};
@@ -388,7 +383,7 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
 // One DRAM pass over each operand instead of two (k_oz_rowexp + k_oz_pack), no exponent memset.
 constexpr int PACK_CORES = 4;  // 32 rows per CTA
 
-template <typename T, int S>
+template <typename T, int S, bool XF>
 __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restrict__ jobs,
                                                       const int64_t* __restrict__ cbegin, int njobs,
                                                       const int32_t* __restrict__ mask, int32_t* __restrict__ exps,
@@ -481,7 +476,7 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
 #pragma unroll
         for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
       }
-      if (J.xa != 1.0 || J.xb != 0.0) {
+      if constexpr (XF) {  // affine operand (Newton's T = ((p+1) I - M) / p), fixed exponent
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           xv[i] = (k0 + i < J.K) ? J.xa * xv[i] + (row == k0 + i ? J.xb : 0.0) : 0.0;
@@ -975,6 +970,7 @@ int OzakiGemmBatch<T>::upload() {
     cbegin[set].push_back(ps.core_ctas);
     ps.core_ctas += (rc + PACK_CORES - 1) / PACK_CORES;
     if (!(k.div == 0x7fffffff && k.lo == 1)) ps.all_contig = false;
+    if (xa != 1.0 || xb != 0.0) ps.has_xform = true;
     jobs[set].push_back(J);
     if (share_packs_) packed[key] = std::make_tuple(off, rc, exp);
   };
@@ -1033,7 +1029,13 @@ int OzakiGemmBatch<T>::upload() {
   }
   for (int q = 0; q < 2; ++q)
     for (auto& J : jobs[q]) J.exp += sets_[q].exp_begin;
-  for (auto& ps : sets_) ps.fused_ok = ps.all_contig && ps.core_ctas >= 2 * kNumSMs;
+  for (auto& ps : sets_) {
+    ps.fused_ok = ps.all_contig && ps.core_ctas >= 2 * kNumSMs;
+    if (ps.has_xform && !ps.all_contig) {
+      set_error("affine operand packs need row-contiguous operands");
+      return SHAMPOO_ERR_INVALID_ARGUMENT;
+    }
+  }
   nred_ = (int)rbegin.size();
   SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemmProblem)));
   SH_CUDA_CHECK(dev_malloc(&d_tp_, tp.size() * sizeof(OzProb)));
@@ -1119,9 +1121,17 @@ int OzakiGemmBatch<T>::launch_pack(const PackSet& ps, cudaStream_t s, const int3
     const char* e = std::getenv("SHAMPOO_OZ_FUSED_PACK");
     return e ? std::atoi(e) != 0 : true;  // 0: always the two-pass k_oz_rowexp + k_oz_pack (A/B)
   }();
+  if (ps.has_xform) {  // affine operands are packed by the fused kernel only (its transform instantiation)
+    OZ_DISPATCH(S_, (k_oz_pack_rows<T, S, true><<<(unsigned)ps.core_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_cbegin,
+                                                                                        ps.njobs, mask, exps_,
+                                                                                        arena_)));
+    SH_LAUNCH_CHECK();
+    return SHAMPOO_OK;
+  }
   if (fused && ps.fused_ok) {
-    OZ_DISPATCH(S_, k_oz_pack_rows<T, S><<<(unsigned)ps.core_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_cbegin, ps.njobs,
-                                                                                  mask, exps_, arena_));
+    OZ_DISPATCH(S_, (k_oz_pack_rows<T, S, false><<<(unsigned)ps.core_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_cbegin,
+                                                                                         ps.njobs, mask, exps_,
+                                                                                         arena_)));
     SH_LAUNCH_CHECK();
     return SHAMPOO_OK;
   }

@@ -115,6 +115,7 @@ class OzakiGemmBatch {
     int64_t* d_cbegin = nullptr;   // fused pack CTA prefix per job (PACK_CORES cores per CTA)
     int64_t exp_begin = 0, exp_elems = 0, pack_ctas = 0, exp_ctas = 0, core_ctas = 0;
     bool all_contig = true, fused_ok = false;  // fused single-pass pack: contiguous rows, >= 2 CTAs per SM
+    bool has_xform = false;                    // affine operands: always the fused kernel's transform variant
     int njobs = 0;
   };
   int launch_pack(const PackSet& ps, cudaStream_t s, const int32_t* mask) const;
