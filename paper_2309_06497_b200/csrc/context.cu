@@ -152,6 +152,13 @@ struct shampoo_ctx {
   int32_t* d_ready = nullptr;      // = d_gomask + 1
   int32_t* d_gomask = nullptr;     // [go word | ready per owned block]
   bool prec0_done = false;         // this step's first mode products ran with the statistics
+  // the statistics write lower triangles only; k_symmetrize restores the upper ones before a refresh
+  // or an export reads full factors
+  SymJob* d_sym_jobs = nullptr;
+  int64_t* d_sym_tbegin = nullptr;
+  int n_sym_jobs = 0;
+  int64_t n_sym_tiles = 0;
+  bool fact_lower = false;
   int32_t *d_cb = nullptr, *d_cc = nullptr;
   // tables
   DevBlock* d_blocks = nullptr;
@@ -206,6 +213,8 @@ struct shampoo_ctx {
     cudaFree(d_fb_chunks);
     cudaFree(d_diag_blocks);
     cudaFree(d_ptrs);
+    cudaFree(d_sym_jobs);
+    cudaFree(d_sym_tbegin);
     cudaFreeHost(h_flag);
     cudaFreeHost(h_ptr_ring);
     for (auto& e : ptr_ev)
@@ -374,7 +383,7 @@ int build_engine(shampoo_ctx* c) {
       for (int q = m + 1; q < order; ++q) inner *= d[q];
       {
         GemmProblem g = make_mode_gram(G + c->vofs[l], outer, d[m], inner, FACT + off, alpha, beta);
-        g.flags |= kGemmMasked;  // predicated on the step's go word (deferred non-finite check)
+        g.flags |= kGemmMasked | kGemmLowerOnly;  // predicated on the step's go word (deferred check)
         g.mask_index = 0;
         if (thin(g)) e->stats_thin.add(g);
         else e->stats.add(g);
@@ -630,6 +639,29 @@ int shampoo_ctx_create(const shampoo_plan* plan, const shampoo_config* cfg, int3
     const int32_t one = 1;
     SH_CUDA_CHECK(cudaMemcpy(c->d_go, &one, sizeof(int32_t), cudaMemcpyHostToDevice));
   }
+  {
+    std::vector<SymJob> sj;
+    std::vector<int64_t> tb;
+    for (size_t l = 0; l < c->owned.size(); ++l) {
+      const BlockPlan& b = plan->blocks[c->owned[l]];
+      if (b.kind != SHAMPOO_BLOCK_SHAMPOO) continue;
+      int64_t off = c->fac_off[l];
+      for (int64_t d : b.dims()) {
+        sj.push_back(SymJob{off, (int32_t)d, 0});
+        tb.push_back(c->n_sym_tiles);
+        const int64_t t = (d + 31) / 32;
+        c->n_sym_tiles += t * (t + 1) / 2;
+        off += d * d;
+      }
+    }
+    c->n_sym_jobs = (int)sj.size();
+    SH_CUDA_CHECK(cudaMalloc(&c->d_sym_jobs, std::max<size_t>(sj.size(), 1) * sizeof(SymJob)));
+    SH_CUDA_CHECK(cudaMalloc(&c->d_sym_tbegin, std::max<size_t>(tb.size(), 1) * sizeof(int64_t)));
+    if (!sj.empty()) {
+      SH_CUDA_CHECK(cudaMemcpy(c->d_sym_jobs, sj.data(), sj.size() * sizeof(SymJob), cudaMemcpyHostToDevice));
+      SH_CUDA_CHECK(cudaMemcpy(c->d_sym_tbegin, tb.data(), tb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+  }
   SH_CUDA_CHECK(cudaMalloc(&c->d_blocks, std::max(nb, 1) * sizeof(DevBlock)));
   SH_CUDA_CHECK(cudaMalloc(&c->d_params, std::max(c->nparams, 1) * sizeof(DevBlock)));
   SH_CUDA_CHECK(cudaMalloc(&c->d_owned_chunks, std::max<size_t>(oc.size(), 1) * sizeof(Chunk)));
@@ -807,6 +839,18 @@ int join_stats(shampoo_ctx* c, cudaStream_t s) {
   return SHAMPOO_OK;
 }
 
+// Restore the upper triangles of the factors (stream-ordered on s after the statistics).
+int symmetrize_factors(shampoo_ctx* c, cudaStream_t s) {
+  if (!c->fact_lower) return SHAMPOO_OK;
+  int rc = join_stats(c, s);
+  if (rc) return rc;
+  rc = c->f32 ? launch_symmetrize<float>(c->d_sym_jobs, c->d_sym_tbegin, c->n_sym_jobs, c->n_sym_tiles, c->FACT, s)
+              : launch_symmetrize<double>(c->d_sym_jobs, c->d_sym_tbegin, c->n_sym_jobs, c->n_sym_tiles, c->FACT, s);
+  if (rc) return rc;
+  c->fact_lower = false;
+  return SHAMPOO_OK;
+}
+
 // The stats phase; gradients from the caller's tensors (grads) or from a reduced gather-layout
 // buffer (gbuf, context dtype, scaled by gscale).
 int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf, double gscale,
@@ -872,6 +916,7 @@ int stats_update_impl(shampoo_ctx* c, const void* const* grads, const void* gbuf
                                                   c->d_diag_blocks, c->n_diag, s);
     if (rc) return rc;
   }
+  c->fact_lower = true;  // the statistics GEMMs wrote lower triangles
   c->graft_step = gstep;
   for (size_t l = 0; l < c->owned.size(); ++l)
     if (c->plan.blocks[c->owned[l]].kind != SHAMPOO_BLOCK_GRAFT_ONLY) ++c->step[l];
@@ -919,7 +964,7 @@ int shampoo_root_inverse(shampoo_ctx* c, int64_t t, int32_t* refreshed, void* st
   if (njobs == 0) return SHAMPOO_OK;
   const double corr = (k.use_bias_correction && k.beta2 < 1.0) ? 1.0 - std::pow(k.beta2, (double)(t + 1)) : 1.0;
   {
-    const int rj = join_stats(c, s);  // the refresh reads this step's factors
+    const int rj = symmetrize_factors(c, s);  // the refresh reads this step's full factors
     if (rj) return rj;
   }
   PhaseScope scope(&c->timer, 1, s);
@@ -1179,6 +1224,9 @@ void* shampoo_state_view(shampoo_ctx* c, int32_t block_id, const char* name, int
     for (int m = 0; m < mode; ++m) off += d[m] * d[m];
     if (numel) *numel = d[mode] * d[mode];
     if (n == "inv_factor" && c->engine) c->engine->inverses_changed();  // the caller may write through it
+    if (n == "factor" && c->fact_lower) {  // exports read full factors (the caller synchronised before)
+      if (symmetrize_factors(c, 0) || cudaStreamSynchronize(0) != cudaSuccess) return nullptr;
+    }
     base = static_cast<char*>(n == "factor" ? c->FACT : c->INV);
     return base + off * c->esz;
   }

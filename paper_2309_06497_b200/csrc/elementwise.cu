@@ -746,6 +746,51 @@ int launch_copy_ptrs(const void* mapped_src, void* dst, int n, cudaStream_t s) {
   return SHAMPOO_OK;
 }
 
+// Lower -> upper triangle of every factor (the statistics write lower triangles only; run before
+// anything reads full factors).  CTA per 32 x 32 tile (ti >= tj) of one factor; off-diagonal tiles
+// are transposed through shared memory, diagonal tiles mirrored in place.
+template <typename T>
+__global__ void __launch_bounds__(256) k_symmetrize(const SymJob* __restrict__ jobs, const int64_t* __restrict__ tbegin,
+                                                    int njobs, T* __restrict__ F) {
+  __shared__ T tile[32][33];
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tbegin[mid] <= (int64_t)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const SymJob J = jobs[lo];
+  const int64_t l = blockIdx.x - tbegin[lo];
+  int ti = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(ti + 1) * (ti + 2) / 2 <= l) ++ti;
+  while ((int64_t)ti * (ti + 1) / 2 > l) --ti;
+  const int tj = (int)(l - (int64_t)ti * (ti + 1) / 2);
+  const int n = J.d;
+  T* C = F + J.off;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int i = ti * 32 + r, j = tj * 32 + tx;
+    tile[r][tx] = (i < n && j < n && i >= j) ? C[(int64_t)i * n + j] : T(0);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // element (tj*32 + r, ti*32 + tx) = (ti*32 + tx, tj*32 + r)
+    const int i2 = tj * 32 + r, j2 = ti * 32 + tx;
+    if (i2 < n && j2 < n && j2 > i2) C[(int64_t)i2 * n + j2] = tile[tx][r];
+  }
+}
+
+template <typename T>
+int launch_symmetrize(const SymJob* jobs, const int64_t* tbegin, int njobs, int64_t ntiles, void* F, cudaStream_t s) {
+  if (!njobs || !ntiles) return SHAMPOO_OK;
+  k_symmetrize<T><<<(unsigned)ntiles, 256, 0, s>>>(jobs, tbegin, njobs, static_cast<T*>(F));
+  SH_LAUNCH_CHECK();
+  return SHAMPOO_OK;
+}
+template int launch_symmetrize<double>(const SymJob*, const int64_t*, int, int64_t, void*, cudaStream_t);
+template int launch_symmetrize<float>(const SymJob*, const int64_t*, int, int64_t, void*, cudaStream_t);
+
 #define SH_INST(T)                                                                                   \
   template int launch_finite<T>(const Chunk*, int, const DevBlock*, const void* const*, int32_t,    \
                                 int32_t*, int32_t*, cudaStream_t);                                             \

@@ -80,6 +80,14 @@ int launch_apply(const Chunk* chunks, int nchunks, const DevBlock* blocks, void*
 template <typename T>
 int launch_pack_grads(const Chunk* chunks, int nchunks, const DevBlock* blocks, const void* const* grads,
                       int32_t dtype, void* buf, cudaStream_t s);
+// factor d x d at element offset `off` of the factor arena
+struct SymJob {
+  int64_t off;
+  int32_t d;
+  int32_t pad;
+};
+template <typename T>
+int launch_symmetrize(const SymJob* jobs, const int64_t* tbegin, int njobs, int64_t ntiles, void* F, cudaStream_t s);
 // host-mapped pinned memory transfers (no copy engine): flag -> host, pointer table <- host
 int launch_publish_flag(const int32_t* src, int32_t* mapped_dst, cudaStream_t s);
 int launch_copy_ptrs(const void* mapped_src, void* dst, int n, cudaStream_t s);

@@ -27,6 +27,8 @@ enum GemmFlags : int32_t {
   kGemmConstB = 16, // same for operand B
   kGemmXformA = 32, // operand A packed as xa * A + xb * I with the fixed row exponent a_fexp (Ozaki path)
   kGemmXformB = 64, // same for operand B (b_xa, b_xb, b_fexp)
+  kGemmLowerOnly = 128, // with kGemmSym: write the lower triangle only (the factor statistics; the upper
+                        // triangle is restored by symmetrize before anything reads the full factor)
 };
 
 struct Idx2 {

@@ -188,7 +188,7 @@ __device__ __forceinline__ void oz_store(const GemmProblem& P, int gi, int gj, d
   if (P.flags & kGemmReadC) v = fma(P.beta, (double)C[at], v);
   const T o = (T)v;
   C[at] = o;
-  if (sym && gi != gj) C[evx(P.c_r, gj) + evx(P.c_c, gi)] = o;
+  if (sym && gi != gj && !(P.flags & kGemmLowerOnly)) C[evx(P.c_r, gj) + evx(P.c_c, gi)] = o;
 }
 
 // Row exponents: e_r = max_k frexp-exponent(x_rk) (|x_rk| < 2^e_r).  Rows contiguous along k:
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
             C[row_off[r] + col_off[c]] = (T)val;
           }
         }
-        if (sym) {
+        if (sym && !(P.flags & kGemmLowerOnly)) {
           asm volatile("bar.sync 1, 256;" ::: "memory");
           for (int e = et; e < TM * TN; e += 256) {
             const int c = e / TM, r = e % TM;

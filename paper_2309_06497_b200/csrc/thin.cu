@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) k_thin_rank1_sym(const GemmProblem* __res
     *at = (T)v;
     tile[r][tx] = (double)(T)v;
   }
-  if (ti == tj) return;
+  if (ti == tj || (P.flags & kGemmLowerOnly)) return;
   __syncthreads();
 #pragma unroll
   for (int r = ty; r < 32; r += 8) {  // row tj*32 + r of C, columns ti*32 + tx: tile[tx][r]
