@@ -113,48 +113,56 @@ __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict
 }
 
 // Rank-1 symmetric update C = beta C + alpha x x^T of a contiguous row-major C (the factor EMA of
-// a vector block, precond.py:232-242), reading only the lower triangle: CTA per 32 x 32 tile (ti >= tj) of one problem;
-// the new tile is stored in place and, for ti > tj, transposed through shared memory into (tj, ti).
-// C is bitwise symmetric and x_i x_j == x_j x_i, so the result equals the full-square update bit for
-// bit with 12 instead of 16 bytes of traffic per element.
+// a vector block, precond.py:232-242): CTA per (problem, row), 16-byte accesses.  With
+// kGemmLowerOnly only columns j <= i are written (the statistics keep lower triangles; k_symmetrize
+// restores the upper ones), else the full row -- x_i x_j == x_j x_i exactly, so the square stays
+// bitwise symmetric.
 template <typename T>
-__global__ void __launch_bounds__(256) k_thin_rank1_sym(const GemmProblem* __restrict__ probs,
-                                                        const int64_t* __restrict__ begin, int nprob,
-                                                        const int32_t* __restrict__ mask) {
-  __shared__ double tile[32][33];
+__global__ void __launch_bounds__(256) k_thin_rank1(const GemmProblem* __restrict__ probs,
+                                                    const int64_t* __restrict__ begin, int nprob,
+                                                    const int32_t* __restrict__ mask) {
   const int p = find64(begin, nprob, blockIdx.x);
   const GemmProblem& P = probs[p];
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
-  const int64_t l = blockIdx.x - begin[p];
-  int ti = (int)((sqrt(8.0 * (double)l + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(ti + 1) * (ti + 2) / 2 <= l) ++ti;
-  while ((int64_t)ti * (ti + 1) / 2 > l) --ti;
-  const int tj = (int)(l - (int64_t)ti * (ti + 1) / 2);
-  const int n = P.N;
+  // lower-only: CTA per row pair (i, N-1-i), i + 1 + N - i = N + 1 elements -- balanced work
+  const bool lower = (P.flags & kGemmLowerOnly) != 0;
+  const int item = (int)(blockIdx.x - begin[p]);
+  for (int h = 0; h < (lower ? 2 : 1); ++h) {
+  const int i = lower ? (h == 0 ? item : P.N - 1 - item) : item;
+  if (h == 1 && i == item) break;  // odd N: the middle row once
   const T* __restrict__ x = static_cast<const T*>(P.A);
-  T* __restrict__ C = static_cast<T*>(P.C);
-  const int64_t step = P.a_r.lo;
+  T* __restrict__ row = static_cast<T*>(P.C) + (int64_t)i * P.N;
+  const double xi = (double)x[ev(P.a_r, i)];
   const bool readc = (P.flags & kGemmReadC) != 0;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int j = tj * 32 + tx;
-  const double xj = j < n ? (double)x[j * step] : 0.0;
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int i = ti * 32 + r;
-    if (i >= n || j >= n) continue;
-    const double xi = (double)x[i * step];
-    double v = P.alpha * (xi * xj);
-    T* at = C + (int64_t)i * n + j;
-    if (readc) v = fma(P.beta, (double)*at, v);
-    *at = (T)v;
-    tile[r][tx] = (double)(T)v;
+  const int64_t step = P.a_r.lo;
+  const int jend = lower ? i + 1 : P.N;
+  if (sizeof(T) == 8 && step == 1 && ((reinterpret_cast<uintptr_t>(row) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    double2* __restrict__ r2 = reinterpret_cast<double2*>(row);
+    const int npair = jend / 2;
+    for (int q = threadIdx.x; q < npair; q += blockDim.x) {
+      const double2 xv = x2[q];
+      double2 cv = readc ? r2[q] : make_double2(0.0, 0.0);
+      double v0 = P.alpha * (xi * xv.x), v1 = P.alpha * (xi * xv.y);
+      if (readc) {
+        v0 = fma(P.beta, cv.x, v0);
+        v1 = fma(P.beta, cv.y, v1);
+      }
+      r2[q] = make_double2(v0, v1);
+    }
+    if ((jend & 1) && threadIdx.x == 0) {  // odd tail (the diagonal of an even row)
+      const int j = jend - 1;
+      double v = P.alpha * (xi * (double)x[j]);
+      if (readc) v = fma(P.beta, (double)row[j], v);
+      row[j] = (T)v;
+    }
+    continue;
   }
-  if (ti == tj || (P.flags & kGemmLowerOnly)) return;
-  __syncthreads();
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {  // row tj*32 + r of C, columns ti*32 + tx: tile[tx][r]
-    const int i2 = tj * 32 + r, j2 = ti * 32 + tx;
-    if (i2 < n && j2 < n) C[(int64_t)i2 * n + j2] = (T)tile[tx][r];
+  for (int j = threadIdx.x; j < jend; j += blockDim.x) {
+    double v = P.alpha * (xi * (double)x[j * step]);
+    if (readc) v = fma(P.beta, (double)row[j], v);
+    row[j] = (T)v;
+  }
   }
 }
 
@@ -276,10 +284,9 @@ int ThinGemmBatch<T>::upload() {
   redp.insert(redp.end(), red8.begin(), red8.end());
   std::vector<int64_t> r1b;
   n_r1_ctas_ = 0;
-  for (const auto& p : r1p) {  // lower-triangle 32 x 32 tiles per problem
+  for (const auto& p : r1p) {  // CTA per row (lower-only: per row pair)
     r1b.push_back(n_r1_ctas_);
-    const int64_t t = (p.M + 31) / 32;
-    n_r1_ctas_ += t * (t + 1) / 2;
+    n_r1_ctas_ += (p.flags & kGemmLowerOnly) ? (p.M + 1) / 2 : p.M;
   }
   n_r1_ = (int)r1p.size();
   if (n_r1_) {
@@ -342,7 +349,7 @@ int ThinGemmBatch<T>::upload() {
 template <typename T>
 int ThinGemmBatch<T>::launch(cudaStream_t s, const int32_t* mask) const {
   if (n_r1_) {
-    k_thin_rank1_sym<T><<<(unsigned)n_r1_ctas_, 256, 0, s>>>(d_r1_, d_r1begin_, n_r1_, mask);
+    k_thin_rank1<T><<<(unsigned)n_r1_ctas_, 256, 0, s>>>(d_r1_, d_r1begin_, n_r1_, mask);
     SH_LAUNCH_CHECK();
   }
   if (n_out_) {
