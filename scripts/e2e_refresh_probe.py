@@ -43,6 +43,10 @@ sf = [torch.empty(n, device=dev) for _ in range(2)]
 sn = [[v.view(s) for v, s in zip(torch.split(f, numels), shapes)] for f in sf]
 for b in range(NB):
     df[b].copy_(hg[b % K])
+if os.environ.get("PROBE_WARM", "1") == "1":  # first-use costs outside the window (bench.py does the same)
+    for q in range(2):
+        torch._foreach_copy_(sn[q], list(opt.params()))
+        hp.copy_(sf[q], non_blocking=True)
 h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
 E = lambda: torch.cuda.Event(enable_timing=True)
 ev = [E() for _ in range(K + 1)]
@@ -81,3 +85,16 @@ for k in range(K):
 torch.cuda.synchronize()
 print(f"copies {copies}: per-step ms (step 0 = refresh)",
       [round(ev[k].elapsed_time(ev[k + 1]), 2) for k in range(K)])
+
+# the same optimizer, resident gradients, straight to the next refresh: is the refresh itself slower
+# inside the e2e loop, or is the difference the loop?
+while opt.step_count % 50 != 0:
+    opt.step(fresh())
+torch.cuda.synchronize()
+e0, e1 = E(), E()
+gg = fresh()
+e0.record(st)
+opt.step(gg)
+e1.record(st)
+torch.cuda.synchronize()
+print(f"next refresh (t={opt.step_count - 1}) with resident gradients: {e0.elapsed_time(e1):.2f} ms")
