@@ -89,6 +89,11 @@ TRAJ_CONFIGS = {
                            precondition_frequency=2, max_preconditioner_dim=6, epsilon=1e-6),
     "normalized_adam": dict(grafting=GraftKind.NORMALIZED_ADAM, betas=(0.5, 0.9),
                             precondition_frequency=2, max_preconditioner_dim=6, epsilon=1e-8),
+    "normalized_adagrad": dict(grafting=GraftKind.NORMALIZED_ADAGRAD, momentum=0.9,
+                               precondition_frequency=3, max_preconditioner_dim=6, epsilon=1e-10),
+    "normalized_rmsprop": dict(grafting=GraftKind.NORMALIZED_RMSPROP, grafting_beta2=0.95,
+                               betas=(0.0, 0.99), weight_decay=1e-3, use_decoupled_weight_decay=False,
+                               precondition_frequency=2, max_preconditioner_dim=5, epsilon=1e-9),
 }
 TRAJ_STEPS = 6
 
