@@ -191,6 +191,13 @@ SHAMPOO_API int shampoo_stats_update(shampoo_ctx* ctx, const void* const* grads,
 /* Step t phase 2: if t >= start and t % frequency == 0, guarded root inverse of
  * every owned factor (eigh or coupled Newton).  Synchronises `stream` (one
  * small readback per solver sweep). Returns 1 in *refreshed if it ran. */
+/* Step phase 3 on several ranks (dist.py:350-359 WorkerSim exchange): in-place NCCL all-gather of the
+ * direction gather buffer within this rank's replica group, on `stream`.  nccl_comm: the group's
+ * ncclComm_t (ranks ordered by group rank, as the plan's owner ranks).  NCCL is resolved at run time
+ * (the libnccl.so.2 already loaded in the process, else the system one); the buffer holds float32
+ * when the parameters are float32 (gather_dtype) or the state is single precision, else float64. */
+SHAMPOO_API int shampoo_allgather(shampoo_ctx* ctx, void* nccl_comm, void* stream);
+
 /* ---- gradient reduction to block owners (replaces the DDP all-reduce the reference
  * does not model, dist.py:332-356): every rank packs its LOCAL gradients into the gather-buffer layout
  * (gbuf: group_size * max_payload scalars of the context dtype, block b at its gather offset), the

@@ -85,6 +85,7 @@ SIGNATURES = {
     "shampoo_check_finite_deferred": (C.c_int, [_P, C.POINTER(_P), _I32, C.c_int64, C.POINTER(_I32), _P]),
     "shampoo_check_finite_resolve": (C.c_int, [_P, C.POINTER(_I32)]),
     "shampoo_gemm_timing": (C.c_int, [_I32, C.POINTER(_D), C.POINTER(_D), _PI64]),
+    "shampoo_allgather": (C.c_int, [_P, _P, _P]),
     "shampoo_stats_update": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I32, _I64, _P]),
     "shampoo_root_inverse": (C.c_int, [_P, _I64, _PI32, _P]),
     "shampoo_pack_gradients": (C.c_int, [_P, C.POINTER(_P), _I32, _P, _P]),

@@ -8,6 +8,8 @@
 //   (group_size x max_payload scalars, dist.py:179-183) and solver workspaces.
 // Each step phase is a handful of grouped launches over device-side block and
 // chunk tables, independent of the number of blocks.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -1117,6 +1119,59 @@ int shampoo_apply(shampoo_ctx* c, void* const* params, int32_t dtype, double lr,
   c->go_armed = false;  // the predicated step ends here
   if (rc) return rc;
   return join_stats(c, s);  // the step ends with everything it launched ordered before the caller's stream
+}
+
+// NCCL, resolved at run time: the library already in the process (PyTorch's) or the system one, so
+// this library does not link a second NCCL next to the caller's.
+namespace {
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+struct NcclApi {
+  nccl_allgather_fn allgather = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  std::string error;
+};
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      a.error = std::string("libnccl.so.2 not found: ") + dlerror();
+      return a;
+    }
+    a.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+    a.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h, "ncclGetErrorString"));
+    if (!a.allgather) a.error = "ncclAllGather not exported by libnccl.so.2";
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+int shampoo_allgather(shampoo_ctx* c, void* nccl_comm, void* stream) {
+  if (!nccl_comm) {
+    set_error("allgather: null communicator");
+    return SHAMPOO_ERR_INVALID_ARGUMENT;
+  }
+  const NcclApi& api = nccl_api();
+  if (!api.allgather) {
+    set_error("allgather: " + api.error);
+    return SHAMPOO_ERR_CUDA;
+  }
+  const int64_t count = c->plan.max_payload;
+  if (count == 0) return SHAMPOO_OK;
+  const bool f32 = c->buf_f32 || c->f32;
+  const size_t es = f32 ? 4 : 8;
+  char* buf = static_cast<char*>(c->BUF);
+  // in place: this rank's region is already at group_rank * max_payload of the group buffer
+  const int r = api.allgather(buf + (size_t)c->grank * count * es, buf, (size_t)count, f32 ? 7 : 8, nccl_comm,
+                              static_cast<cudaStream_t>(stream));
+  if (r != 0) {
+    set_error(std::string("ncclAllGather: ") + (api.errstr ? api.errstr(r) : std::to_string(r)));
+    return SHAMPOO_ERR_CUDA;
+  }
+  return SHAMPOO_OK;
 }
 
 int shampoo_timing_enable(shampoo_ctx* c, int32_t enable) {
