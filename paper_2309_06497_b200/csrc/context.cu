@@ -9,6 +9,7 @@
 // Each step phase is a handful of grouped launches over device-side block and
 // chunk tables, independent of the number of blocks.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: phase ranges for nsys / ncu --nvtx (no-ops untraced)
 
 #include <algorithm>
 #include <cmath>
@@ -98,12 +99,17 @@ struct PhaseScope {
   cudaEvent_t a = nullptr;
   int prev_tag;
   PhaseScope(PhaseTimer* t_, int p, cudaStream_t s_) : t(t_), phase(p), s(s_), prev_tag(oz_set_tag(p)) {
+    static const char* const kNames[SHAMPOO_NUM_PHASES] = {"shampoo.stats", "shampoo.root_inverse",
+                                                            "shampoo.precondition", "shampoo.graft_momentum",
+                                                            "shampoo.apply"};
+    nvtxRangePushA(kNames[p]);
     if (t->on) {
       a = t->get();
       cudaEventRecord(a, s);
     }
   }
   ~PhaseScope() {
+    nvtxRangePop();
     oz_set_tag(prev_tag);
     if (t->on) {
       cudaEvent_t b = t->get();
