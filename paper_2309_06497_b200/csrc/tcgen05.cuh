@@ -13,25 +13,28 @@
 //   x_rk = 2^e_r * sum_{s=0}^{S-1} q_rks 2^(-7(s+1)) + O(2^(e_r - 7S)),  q in [-127, 127]
 //   C_ij = 2^(e_i + f_j) * sum_{d=0}^{S-1} 2^(-7(d+2)) * acc_d[i][j],
 //   acc_d = sum over slice pairs (s, t), s + t = d, of the exact int32 dot products.
-// Pairs with s + t >= S are dropped (below the truncation error).  S = 8 for
-// precision "double" (operand truncation 2^-56 of the row maximum: FP64 class),
-// S = 5 for "single" (2^-35).  Used for the factor statistics (precond.py:161-165,
-// 232-242) and the mode products (precond.py:168-174) of both precisions.
+// Pairs with s + t >= S are dropped (below the truncation error).  Slice counts: 6 for the plain
+// steps of precision "double" (statistics and mode products, 2^-42 of the row maximum), 8 for the
+// root-inverse iterates (FP64 class: the Newton errors scale with 2^-7S), 5 for "single" (2^-35).
+// Used for the factor statistics (precond.py:161-165, 232-242), the mode products
+// (precond.py:168-174) and the root-inverse GEMMs (matfun.py:164-222).
 //
 // Pipeline per launch (one launch set covers every block of a phase):
-//   k_oz_rowexp  per-row exponents (atomicMax of frexp exponents);
-//   k_oz_pack    operands -> int8 slice planes in the canonical no-swizzle K-major UMMA
-//                layout, [stage][slice][8-row core][2 K cores][8 rows][16 B]; a tile's
-//                row cores of one slice are one contiguous cp.async.bulk;
-//   k_oz_gemm    one CTA per (problem, 128x64 tile, K split): warp 0 issues the bulk
-//                copies (mbarrier complete_tx), warp 1 owns TMEM and issues
-//                tcgen05.mma (one elected thread): A slice sa against the B slices
-//                0..S-1-sa stacked along N, so output block sb lands in the TMEM
-//                accumulator of diagonal d = sa + sb (12 MMAs per 32-wide k step for
-//                S = 8); warps 2-5 drain TMEM with tcgen05.ld, combine the diagonals in
-//                FP64 and store through a shared-memory tile (coalesced; alpha, beta*C,
-//                SYRK mirror, split-K partials);
-//   k_oz_reduce  split-K partials summed in FP64 in a fixed order (deterministic).
+//   k_oz_rowexp     per-row exponents (atomicMax of frexp exponents);
+//   k_oz_pack       operands -> int8 slice planes in the canonical no-swizzle K-major UMMA layout,
+//                   [stage][slice][8-row core][2 K cores][8 rows][16 B] (branch-free integer slicing,
+//                   16-byte operand loads); k_oz_pack_rows fuses both passes for row-contiguous sets
+//                   and applies affine operand maps (Newton's T = ((p+1) I - M) / p, fixed exponent);
+//                   problems of one launch that read the same operand share one pack;
+//   k_oz_gemm_p     persistent, one CTA per SM over (problem, 128x64 tile, K split) items: warp 0
+//                   issues TMA (cp.async.bulk.tensor) boxes into a 3-5 stage mbarrier ring, warp 1
+//                   owns TMEM and issues tcgen05.mma (one elected thread): A slice sa against the B
+//                   slices 0..S-1-sa stacked along N (<= 4 per instruction), so output block sb lands
+//                   in the TMEM accumulator of diagonal d = sa + sb; warps 2-9 drain TMEM with
+//                   tcgen05.ld, combine the diagonals in FP64 and store through a shared-memory tile
+//                   (coalesced; alpha, beta*C, SYRK mirror or lower triangle only, split-K partials).
+//                   Accumulators double-buffered when 2 x S x 64 columns fit TMEM (S <= 4);
+//   k_oz_reduce     split-K partials summed in FP64 in a fixed order (deterministic).
 #pragma once
 
 #include <vector>
