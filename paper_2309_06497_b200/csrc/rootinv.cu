@@ -897,8 +897,32 @@ __global__ void __launch_bounds__(256) k_pow_mv(const RootJob* __restrict__ jobs
   double* y = const_cast<double*>(x) + n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
-    double sum = 0.0;
-    for (int k = lane; k < n; k += 32) sum = fma(A[(int64_t)i * J.np + k], x[k], sum);
+    const double* __restrict__ ar = A + (int64_t)i * J.np;
+    // 16-byte loads, four independent chains per lane (the row is np-padded and 16-byte aligned)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = 2 * lane;
+    if ((J.np & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+      for (; k + 64 + 1 < n; k += 128) {
+        const double2 a0 = *reinterpret_cast<const double2*>(ar + k);
+        const double2 x0 = *reinterpret_cast<const double2*>(x + k);
+        const double2 a1 = *reinterpret_cast<const double2*>(ar + k + 64);
+        const double2 x1 = *reinterpret_cast<const double2*>(x + k + 64);
+        s0 = fma(a0.x, x0.x, s0);
+        s1 = fma(a0.y, x0.y, s1);
+        s2 = fma(a1.x, x1.x, s2);
+        s3 = fma(a1.y, x1.y, s3);
+      }
+      for (; k + 1 < n; k += 64) {
+        const double2 a0 = *reinterpret_cast<const double2*>(ar + k);
+        const double2 x0 = *reinterpret_cast<const double2*>(x + k);
+        s0 = fma(a0.x, x0.x, s0);
+        s1 = fma(a0.y, x0.y, s1);
+      }
+      if (k < n) s0 = fma(ar[k], x[k], s0);
+    } else {
+      for (k = lane; k < n; k += 32) s0 = fma(ar[k], x[k], s0);
+    }
+    double sum = (s0 + s1) + (s2 + s3);
     sum = warp_sum(sum);
     if (lane == 0) y[i] = sum;
   }

@@ -246,51 +246,52 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
 }
 
 // The S signed 7-bit slices of y = x 2^-e (|y| < 1): the digits of the fixed-point |y| in base 128
-// with the sign of x, the last one rounded half-to-even on the remaining bits and clamped to +-127
-// -- exactly  t = 128 y, q = trunc(t), y = t - q  for the first S - 1 slices and q = rint(t) for
-// the last (unbiased truncation of the dropped remainder), computed on the integer mantissa (no
-// FP64 / conversion-pipe work).  Split for packing: the magnitude digits 0..S-2 are bit fields of
-// `top`, the rounded last digit is `last`, the sign `neg` (applied per byte after packing).
+// with the sign of x, the last one rounded to nearest (ties away from zero) on the remaining bits
+// and clamped to +-127 -- t = 128 y, q = trunc(t), y = t - q for the first S - 1 slices and
+// q = round(t) for the last (the dropped remainder is rounded, not truncated: no bias in the
+// factor sums), computed on the integer significand (no FP64 / conversion-pipe work).
+// Y = floor(|x| 2^(63 - e)) < 2^63 is one variable right shift of the significand left-aligned
+// at bit 63: digit k is bits [56 - 7k, 63 - 7k) of Y, the remainder the RB = 63 - 7S bits below.
+// Split for packing: digits 0..S-2 as bit fields of `top`, the rounded last digit `last`.
 template <int S>
-__device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& top, uint32_t& last, uint32_t& neg) {
-  // branch-free (the elements of a warp take different shift cases; branches serialised them):
-  // yg = m 2^sh with |x| < 2^e, so sh <= 7S + G - 53 -- a left shift exists only for S >= 7, and a
-  // right shift of 63 clears any 53-bit mantissa
-  constexpr int G = 7;
+__device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& top, uint32_t& last) {
+  constexpr int RB = 63 - 7 * S;
   const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-  const int bexp = (int)((bits >> 52) & 0x7ff);
-  const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | ((unsigned long long)(bexp != 0) << 52);
-  const int sh = max(bexp, 1) - 1075 - e + 7 * S + G;
-  const int rs = min(max(-sh, 0), 63);
-  unsigned long long ml = m;
-  if constexpr (7 * S + G > 53) ml = m << max(sh, 0);
-  const unsigned long long yg = ml >> rs;
-  const uint32_t sticky = (ml & ((1ull << rs) - 1ull)) != 0ull;
-  top = yg >> G;
-  const uint32_t frac = (uint32_t)yg & ((1u << G) - 1u), half = 1u << (G - 1);
-  uint32_t l = (uint32_t)(top & 127ull);
-  l += (uint32_t)(frac > half) | ((uint32_t)(frac == half) & (sticky | (l & 1u)));
-  last = min(l, 127u);
-  neg = (uint32_t)(bits >> 63);
+  const int bexp = (int)(bits >> 52) & 0x7ff;
+  const unsigned long long M = (bits << 11) | ((unsigned long long)(bexp != 0) << 63);
+  // |x| = (M >> 11) 2^(max(bexp,1) - 1075) < 2^e  =>  shift >= 1 for every nonzero x; an all-zero
+  // row's floor exponent makes it negative (M = 0 there): clamp
+  const int rs = min(max(1023 + e - max(bexp, 1), 0), 63);
+  const unsigned long long Y = M >> rs;
+  top = Y >> (RB + 7);
+  const uint32_t l = (uint32_t)(Y >> RB) & 127u;
+  const uint32_t up = (RB <= 32) ? (uint32_t)((uint32_t)Y & (uint32_t)((1ull << RB) - 1ull)) >= (1u << (RB - 1))
+                                 : (Y & ((1ull << RB) - 1ull)) >= (1ull << (RB - 1));
+  last = min(l + up, 127u);
 }
 
 // Four consecutive elements -> S words of packed int8 slices (byte i = element i): magnitudes
-// gathered with byte permutes, the signs applied per byte (two's complement: (v ^ m) - m).
+// gathered with byte permutes; signs as a byte mask (PRMT sign replication of the high bytes) and
+// applied per byte: -d = (0x80 - d) ^ 0x80 for d in [0, 127], no borrow across bytes.
 template <int S>
 __device__ __forceinline__ void ozaki_pack4(const double (&x)[4], int e, uint32_t (&w)[S]) {
   unsigned long long t[4];
-  uint32_t l[4], n[4];
+  uint32_t l[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) ozaki_mag<S>(x[i], e, t[i], l[i], n[i]);
-  const uint32_t msk = (n[0] ? 0x000000FFu : 0u) | (n[1] ? 0x0000FF00u : 0u) | (n[2] ? 0x00FF0000u : 0u) |
-                       (n[3] ? 0xFF000000u : 0u);
+  for (int i = 0; i < 4; ++i) ozaki_mag<S>(x[i], e, t[i], l[i]);
+  // prmt sign mode (selector nibble bit 3): result byte = the selected byte's sign bit replicated
+  uint32_t h01, h23;
+  asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(h01) : "r"(__double2hiint(x[0])), "r"(__double2hiint(x[1])));
+  asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(h23) : "r"(__double2hiint(x[2])), "r"(__double2hiint(x[3])));
+  const uint32_t msk = __byte_perm(h01, h23, 0x6420);  // byte i = 0xFF iff x[i] has its sign bit set
 #pragma unroll
   for (int sl = 0; sl < S; ++sl) {
     uint32_t b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] = (sl + 1 < S) ? ((uint32_t)(t[i] >> (7 * (S - 1 - sl))) & 127u) : l[i];
+    for (int i = 0; i < 4; ++i) b[i] = (sl + 1 < S) ? ((uint32_t)(t[i] >> (7 * (S - 2 - sl))) & 127u) : l[i];
     const uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-    w[sl] = __vsub4(word ^ msk, msk);
+    const uint32_t negw = (0x80808080u - word) ^ 0x80808080u;
+    w[sl] = (word & ~msk) | (negw & msk);
   }
 }
 
@@ -494,6 +495,150 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
 #pragma unroll
     for (int s_ = 0; s_ < S; ++s_)
       *reinterpret_cast<uint4*>(dst + (int64_t)s_ * J.rc * 256) = make_uint4(w[s_][0], w[s_][1], w[s_][2], w[s_][3]);
+  }
+}
+
+// Transposed operand pairs (OzDualJob).  The column operand's own path reads X down columns
+// (strided, 8-byte loads) twice -- once for its maxima, once to pack; here both operands take one
+// coalesced exponent pass and one pack pass whose 64 x 32 tile is staged in shared memory and read
+// by rows (operand a) and by columns (operand b).  Bytes per element: 2 reads + 2 S plane bytes,
+// against 4 reads + 2 S (two k_oz_rowexp + two k_oz_pack passes).
+constexpr int DX_R = 64, DX_C = 64;  // exponent tile: a half warp per 16-column row segment
+constexpr int DP_R = 64, DP_C = 32;  // pack tile: a = 8 cores x 1 stage, b = 4 cores x 2 stages
+
+__device__ __forceinline__ bool dual_on(const OzDualJob& J, const int32_t* __restrict__ mask) {
+  if (!mask) return true;
+  return J.mask_a < 0 || J.mask_b < 0 || mask[J.mask_a] || mask[J.mask_b];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_oz_dual_exp(const OzDualJob* __restrict__ jobs,
+                                                     const int64_t* __restrict__ tbegin, int njobs,
+                                                     const int32_t* __restrict__ mask, int32_t* __restrict__ exps) {
+  __shared__ double cmax[16][DX_C + 1];
+  const int j = find64<OzDualJob>(tbegin, njobs, blockIdx.x);
+  const OzDualJob& J = jobs[j];
+  if (!dual_on(J, mask)) return;
+  const int64_t t = blockIdx.x - tbegin[j];
+  // job fields in registers and read-only global loads: all 16 loads issue back to back
+  const int R = J.R, C = J.C;
+  const int64_t ld = J.ld;
+  const T* __restrict__ src = static_cast<const T*>(J.src);
+  const int tcn = (C + DX_C - 1) / DX_C;
+  const int tt = (int)t;
+  const int r0 = (tt / tcn) * DX_R, c0 = (tt % tcn) * DX_C;
+  const int cg = threadIdx.x & 15, rg = threadIdx.x >> 4;
+  T x[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = r0 + rg + 16 * q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = c0 + cg + 16 * i;
+      x[q][i] = (r < R && c < C) ? __ldg(src + (int64_t)r * ld + c) : T(0);
+    }
+  }
+  double v[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[q][i] = fabs((double)x[q][i]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // row maxima: the 16 lanes of a half warp share a row
+    double m = fmax(fmax(v[q][0], v[q][1]), fmax(v[q][2], v[q][3]));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int r = r0 + rg + 16 * q;
+    if (cg == 0 && m > 0.0 && r < R) {
+      int e;
+      frexp(m, &e);
+      atomicMax(exps + J.exp_a + r, e);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) cmax[rg][cg + 16 * i] = fmax(fmax(v[0][i], v[1][i]), fmax(v[2][i], v[3][i]));
+  __syncthreads();
+  if (threadIdx.x < DX_C) {  // column maxima over the 16 row groups
+    double m = cmax[0][threadIdx.x];
+#pragma unroll
+    for (int g = 1; g < 16; ++g) m = fmax(m, cmax[g][threadIdx.x]);
+    const int c = c0 + threadIdx.x;
+    if (m > 0.0 && c < C) {
+      int e;
+      frexp(m, &e);
+      atomicMax(exps + J.exp_b + c, e);
+    }
+  }
+}
+
+// One 16-element unit of slice planes from values already in registers (same bytes as k_oz_pack).
+template <int S>
+__device__ __forceinline__ void pack_unit16(const double (&xv)[16], int e, int8_t* __restrict__ dst, int64_t plane) {
+  uint32_t w[S][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const double x4[4] = {xv[4 * g], xv[4 * g + 1], xv[4 * g + 2], xv[4 * g + 3]};
+    uint32_t ws[S];
+    ozaki_pack4<S>(x4, e, ws);
+#pragma unroll
+    for (int s_ = 0; s_ < S; ++s_) w[s_][g] = ws[s_];
+  }
+#pragma unroll
+  for (int s_ = 0; s_ < S; ++s_)
+    *reinterpret_cast<uint4*>(dst + (int64_t)s_ * plane) = make_uint4(w[s_][0], w[s_][1], w[s_][2], w[s_][3]);
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(256) k_oz_pack_dual(const OzDualJob* __restrict__ jobs,
+                                                      const int64_t* __restrict__ tbegin, int njobs,
+                                                      const int32_t* __restrict__ mask,
+                                                      const int32_t* __restrict__ exps, int8_t* __restrict__ arena) {
+  __shared__ double tile[DP_R][DP_C + 1];  // +1: row and column reads both conflict-free
+  const int j = find64<OzDualJob>(tbegin, njobs, blockIdx.x);
+  const OzDualJob& J = jobs[j];
+  if (!dual_on(J, mask)) return;
+  const int64_t t = blockIdx.x - tbegin[j];
+  const int R = J.R, C = J.C;
+  const int64_t ld = J.ld;
+  const T* __restrict__ src = static_cast<const T*>(J.src);
+  const int tcn = (C + DP_C - 1) / DP_C;
+  const int tt = (int)t;
+  const int r0 = (tt / tcn) * DP_R, c0 = (tt % tcn) * DP_C;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const int c = c0 + lane;
+    T x[DP_R / 8];
+#pragma unroll
+    for (int q = 0; q < DP_R / 8; ++q) {  // a warp per 32-wide row segment; all loads before the stores
+      const int r = r0 + warp + 8 * q;
+      x[q] = (r < R && c < C) ? __ldg(src + (int64_t)r * ld + c) : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < DP_R / 8; ++q) tile[warp + 8 * q][lane] = (double)x[q];
+  }
+  __syncthreads();
+  const int u = tid & 127, r8 = u & 7, kc = (u >> 3) & 1;
+  double xv[16];
+  if (tid < 128) {  // operand a (rows of X): core r0/8 + cl, stage c0/32
+    const int cl = u >> 4, core = r0 / 8 + cl;
+    if (core >= J.rc_a) return;
+    const int lr = cl * 8 + r8;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xv[i] = tile[lr][kc * 16 + i];
+    const int e = max(exps[J.exp_a + r0 + lr], kExpFloor);
+    const int stage = c0 / TKB;
+    pack_unit16<S>(xv, e, arena + J.dst_a + ((int64_t)stage * S * J.rc_a + core) * 256 + kc * 128 + r8 * 16,
+                   (int64_t)J.rc_a * 256);
+  } else {  // operand b (columns of X): core c0/8 + cl, stage r0/32 + st
+    const int cl = (u >> 4) & 3, st = u >> 6;
+    const int core = c0 / 8 + cl, stage = r0 / TKB + st;
+    if (core >= J.rc_b || stage >= J.ks_b) return;
+    const int lc = cl * 8 + r8;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xv[i] = tile[st * 32 + kc * 16 + i][lc];
+    const int e = max(exps[J.exp_b + c0 + lc], kExpFloor);
+    pack_unit16<S>(xv, e, arena + J.dst_b + ((int64_t)stage * S * J.rc_b + core) * 256 + kc * 128 + r8 * 16,
+                   (int64_t)J.rc_b * 256);
   }
 }
 
@@ -886,6 +1031,9 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
     dev_free(ps.d_pbegin);
     dev_free(ps.d_ebegin);
     dev_free(ps.d_cbegin);
+    dev_free(ps.d_dual);
+    dev_free(ps.d_dxbegin);
+    dev_free(ps.d_dpbegin);
   }
   dev_free(d_rbegin_);
   dev_free(d_rprob_);
@@ -893,6 +1041,49 @@ OzakiGemmBatch<T>::~OzakiGemmBatch() {
   dev_free(exps_);
   dev_free(ws_);
   dev_free(d_tmaps_);
+}
+
+inline bool k_contig_host(const OzPackJob& J) { return J.k.div == 0x7fffffff && J.k.lo == 1; }
+
+// Moves every (rows of X, columns of X) job pair out of `jobs` into `dual`: a = rows (unit k
+// stride, row stride ld >= K), b = columns (unit row stride, k stride ld) of the same source, both
+// untransformed with computed exponents.
+static void pair_transposed(std::vector<OzPackJob>& jobs, std::vector<OzDualJob>& dual) {
+  auto plain = [](const OzPackJob& J) { return J.xa == 1.0 && J.xb == 0.0 && J.fexp == kNoFixedExp; };
+  std::map<std::tuple<const void*, int64_t, int32_t, int32_t>, size_t> rows_of;  // (src, ld, R, C) -> a
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const OzPackJob& J = jobs[i];
+    if (plain(J) && k_contig_host(J) && J.r.div == 0x7fffffff && J.r.lo >= J.K && J.rows > 0 && J.K > 0)
+      rows_of.emplace(std::make_tuple(J.src, J.r.lo, J.rows, J.K), i);
+  }
+  std::vector<char> gone(jobs.size(), 0);
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    const OzPackJob& B = jobs[i];
+    if (!plain(B) || B.r.div != 0x7fffffff || B.r.lo != 1 || B.k.div != 0x7fffffff || B.k.lo < 2) continue;
+    const auto it = rows_of.find(std::make_tuple(B.src, B.k.lo, B.K, B.rows));
+    if (it == rows_of.end() || gone[it->second]) continue;
+    const OzPackJob& A = jobs[it->second];
+    OzDualJob D{};
+    D.src = A.src;
+    D.ld = A.r.lo;
+    D.R = A.rows;
+    D.C = A.K;
+    D.mask_a = A.mask_index;
+    D.mask_b = B.mask_index;
+    D.rc_a = A.rc;
+    D.rc_b = B.rc;
+    D.ks_b = B.ks;
+    D.dst_a = A.dst;
+    D.dst_b = B.dst;
+    D.exp_a = A.exp;
+    D.exp_b = B.exp;
+    dual.push_back(D);
+    gone[it->second] = gone[i] = 1;
+  }
+  std::vector<OzPackJob> rest;
+  for (size_t i = 0; i < jobs.size(); ++i)
+    if (!gone[i]) rest.push_back(jobs[i]);
+  jobs.swap(rest);
 }
 
 template <typename T>
@@ -962,15 +1153,6 @@ int OzakiGemmBatch<T>::upload() {
     J.echunks = (k.div == 0x7fffffff && k.lo == 1)
                     ? (int64_t)rows * ((K + EXP_WARP_CHUNK - 1) / EXP_WARP_CHUNK) * 32  // threads (warps x 32)
                     : (int64_t)rows * ((K + EXP_CHUNK - 1) / EXP_CHUNK);
-    PackSet& ps = sets_[set];
-    pbegin[set].push_back(ps.pack_ctas);
-    ps.pack_ctas += (J.units + PACK_UNITS - 1) / PACK_UNITS;
-    ebegin[set].push_back(ps.exp_ctas);
-    ps.exp_ctas += std::max<int64_t>(1, (J.echunks + 255) / 256);
-    cbegin[set].push_back(ps.core_ctas);
-    ps.core_ctas += (rc + PACK_CORES - 1) / PACK_CORES;
-    if (!(k.div == 0x7fffffff && k.lo == 1)) ps.all_contig = false;
-    if (xa != 1.0 || xb != 0.0) ps.has_xform = true;
     jobs[set].push_back(J);
     if (share_packs_) packed[key] = std::make_tuple(off, rc, exp);
   };
@@ -1029,6 +1211,31 @@ int OzakiGemmBatch<T>::upload() {
   }
   for (int q = 0; q < 2; ++q)
     for (auto& J : jobs[q]) J.exp += sets_[q].exp_begin;
+  // transposed operand pairs leave the per-operand job lists for the dual kernels
+  std::vector<OzDualJob> dual[2];
+  std::vector<int64_t> dxbegin[2], dpbegin[2];
+  const char* dp_env = std::getenv("SHAMPOO_OZ_DUAL_PACK");
+  if (!dp_env || std::atoi(dp_env) != 0)
+    for (int q = 0; q < 2; ++q) pair_transposed(jobs[q], dual[q]);
+  for (int q = 0; q < 2; ++q) {
+    PackSet& ps = sets_[q];
+    for (const OzPackJob& J : jobs[q]) {
+      pbegin[q].push_back(ps.pack_ctas);
+      ps.pack_ctas += (J.units + PACK_UNITS - 1) / PACK_UNITS;
+      ebegin[q].push_back(ps.exp_ctas);
+      ps.exp_ctas += std::max<int64_t>(1, (J.echunks + 255) / 256);
+      cbegin[q].push_back(ps.core_ctas);
+      ps.core_ctas += (J.rc + PACK_CORES - 1) / PACK_CORES;
+      if (!k_contig_host(J)) ps.all_contig = false;
+      if (J.xa != 1.0 || J.xb != 0.0) ps.has_xform = true;
+    }
+    for (const OzDualJob& D : dual[q]) {
+      dxbegin[q].push_back(ps.dual_exp_ctas);
+      ps.dual_exp_ctas += (int64_t)((D.R + DX_R - 1) / DX_R) * ((D.C + DX_C - 1) / DX_C);
+      dpbegin[q].push_back(ps.dual_pack_ctas);
+      ps.dual_pack_ctas += (int64_t)((D.R + DP_R - 1) / DP_R) * ((D.C + DP_C - 1) / DP_C);
+    }
+  }
   for (auto& ps : sets_) {
     ps.fused_ok = ps.all_contig && ps.core_ctas >= 2 * kNumSMs;
     if (ps.has_xform && !ps.all_contig) {
@@ -1040,7 +1247,7 @@ int OzakiGemmBatch<T>::upload() {
   SH_CUDA_CHECK(dev_malloc(&d_prob_, host.size() * sizeof(GemmProblem)));
   SH_CUDA_CHECK(dev_malloc(&d_tp_, tp.size() * sizeof(OzProb)));
   SH_CUDA_CHECK(dev_malloc(&d_begin_, begin.size() * sizeof(int64_t)));
-  if (ext_arena_ && arena <= ext_cap_ && sets_[1].pack_ctas == 0) {
+  if (ext_arena_ && arena <= ext_cap_ && sets_[1].pack_ctas == 0 && sets_[1].dual_pack_ctas == 0) {
     arena_ = ext_arena_;
     own_arena_ = false;
   } else {
@@ -1063,6 +1270,17 @@ int OzakiGemmBatch<T>::upload() {
     SH_CUDA_CHECK(cudaMemcpy(ps.d_ebegin, ebegin[q].data(), ebegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SH_CUDA_CHECK(dev_malloc(&ps.d_cbegin, cbegin[q].size() * sizeof(int64_t)));
     SH_CUDA_CHECK(cudaMemcpy(ps.d_cbegin, cbegin[q].data(), cbegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  for (int q = 0; q < 2; ++q) {
+    PackSet& ps = sets_[q];
+    ps.ndual = (int)dual[q].size();
+    if (!ps.ndual) continue;
+    SH_CUDA_CHECK(dev_malloc(&ps.d_dual, dual[q].size() * sizeof(OzDualJob)));
+    SH_CUDA_CHECK(dev_malloc(&ps.d_dxbegin, dual[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(dev_malloc(&ps.d_dpbegin, dual[q].size() * sizeof(int64_t)));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_dual, dual[q].data(), dual[q].size() * sizeof(OzDualJob), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_dxbegin, dxbegin[q].data(), dxbegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SH_CUDA_CHECK(cudaMemcpy(ps.d_dpbegin, dpbegin[q].data(), dpbegin[q].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   cached_valid_ = false;
   // TMA tensor maps of the packed operands: [S * ks slices-by-stage][rc cores][256 B core block]
@@ -1112,6 +1330,15 @@ int OzakiGemmBatch<T>::upload() {
 
 template <typename T>
 int OzakiGemmBatch<T>::launch_pack(const PackSet& ps, cudaStream_t s, const int32_t* mask) const {
+  if (ps.ndual) {
+    SH_CUDA_CHECK(cudaMemsetAsync(exps_ + ps.exp_begin, 0x80, ps.exp_elems * sizeof(int32_t), s));
+    k_oz_dual_exp<T><<<(unsigned)ps.dual_exp_ctas, 256, 0, s>>>(ps.d_dual, ps.d_dxbegin, ps.ndual, mask, exps_);
+    SH_LAUNCH_CHECK();
+    OZ_DISPATCH(S_, (k_oz_pack_dual<T, S><<<(unsigned)ps.dual_pack_ctas, 256, 0, s>>>(ps.d_dual, ps.d_dpbegin,
+                                                                                       ps.ndual, mask, exps_,
+                                                                                       arena_)));
+    SH_LAUNCH_CHECK();
+  }
   if (!ps.njobs) return SHAMPOO_OK;
   // The fused single-pass kernel wins on row-contiguous operands with enough rows to fill the machine
   // (the root inverse's n x n iterates: 34.7 -> 27.0 ms of packing per steady-state refresh); operands
@@ -1135,7 +1362,8 @@ int OzakiGemmBatch<T>::launch_pack(const PackSet& ps, cudaStream_t s, const int3
     SH_LAUNCH_CHECK();
     return SHAMPOO_OK;
   }
-  SH_CUDA_CHECK(cudaMemsetAsync(exps_ + ps.exp_begin, 0x80, ps.exp_elems * sizeof(int32_t), s));  // very negative
+  if (!ps.ndual)  // very negative (done above with the pairs)
+    SH_CUDA_CHECK(cudaMemsetAsync(exps_ + ps.exp_begin, 0x80, ps.exp_elems * sizeof(int32_t), s));
   k_oz_rowexp<T><<<(unsigned)ps.exp_ctas, 256, 0, s>>>(ps.d_jobs, ps.d_ebegin, ps.njobs, mask, exps_);
   SH_LAUNCH_CHECK();
   OZ_DISPATCH(S_, k_oz_pack<T, S><<<(unsigned)ps.pack_ctas, PACK_UNITS, 0, s>>>(ps.d_jobs, ps.d_pbegin, ps.njobs,

@@ -73,6 +73,21 @@ struct OzPackJob {
 };
 constexpr int32_t kNoFixedExp = 0x7fffffff;
 
+// A source matrix X (R x C, row stride ld, unit column stride) that is an operand both by rows
+// (k along a row: job a) and by columns (k down a column: job b) -- an order-2 block's two
+// statistics, or a mode-0 statistic and the first mode product's B operand.  Packed by one
+// exponent pass and one tile-transposing pack pass instead of two of each.
+struct OzDualJob {
+  const void* src;
+  int64_t ld;
+  int32_t R, C;
+  int32_t mask_a, mask_b;  // -1: unmasked; the pair runs if either is on
+  int32_t rc_a, rc_b;      // 8-row cores of the row (a) and column (b) operands
+  int32_t ks_b, pad;       // stages of b (a's stage never exceeds its ks)
+  int64_t dst_a, dst_b;    // byte offsets of the two plane sets
+  int64_t exp_a, exp_b;    // exponent offsets (R rows, C columns)
+};
+
 // Step-phase tag of the calling host thread for the GEMM kernel timer / counters (returns the
 // previous tag; out-of-range = untagged).
 int oz_set_tag(int tag);
@@ -120,6 +135,11 @@ class OzakiGemmBatch {
     bool all_contig = true, fused_ok = false;  // fused single-pass pack: contiguous rows, >= 2 CTAs per SM
     bool has_xform = false;                    // affine operands: always the fused kernel's transform variant
     int njobs = 0;
+    OzDualJob* d_dual = nullptr;   // transposed operand pairs (k_oz_dual_exp + k_oz_pack_dual)
+    int64_t* d_dxbegin = nullptr;  // exponent-tile CTA prefix per pair
+    int64_t* d_dpbegin = nullptr;  // pack-tile CTA prefix per pair
+    int64_t dual_exp_ctas = 0, dual_pack_ctas = 0;
+    int ndual = 0;
   };
   int launch_pack(const PackSet& ps, cudaStream_t s, const int32_t* mask) const;
   GemmProblem* d_prob_ = nullptr;
