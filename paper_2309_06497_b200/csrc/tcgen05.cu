@@ -132,16 +132,21 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
-  uint32_t r[16];
+// tcgen05.ld without the wait (several loads in flight, one tcgen05.wait::ld for all of them);
+// reg_fence16 after the wait keeps the consumers of the registers behind it
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = (int32_t)r[i];
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void reg_fence16(uint32_t* r) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]));
 }
 
 template <typename P>
@@ -235,8 +240,23 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__
     if (u >= J.echunks) return;
     row = (int)(u % J.rows);
     const int k0 = (int)(u / J.rows) * EXP_CHUNK, k1 = min(J.K, k0 + EXP_CHUNK);
-    const int64_t rb = evx(J.r, row);
-    for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)src[rb + evx(J.k, k)]));
+    const Idx2 kx = J.k;
+    if (kx.div == 0x7fffffff) {
+      const T* __restrict__ rp = src + evx(J.r, row) + (int64_t)k0 * kx.lo;
+      for (int k = k0; k < k1; ++k, rp += kx.lo) m = fmax(m, fabs((double)*rp));
+    } else {  // two-level k: one division, then carries
+      int q = k0 / kx.div, r = k0 - q * kx.div;
+      int64_t off = evx(J.r, row) + (int64_t)q * kx.hi + (int64_t)r * kx.lo;
+      const int64_t wrap = kx.hi - (int64_t)kx.div * kx.lo;
+      for (int k = k0; k < k1; ++k) {
+        m = fmax(m, fabs((double)src[off]));
+        off += kx.lo;
+        if (++r == kx.div) {
+          r = 0;
+          off += wrap;
+        }
+      }
+    }
   }
   if (m > 0.0) {
     int e;
@@ -358,9 +378,19 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
       const T* rp = src + rb + (int64_t)k0 * kx.lo;
 #pragma unroll
       for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)rp[(int64_t)i * kx.lo] : 0.0;
-    } else {
+    } else {  // two-level k: one division, then the (q, r) digits advance by carries
+      int q = k0 / kx.div, r = k0 - q * kx.div;
+      int64_t off = rb + (int64_t)q * kx.hi + (int64_t)r * kx.lo;
+      const int64_t wrap = kx.hi - (int64_t)kx.div * kx.lo;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) xv[i] = (k0 + i < J.K) ? (double)src[rb + evx(kx, k0 + i)] : 0.0;
+      for (int i = 0; i < 16; ++i) {
+        xv[i] = (k0 + i < J.K) ? (double)src[off] : 0.0;
+        off += kx.lo;
+        if (++r == kx.div) {
+          r = 0;
+          off += wrap;
+        }
+      }
     }
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -841,25 +871,51 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
         row_off[et] = evx(P.c_r, gi);
         mcol_off[et] = evx(P.c_c, gi);
       }
+      if ((P.flags & kGemmReadC) && T_.ksplit == 1) {
+        // beta C does not depend on the MMAs: pull this thread's half row of the C tile into L2 while
+        // they run (small-K statistics tiles are otherwise bound by the epilogue's C round trips)
+        const int gi = tm * TM + (et >> 1), gj = tn * TN + (et & 1) * (TN / 2);
+        if (gi < P.M && gj < P.N) {
+          const char* pc = reinterpret_cast<const char*>(static_cast<const T*>(P.C) + evx(P.c_r, gi) + evx(P.c_c, gj));
+#pragma unroll
+          for (int o = 0; o < (int)(TN / 2 * sizeof(T)); o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + o));
+        }
+      }
       const uint32_t b = tcount % PC::NBUF;
       mbar_wait_sleep(&tfull[b], (tcount / PC::NBUF) & 1u);
       tc_fence_after();
       const uint32_t acc = tmem + b * PC::ACC_COLS;
       const double rscale = pow2i(exps[T_.a_exp + min(tm * TM + rl, T_.a_rc * 8 - 1)]);
       constexpr int H = (S + 1) / 2;
-      int32_t v[16];
       for (int c0 = cbeg; c0 < cbeg + TN / 2; c0 += 16) {
         long long hi[16], lo[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0;
         if (it.nk > 0) {
+          // two batches of diagonals (hi: d < H, lo: d >= H), each with its loads in flight together
+          const uint32_t ta = acc + ((uint32_t)(lg * 32) << 16) + (uint32_t)c0;
+          {
+            uint32_t raw[H][16];
 #pragma unroll
-          for (int d = 0; d < S; ++d) {
-            tmem_ld16(acc + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * TN + c0), v);
+            for (int d = 0; d < H; ++d) tmem_ld16_async(ta + (uint32_t)(d * TN), raw[d]);
+            tmem_wait_ld();
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              if (d < H) hi[q] += (long long)v[q] << (7 * (H - 1 - d));
-              else lo[q] += (long long)v[q] << (7 * (S - 1 - d));
+            for (int d = 0; d < H; ++d) {
+              reg_fence16(raw[d]);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) hi[q] += (long long)(int32_t)raw[d][q] << (7 * (H - 1 - d));
+            }
+          }
+          if constexpr (S > H) {
+            uint32_t raw[S - H][16];
+#pragma unroll
+            for (int d = H; d < S; ++d) tmem_ld16_async(ta + (uint32_t)(d * TN), raw[d - H]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int d = H; d < S; ++d) {
+              reg_fence16(raw[d - H]);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) lo[q] += (long long)(int32_t)raw[d - H][q] << (7 * (S - 1 - d));
             }
           }
         }
@@ -876,17 +932,18 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
       if (T_.ksplit == 1) {
         T* __restrict__ C = static_cast<T*>(P.C);
         const bool readc = (P.flags & kGemmReadC) != 0;
-        for (int e0 = et; e0 < TM * TN; e0 += 8 * 256) {
-          double cv[8];
+        constexpr int PER = 16;  // C values loaded per round trip (all issued before any store)
+        for (int e0 = et; e0 < TM * TN; e0 += PER * 256) {
+          double cv[PER];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < PER; ++u) {
             const int e = e0 + u * 256, r = e / TN, c = e % TN;
             const int gi = tm * TM + r, gj = tn * TN + c;
             const bool live = gi < P.M && gj < P.N && !(sym && gi < gj);
             cv[u] = (readc && live) ? (double)C[row_off[r] + col_off[c]] : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < PER; ++u) {
             const int e = e0 + u * 256, r = e / TN, c = e % TN;
             const int gi = tm * TM + r, gj = tn * TN + c;
             if (gi >= P.M || gj >= P.N || (sym && gi < gj)) continue;
