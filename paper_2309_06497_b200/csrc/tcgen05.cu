@@ -290,11 +290,30 @@ __device__ __forceinline__ void ozaki_mag(double x, int e, unsigned long long& t
   last = min(l + up, 127u);
 }
 
-// Four consecutive elements -> S words of packed int8 slices (byte i = element i): magnitudes
-// gathered with byte permutes; signs as a byte mask (PRMT sign replication of the high bytes) and
-// applied per byte: -d = (0x80 - d) ^ 0x80 for d in [0, 127], no borrow across bytes.
+// The 7-bit fields [7k, 7k + 7) of v, k < 4, into byte k (shifts on the FMA pipe as IMAD.SHL,
+// masks on the ALU: the slicing kernels are ALU-bound).
+__device__ __forceinline__ uint32_t spread4(uint32_t v) {
+  return (v & 0x7fu) | ((v << 1) & 0x7f00u) | ((v << 2) & 0x7f0000u) | ((v << 3) & 0x7f000000u);
+}
+// 4 x 4 byte transpose: o[k] byte i = w[i] byte k.
+__device__ __forceinline__ void transpose4(const uint32_t (&w)[4], uint32_t (&o)[4]) {
+  const uint32_t alo = __byte_perm(w[0], w[1], 0x5140), ahi = __byte_perm(w[0], w[1], 0x7362);
+  const uint32_t blo = __byte_perm(w[2], w[3], 0x5140), bhi = __byte_perm(w[2], w[3], 0x7362);
+  o[0] = __byte_perm(alo, blo, 0x5410);
+  o[1] = __byte_perm(alo, blo, 0x7632);
+  o[2] = __byte_perm(ahi, bhi, 0x5410);
+  o[3] = __byte_perm(ahi, bhi, 0x7632);
+}
+
+// Four consecutive elements -> S words of packed int8 slices (byte i = element i).  The S - 1
+// truncated digits of an element sit in `top` 7 bits apart: groups of four are spread into the
+// bytes of one word per element and byte-transposed across the four elements (8 PRMT per four
+// slice words instead of 12, and no shift + mask per digit); a lone digit and the rounded last one
+// are gathered directly.  Signs as a byte mask (PRMT sign replication of the high bytes), applied
+// per byte: -d = (0x80 - d) ^ 0x80 for d in [0, 127], no borrow across bytes.
 template <int S>
 __device__ __forceinline__ void ozaki_pack4(const double (&x)[4], int e, uint32_t (&w)[S]) {
+  constexpr int ND = S - 1;
   unsigned long long t[4];
   uint32_t l[4];
 #pragma unroll
@@ -304,14 +323,31 @@ __device__ __forceinline__ void ozaki_pack4(const double (&x)[4], int e, uint32_
   asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(h01) : "r"(__double2hiint(x[0])), "r"(__double2hiint(x[1])));
   asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(h23) : "r"(__double2hiint(x[2])), "r"(__double2hiint(x[3])));
   const uint32_t msk = __byte_perm(h01, h23, 0x6420);  // byte i = 0xFF iff x[i] has its sign bit set
+  uint32_t mag[S];
+#pragma unroll
+  for (int g = 0; 4 * g < ND; ++g) {  // digit sl = ND - 1 - 4 g - k is field k of t >> 28 g
+    const int nd = ND - 4 * g < 4 ? ND - 4 * g : 4;
+    if (nd == 1) {
+      uint32_t b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b[i] = (uint32_t)(t[i] >> (28 * g)) & 127u;
+      mag[ND - 1 - 4 * g] =
+          __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    } else {
+      uint32_t wv[4], o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) wv[i] = spread4((uint32_t)(t[i] >> (28 * g)));
+      transpose4(wv, o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < nd) mag[ND - 1 - 4 * g - k] = o[k];
+    }
+  }
+  mag[S - 1] = __byte_perm(__byte_perm(l[0], l[1], 0x0040), __byte_perm(l[2], l[3], 0x0040), 0x5410);
 #pragma unroll
   for (int sl = 0; sl < S; ++sl) {
-    uint32_t b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] = (sl + 1 < S) ? ((uint32_t)(t[i] >> (7 * (S - 2 - sl))) & 127u) : l[i];
-    const uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-    const uint32_t negw = (0x80808080u - word) ^ 0x80808080u;
-    w[sl] = (word & ~msk) | (negw & msk);
+    const uint32_t negw = (0x80808080u - mag[sl]) ^ 0x80808080u;
+    w[sl] = (mag[sl] & ~msk) | (negw & msk);
   }
 }
 
