@@ -1128,9 +1128,29 @@ __global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restri
   const int r0 = (blockIdx.x - ebegin[j]) * rows_per;
   const double* M = nx + N.off + (int64_t)(2 + nxt) * n * n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool v2 = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0;
   for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
-    double sum = 0.0;
-    for (int k = lane; k < n; k += 32) sum += fabs(M[(int64_t)i * n + k] - (i == k ? 1.0 : 0.0));
+    const double* __restrict__ mr = M + (int64_t)i * n;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (v2) {  // 16-byte loads, four independent sums per lane (rows of even n are 16-byte aligned)
+      int k = 2 * lane;
+      for (; k + 65 < n; k += 128) {
+        const double2 a = *reinterpret_cast<const double2*>(mr + k);
+        const double2 b = *reinterpret_cast<const double2*>(mr + k + 64);
+        s0 += fabs(a.x - (i == k ? 1.0 : 0.0));
+        s1 += fabs(a.y - (i == k + 1 ? 1.0 : 0.0));
+        s2 += fabs(b.x - (i == k + 64 ? 1.0 : 0.0));
+        s3 += fabs(b.y - (i == k + 65 ? 1.0 : 0.0));
+      }
+      for (; k + 1 < n; k += 64) {
+        const double2 a = *reinterpret_cast<const double2*>(mr + k);
+        s0 += fabs(a.x - (i == k ? 1.0 : 0.0));
+        s1 += fabs(a.y - (i == k + 1 ? 1.0 : 0.0));
+      }
+    } else {
+      for (int k = lane; k < n; k += 32) s0 += fabs(mr[k] - (i == k ? 1.0 : 0.0));
+    }
+    double sum = (s0 + s1) + (s2 + s3);
     sum = warp_sum(sum);
     if (lane == 0) {
       const unsigned long long b = isnan(sum) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(sum);
