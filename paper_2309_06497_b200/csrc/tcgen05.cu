@@ -773,7 +773,11 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
   __shared__ double col_scale[TN];
   __shared__ int64_t row_off[TM], col_off[TN], mrow_off[TN], mcol_off[TM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned base by pointer arithmetic on the __shared__ array (no integer round trip), so the
+  // compiler keeps the shared address space: tileS accesses are LDS/STS, not generic loads and
+  // stores that it must order against the epilogue's global stores (the store loop had serialised
+  // on exactly that: 13 us per tile)
+  uint8_t* sbase = oz_smem + ((1024u - (smem_u32(oz_smem) & 1023u)) & 1023u);
   double* tileS = reinterpret_cast<double*>(sbase + (size_t)PC::STAGES * PC::STAGE);
 
   if (warp == 0 && lane == 0) {
@@ -964,38 +968,48 @@ __global__ void __launch_bounds__(GEMM_THREADS_P, 1) k_oz_gemm_p(const GemmProbl
       asm volatile("bar.sync 1, 256;" ::: "memory");  // all TMEM reads of buffer b done, tileS complete
       if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
       ++tcount;
-      const bool sym = (P.flags & kGemmSym) != 0;
+      // problem fields in registers: C's stores could alias the problem table as far as the
+      // compiler knows, which made it reload them after every store
+      const int pflags = P.flags, PM = P.M, PN = P.N;
+      const double palpha = P.alpha, pbeta = P.beta;
+      const bool sym = (pflags & kGemmSym) != 0;
       if (T_.ksplit == 1) {
         T* __restrict__ C = static_cast<T*>(P.C);
-        const bool readc = (P.flags & kGemmReadC) != 0;
-        constexpr int PER = 16;  // C values loaded per round trip (all issued before any store)
-        for (int e0 = et; e0 < TM * TN; e0 += PER * 256) {
+        const bool readc = (pflags & kGemmReadC) != 0;
+        const bool mirror = sym && !(pflags & kGemmLowerOnly);
+        // thread et owns column c = et % TN of rows et / TN + 4 u: the column's scale and offset
+        // are loaded once (the tensor core's operand reads keep shared memory busy while the
+        // epilogue runs: fewer LDS per element)
+        constexpr int RSTEP = 256 / TN, PER = 16;  // C values loaded per round trip (before any store)
+        const int c = et % TN, rb = et / TN, gj = tn * TN + c;
+        const double cs = palpha * col_scale[c];
+        const int64_t coff = col_off[c];
+        const bool cin = gj < PN;
+        for (int r0 = rb; r0 < TM; r0 += PER * RSTEP) {
           double cv[PER];
 #pragma unroll
           for (int u = 0; u < PER; ++u) {
-            const int e = e0 + u * 256, r = e / TN, c = e % TN;
-            const int gi = tm * TM + r, gj = tn * TN + c;
-            const bool live = gi < P.M && gj < P.N && !(sym && gi < gj);
-            cv[u] = (readc && live) ? (double)C[row_off[r] + col_off[c]] : 0.0;
+            const int r = r0 + u * RSTEP, gi = tm * TM + r;
+            const bool live = cin && gi < PM && !(sym && gi < gj);
+            cv[u] = (readc && live) ? (double)__ldcg(C + row_off[r] + coff) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < PER; ++u) {
-            const int e = e0 + u * 256, r = e / TN, c = e % TN;
-            const int gi = tm * TM + r, gj = tn * TN + c;
-            if (gi >= P.M || gj >= P.N || (sym && gi < gj)) continue;
-            double val = P.alpha * (tileS[r * LDE + c] * col_scale[c]);
-            if (readc) val = fma(P.beta, cv[u], val);
-            tileS[r * LDE + c] = val;
-            C[row_off[r] + col_off[c]] = (T)val;
+            const int r = r0 + u * RSTEP, gi = tm * TM + r;
+            if (!cin || gi >= PM || (sym && gi < gj)) continue;
+            double val = tileS[r * LDE + c] * cs;
+            if (readc) val = fma(pbeta, cv[u], val);
+            if (mirror) tileS[r * LDE + c] = val;
+            __stcg(C + row_off[r] + coff, (T)val);  // global stores (C is a generic pointer)
           }
         }
-        if (sym && !(P.flags & kGemmLowerOnly)) {
+        if (mirror) {
           asm volatile("bar.sync 1, 256;" ::: "memory");
           for (int e = et; e < TM * TN; e += 256) {
             const int c = e / TM, r = e % TM;
             const int gi = tm * TM + r, gj = tn * TN + c;
-            if (gi >= P.M || gj >= P.N || gi <= gj) continue;
-            C[mrow_off[c] + mcol_off[r]] = (T)tileS[r * LDE + c];
+            if (gi >= PM || gj >= PN || gi <= gj) continue;
+            __stcg(C + mrow_off[c] + mcol_off[r], (T)tileS[r * LDE + c]);
           }
         }
       } else {
