@@ -1037,7 +1037,7 @@ __global__ void __launch_bounds__(256) k_oz_reduce(const GemmProblem* __restrict
                                                    const double* __restrict__ ws) {
   const int r = find64<int32_t>(rbegin, nred, blockIdx.x);
   const int pi = rprob[r];
-  const GemmProblem& P = probs[pi];
+  const GemmProblem P = probs[pi];  // by value: fields stay in registers across the stores to C
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   const OzProb& T_ = tps[pi];
   const int64_t tile = blockIdx.x - rbegin[r];

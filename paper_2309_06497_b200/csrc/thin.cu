@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_thin_kout(const GemmProblem* __restrict
                                                    const int64_t* __restrict__ begin, int nprob,
                                                    const int32_t* __restrict__ mask) {
   const int p = find64(begin, nprob, blockIdx.x);
-  const GemmProblem& P = probs[p];
+  const GemmProblem P = probs[p];  // by value: fields stay in registers across the stores to C
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   // CTA item = (block of R rows, chunk of KOUT_ITEMS columns): wide problems spread over many CTAs
   const int R = max(1, KOUT_ITEMS / P.N);
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k_thin_rank1(const GemmProblem* __restric
                                                     const int64_t* __restrict__ begin, int nprob,
                                                     const int32_t* __restrict__ mask) {
   const int p = find64(begin, nprob, blockIdx.x);
-  const GemmProblem& P = probs[p];
+  const GemmProblem P = probs[p];  // by value: fields stay in registers across the stores to C
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   // lower-only: CTA per row pair (i, N-1-i), i + 1 + N - i = N + 1 elements -- balanced work
   const bool lower = (P.flags & kGemmLowerOnly) != 0;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_thin_kred(const GemmProblem* __restrict
                                                    double* __restrict__ ws) {
   __shared__ double red[TB * TB][8];
   const int p = find64(begin, nprob, blockIdx.x);
-  const GemmProblem& P = probs[p];
+  const GemmProblem P = probs[p];  // by value: fields stay in registers across the stores to C
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   const int chunk = (int)(blockIdx.x - begin[p]);
   const T* __restrict__ A = static_cast<const T*>(P.A);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) k_thin_kred_final(const GemmProblem* __re
                                                          const int32_t* __restrict__ nchunks,
                                                          const double* __restrict__ ws) {
   const int p = blockIdx.x;
-  const GemmProblem& P = probs[p];
+  const GemmProblem P = probs[p];  // by value: fields stay in registers across the stores to C
   if ((P.flags & kGemmMasked) && mask && !mask[P.mask_index]) return;
   const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
   for (int e = w; e < TMAX * TMAX; e += 8) {
