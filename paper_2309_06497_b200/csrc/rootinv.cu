@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_init(const RootJob* __restrict__ jobs, 
                                               double* __restrict__ xs, double in_scale) {
   __shared__ double red[32];
   const int j = find_job(ebegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   const int64_t tot = (int64_t)J.np * J.np;
   double s2 = 0, tr = 0;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(256, 3) k_subsolve(const RootJob* __restrict__
   double* U = smem + NS * LDS_;
   const int j = find_job(pbegin, njobs, blockIdx.x);
   if (!st[j].active) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int pair = blockIdx.x - pbegin[j];
   const int np = J.np;
   double* A = ws + J.ws_off;
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(256, 4) k_apply(const RootJob* __restrict__ jo
   double* X = smem;  // loaded tile, later T = X UQ; U slots are read from L1/L2 directly
   __shared__ int rows[NS];
   const int j = find_job(ibegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   if (J.m == 0 || !st[j].active) return;
   const int item = blockIdx.x - ibegin[j];
   const int h = J.m / 2, np = J.np, r = st[j].round;
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(256) k_rr(const RootJob* __restrict__ jobs, co
                                             double* __restrict__ wv) {
   const int j = find_job(cbegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int k = (blockIdx.x - cbegin[j]) * blockDim.x + threadIdx.x;
   if (k >= J.n) return;
   const double* T = ws + J.ws_off;
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(256) k_symmetrize(const RootJob* __restrict__ 
                                                     double* __restrict__ ws) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   const int64_t tot = (int64_t)J.np * J.np;
   double* A = ws + J.ws_off;
@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(256) k_eig_scale(const RootJob* __restrict__ j
                                                    int32_t* mask, double* __restrict__ wv, double eta, double eps) {
   __shared__ double red[32];
   const int j = blockIdx.x;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   if (st[j].status != kEigOk || st[j].via_newton) {  // (Newton pre-pass jobs already hold X)
     if (threadIdx.x == 0) mask[j] = 0;
     return;
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(256) k_eig_y(const RootJob* __restrict__ jobs,
                                                const double* __restrict__ wv) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   const int64_t tot = (int64_t)J.np * J.np;
   for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(256) k_check_x(const RootJob* __restrict__ job
                                                  const double* __restrict__ xs) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
   const int64_t tot = (int64_t)J.n * J.n;
   int bad = 0;
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(256) k_select(const RootJob* __restrict__ jobs
                                                 const int32_t* __restrict__ ebegin, int njobs,
                                                 const double* __restrict__ xs) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const bool ok = st[j].status == kEigOk;
   if ((!ok && J.has_prev) || st[j].status == kEigSkipped) return;
   const int64_t base = (int64_t)(blockIdx.x - ebegin[j]) * ECH;
@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(256) k_pow_mv(const RootJob* __restrict__ jobs
                                                 double* __restrict__ nx, const int32_t* __restrict__ cand) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (st[j].status != kEigOk || (cand && !cand[j])) return;
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   const int n = J.n;
   const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
   const int rows_per = (n + nch - 1) / nch;
@@ -963,8 +963,8 @@ __global__ void __launch_bounds__(256) k_newton_ub_prep(const RootJob* __restric
                                                         const double* __restrict__ ws, double* __restrict__ nx,
                                                         double eps, const int32_t* __restrict__ cand) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
-  const NewtonJob& N = nj[j];
+  const RootJob J = jobs[j];
+  const NewtonJob N = nj[j];
   const int n = J.n, p = J.root_p;
   const double fro2 = st[j].norm2 + (eps > 0.0 ? 2.0 * eps * st[j].trace + n * eps * eps : 0.0);
   const bool need = st[j].status == kEigOk && (!cand || cand[j]) && sqrt(st[j].norm2) > 0.0 &&
@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(256) k_newton_init(const RootJob* __restrict__
                                                      double eps, const int32_t* __restrict__ cand, int lam_scale) {
   // after k_init (||A||, tr A known): c, X0 = I/c, M0 = (A + eps I)/c^p, Xbest; cand: jobs to run (null: all)
   const int j = find_job(ebegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
+  const RootJob J = jobs[j];
   NewtonJob& N = nj[j];
   if (st[j].status != kEigOk || (cand && !cand[j])) {
     if (threadIdx.x == 0 && blockIdx.x == ebegin[j]) mask[j] = 0;
@@ -1090,7 +1090,7 @@ __global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ 
                                                   double* __restrict__ nx, int cur) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const NewtonJob& N = nj[j];
+  const NewtonJob N = nj[j];
   const int64_t tot = (int64_t)N.n * N.n;
   double* M = nx + N.off + (2 + cur) * tot;
   double* T = nx + N.off + 4 * tot;
@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restri
                                                        unsigned long long* resbits) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!mask[j]) return;
-  const NewtonJob& N = nj[j];
+  const NewtonJob N = nj[j];
   const int n = N.n;
   const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
   const int rows_per = (n + nch - 1) / nch;
@@ -1216,7 +1216,7 @@ __global__ void __launch_bounds__(256) k_newton_copybest(const NewtonJob* __rest
                                                          double* __restrict__ nx, int nxt) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
   if (!improved[j]) return;
-  const NewtonJob& N = nj[j];
+  const NewtonJob N = nj[j];
   const int64_t tot = (int64_t)N.n * N.n;
   const double* X = nx + N.off + nxt * tot;
   double* XB = nx + N.off + 7 * tot;
@@ -1231,8 +1231,8 @@ __global__ void __launch_bounds__(256) k_newton_finish(const RootJob* __restrict
                                                        const double* __restrict__ nx, double* __restrict__ xs,
                                                        const int32_t* __restrict__ cand, int only_converged) {
   const int j = find_job(ebegin, njobs, blockIdx.x);
-  const RootJob& J = jobs[j];
-  const NewtonJob& N = nj[j];
+  const RootJob J = jobs[j];
+  const NewtonJob N = nj[j];
   if (st[j].status != kEigOk || (cand && !cand[j]) || (only_converged && !N.converged)) return;
   const int n = J.n;
   const int64_t tot = (int64_t)n * n;

@@ -205,7 +205,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_oz_rowexp(const OzPackJob* __restrict__ jobs, const int64_t* __restrict__ ebegin,
                                                    int njobs, const int32_t* __restrict__ mask, int32_t* __restrict__ exps) {
   const int j = find64<OzPackJob>(ebegin, njobs, blockIdx.x);
-  const OzPackJob& J = jobs[j];
+  const OzPackJob J = jobs[j];  // by value: no reloads after the plane stores
   if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
   const int64_t u = (int64_t)(blockIdx.x - ebegin[j]) * 256 + threadIdx.x;
   if (J.fexp != kNoFixedExp) {  // fixed exponent: one thread per row writes it
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(PACK_UNITS) k_oz_pack(const OzPackJob* __restr
                                                         const int32_t* __restrict__ mask,
                                                         const int32_t* __restrict__ exps, int8_t* __restrict__ arena) {
   const int j = find64<OzPackJob>(pbegin, njobs, blockIdx.x);
-  const OzPackJob& J = jobs[j];
+  const OzPackJob J = jobs[j];  // by value: no reloads after the plane stores
   if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
   const int64_t u = (int64_t)(blockIdx.x - pbegin[j]) * PACK_UNITS + threadIdx.x;
   if (u >= J.units) return;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(256) k_oz_pack_rows(const OzPackJob* __restric
   __shared__ double rmax[8][PACK_CORES * 8 + 1];
   __shared__ int rexp[PACK_CORES * 8];
   const int j = find64<OzPackJob>(cbegin, njobs, blockIdx.x);
-  const OzPackJob& J = jobs[j];
+  const OzPackJob J = jobs[j];  // by value: no reloads after the plane stores
   if (J.mask_index >= 0 && mask && !mask[J.mask_index]) return;
   const int core0 = (int)(blockIdx.x - cbegin[j]) * PACK_CORES;
   const int ncores = min(PACK_CORES, J.rc - core0);
