@@ -1098,11 +1098,39 @@ __global__ void __launch_bounds__(256) k_newton_t(const NewtonJob* __restrict__ 
   if (N.scale != 1.0) {
     // scaled step: M <- s M, X <- s^(1/p) X keeps M = X^p (A + eps I); lifts the small eigenvalues
     // of M (the linear phase) while the spectrum stays inside (0, p + 1) (s max(M) <= s < 2)
-    double* X = nx + N.off + (int64_t)cur * tot;
+    double* __restrict__ X = nx + N.off + (int64_t)cur * tot;
+    double* __restrict__ Mr = M;
     const double s = N.scale, sx = pow(s, 1.0 / N.p);
-    for (int64_t e = base + threadIdx.x; e < base + ECH && e < tot; e += blockDim.x) {
-      M[e] *= s;
-      X[e] *= sx;
+    const int64_t end = base + ECH < tot ? base + ECH : tot;
+    if (((base | end) & 1) == 0 && ((reinterpret_cast<uintptr_t>(Mr) | reinterpret_cast<uintptr_t>(X)) & 15) == 0) {
+      // 16-byte pairs, four pairs of each matrix loaded before their stores
+      double2* __restrict__ M2 = reinterpret_cast<double2*>(Mr);
+      double2* __restrict__ X2 = reinterpret_cast<double2*>(X);
+      const int64_t q0 = base / 2, q1 = end / 2;
+      for (int64_t q = q0 + threadIdx.x; q < q1; q += 4 * blockDim.x) {
+        double2 m[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t qq = q + (int64_t)u * blockDim.x;
+          if (qq < q1) {
+            m[u] = M2[qq];
+            x[u] = X2[qq];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t qq = q + (int64_t)u * blockDim.x;
+          if (qq < q1) {
+            M2[qq] = make_double2(m[u].x * s, m[u].y * s);
+            X2[qq] = make_double2(x[u].x * sx, x[u].y * sx);
+          }
+        }
+      }
+    } else {
+      for (int64_t e = base + threadIdx.x; e < end; e += blockDim.x) {
+        Mr[e] *= s;
+        X[e] *= sx;
+      }
     }
   }
   if (N.tpack) return;  // T is packed straight from M by the X T / T T launch
