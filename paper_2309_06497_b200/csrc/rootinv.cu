@@ -890,18 +890,36 @@ __global__ void __launch_bounds__(256) k_pow_mv(const RootJob* __restrict__ jobs
   const RootJob J = jobs[j];
   const int n = J.n;
   const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
-  const int rows_per = (n + nch - 1) / nch;
-  const int r0 = (blockIdx.x - ebegin[j]) * rows_per;
   const double* A = ws + J.ws_off;
   const double* x = nx + nj[j].off + 5 * (int64_t)n * n;
   double* y = const_cast<double*>(x) + n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
+  // rows over every warp of the job's CTAs (its n^2 / ECH element chunks outnumber n / 8: with
+  // rows split per CTA most warps idled and the row streams were too few to fill HBM)
+  for (int i = (blockIdx.x - ebegin[j]) * 8 + warp; i < n; i += nch * 8) {
     const double* __restrict__ ar = A + (int64_t)i * J.np;
     // 16-byte loads, four independent chains per lane (the row is np-padded and 16-byte aligned)
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int k = 2 * lane;
     if ((J.np & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+      for (; k + 192 + 1 < n; k += 256) {  // 64 B of the row in flight per lane
+        const double2 a0 = *reinterpret_cast<const double2*>(ar + k);
+        const double2 a1 = *reinterpret_cast<const double2*>(ar + k + 64);
+        const double2 a2 = *reinterpret_cast<const double2*>(ar + k + 128);
+        const double2 a3 = *reinterpret_cast<const double2*>(ar + k + 192);
+        const double2 x0 = *reinterpret_cast<const double2*>(x + k);
+        const double2 x1 = *reinterpret_cast<const double2*>(x + k + 64);
+        const double2 x2 = *reinterpret_cast<const double2*>(x + k + 128);
+        const double2 x3 = *reinterpret_cast<const double2*>(x + k + 192);
+        s0 = fma(a0.x, x0.x, s0);
+        s1 = fma(a0.y, x0.y, s1);
+        s2 = fma(a1.x, x1.x, s2);
+        s3 = fma(a1.y, x1.y, s3);
+        s0 = fma(a2.x, x2.x, s0);
+        s1 = fma(a2.y, x2.y, s1);
+        s2 = fma(a3.x, x3.x, s2);
+        s3 = fma(a3.y, x3.y, s3);
+      }
       for (; k + 64 + 1 < n; k += 128) {
         const double2 a0 = *reinterpret_cast<const double2*>(ar + k);
         const double2 x0 = *reinterpret_cast<const double2*>(x + k);
@@ -1152,16 +1170,28 @@ __global__ void __launch_bounds__(256) k_newton_rowmax(const NewtonJob* __restri
   const NewtonJob N = nj[j];
   const int n = N.n;
   const int nch = (j + 1 < njobs ? ebegin[j + 1] : echunks) - ebegin[j];
-  const int rows_per = (n + nch - 1) / nch;
-  const int r0 = (blockIdx.x - ebegin[j]) * rows_per;
   const double* M = nx + N.off + (int64_t)(2 + nxt) * n * n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool v2 = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0;
-  for (int i = r0 + warp; i < min(n, r0 + rows_per); i += 8) {
+  for (int i = (blockIdx.x - ebegin[j]) * 8 + warp; i < n; i += nch * 8) {  // every warp a row
     const double* __restrict__ mr = M + (int64_t)i * n;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (v2) {  // 16-byte loads, four independent sums per lane (rows of even n are 16-byte aligned)
       int k = 2 * lane;
+      for (; k + 193 < n; k += 256) {  // 64 B of the row in flight per lane
+        const double2 a = *reinterpret_cast<const double2*>(mr + k);
+        const double2 b = *reinterpret_cast<const double2*>(mr + k + 64);
+        const double2 c = *reinterpret_cast<const double2*>(mr + k + 128);
+        const double2 d = *reinterpret_cast<const double2*>(mr + k + 192);
+        s0 += fabs(a.x - (i == k ? 1.0 : 0.0));
+        s1 += fabs(a.y - (i == k + 1 ? 1.0 : 0.0));
+        s2 += fabs(b.x - (i == k + 64 ? 1.0 : 0.0));
+        s3 += fabs(b.y - (i == k + 65 ? 1.0 : 0.0));
+        s0 += fabs(c.x - (i == k + 128 ? 1.0 : 0.0));
+        s1 += fabs(c.y - (i == k + 129 ? 1.0 : 0.0));
+        s2 += fabs(d.x - (i == k + 192 ? 1.0 : 0.0));
+        s3 += fabs(d.y - (i == k + 193 ? 1.0 : 0.0));
+      }
       for (; k + 65 < n; k += 128) {
         const double2 a = *reinterpret_cast<const double2*>(mr + k);
         const double2 b = *reinterpret_cast<const double2*>(mr + k + 64);
