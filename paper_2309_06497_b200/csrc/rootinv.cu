@@ -271,12 +271,18 @@ __device__ int cta_jacobi64_rounds(T* S, T* U, T tol_abs, T tol_null) {
   constexpr int NROUNDS = CROSS ? HB : NS - 1;
   __shared__ T2 pcs[NS / 2];
   __shared__ T pt[NS / 2], papq[NS / 2], papp[NS / 2], paqq[NS / 2];
-  __shared__ int rot_round, rot_any;
+  // per-round "any rotation" flag, double-buffered by round parity: a round without rotations
+  // skips its trailing barrier, so the flag the next round clears must not be the one still being
+  // read (compute-sanitizer racecheck: write/read race on a single flag)
+  __shared__ int rot_flag[2], rot_any;
   const int tid = threadIdx.x;
   for (int e = tid; e < NS * NS; e += 256) U[(e >> 6) * LDS_ + (e & 63)] = ((e >> 6) == (e & 63)) ? T(1) : T(0);
-  if (tid == 0) rot_any = 0;
+  if (tid == 0) {
+    rot_any = 0;
+    rot_flag[0] = 0;
+    rot_flag[1] = 0;
+  }
   for (int r = 0; r < NROUNDS; ++r) {
-    if (tid == 0) rot_round = 0;
     __syncthreads();
     if (tid < NS / 2) {
       int a, b;
@@ -293,7 +299,7 @@ __device__ int cta_jacobi64_rounds(T* S, T* U, T tol_abs, T tol_null) {
         t = e * copysign(T(1), d) / (fabs(d) + h);
         c = eig_rsqrt(fma(t, t, T(1)));
         sn = t * c;
-        rot_round = 1;
+        rot_flag[r & 1] = 1;
       }
       T2 cs;
       cs.x = c;
@@ -305,7 +311,10 @@ __device__ int cta_jacobi64_rounds(T* S, T* U, T tol_abs, T tol_null) {
       paqq[tid] = aqq;
     }
     __syncthreads();
-    if (!rot_round) continue;  // uniform: every thread read it after the barrier
+    const int rot = rot_flag[r & 1];
+    // the next round's flag was last read before this round's first barrier: clear it now
+    if (tid == 0) rot_flag[(r + 1) & 1] = 0;
+    if (!rot) continue;  // uniform: every thread read it after the barrier
     // S <- J^T S J by 2x2 blocks (pair i rows, pair j columns)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
